@@ -1,0 +1,212 @@
+"""CPU oracle for mdps_eval_diff — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+--impl reference) may import this package.  The product path
+(paper_2012_06607_b200/) never imports it, and it shares no code with the
+CUDA library.  The arithmetic lives in mdoracle.c (see its header for the
+definitions it follows and the PAPER.md passages it cites); this module only
+builds it and marshals numpy arrays.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mdoracle.c")
+_LIB = os.path.join(_HERE, "libmdoracle.so")
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-pthread", "-Wall"]
+MAXL = 16
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle/libmdoracle.so (gcc, no fast-math, no FP contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        P = ctypes.POINTER
+        d, i32, ll = ctypes.c_double, ctypes.c_int, ctypes.c_longlong
+        L.mdo_round.argtypes = [P(d), i32, i32, P(d)]
+        for f in ("mdo_add", "mdo_mul", "mdo_div"):
+            getattr(L, f).argtypes = [P(d), P(d), i32, P(d)]
+        L.mdo_sqrt.argtypes = [P(d), i32, P(d)]
+        L.mdo_norm2.argtypes = [P(d), i32, i32, P(d)]
+        L.mdo_series_mul.argtypes = [P(d), P(d), i32, i32, P(d), P(ll)]
+        L.mdo_series_add.argtypes = [P(d), P(d), i32, i32, P(d)]
+        L.mdo_series_inv.argtypes = [P(d), i32, i32, P(d)]
+        L.mdo_eval_entries.argtypes = [i32, i32, P(i32), P(i32), P(i32), P(i32), P(d), P(d), i32, i32,
+                                       i32, P(i32), P(i32), P(d), i32, P(ll)]
+        L.mdo_series_err.argtypes = [P(d), P(d), i32, i32, i32, P(d)]
+        _lib = L
+    return _lib
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ip(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise ArithmeticError(f"oracle {what} failed (rc={rc})")
+
+
+# ---- multiple-double numbers (real, L limbs) ------------------------------------
+def md_round(values: Sequence[float], L: int) -> np.ndarray:
+    """Greedy L-limb round-to-nearest of the exact sum of `values`."""
+    v = _f64(values).ravel()
+    out = np.zeros(L)
+    _check(lib().mdo_round(_dp(v), v.size, L, _dp(out)), "round")
+    return out
+
+
+def _binop(name: str, a, b) -> np.ndarray:
+    a, b = _f64(a), _f64(b)
+    assert a.shape == b.shape and a.ndim == 1
+    out = np.zeros_like(a)
+    _check(getattr(lib(), name)(_dp(a), _dp(b), a.size, _dp(out)), name)
+    return out
+
+
+def md_add(a, b):
+    return _binop("mdo_add", a, b)
+
+
+def md_mul(a, b):
+    return _binop("mdo_mul", a, b)
+
+
+def md_div(a, b):
+    return _binop("mdo_div", a, b)
+
+
+def md_sqrt(a) -> np.ndarray:
+    a = _f64(a)
+    out = np.zeros_like(a)
+    _check(lib().mdo_sqrt(_dp(a), a.size, _dp(out)), "sqrt")
+    return out
+
+
+def md_norm2(v) -> np.ndarray:
+    """2-norm of a complex md vector v[count][2][L]."""
+    v = _f64(v)
+    count, two, L = v.shape
+    assert two == 2
+    out = np.zeros(L)
+    _check(lib().mdo_norm2(_dp(v), count, L, _dp(out)), "norm2")
+    return out
+
+
+# ---- truncated power series [2][L][D] ------------------------------------------
+def series_mul(x, y, counts: Optional[np.ndarray] = None) -> np.ndarray:
+    x, y = _f64(x), _f64(y)
+    _, L, D = x.shape
+    z = np.zeros_like(x)
+    cp = None
+    if counts is not None:
+        assert counts.dtype == np.int64 and counts.size >= 2
+        cp = counts.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong))
+    _check(lib().mdo_series_mul(_dp(x), _dp(y), D, L, _dp(z), cp), "series_mul")
+    return z
+
+
+def series_add(x, y) -> np.ndarray:
+    """x + y for series [..., 2, L, D] (any leading shape)."""
+    x, y = _f64(x), _f64(y)
+    assert x.shape == y.shape
+    _, L, D = x.shape[-3:]
+    xf, yf = x.reshape(-1, 2, L, D), y.reshape(-1, 2, L, D)
+    z = np.zeros_like(xf)
+    for t in range(xf.shape[0]):
+        zt = np.zeros((2, L, D))
+        _check(lib().mdo_series_add(_dp(np.ascontiguousarray(xf[t])), _dp(np.ascontiguousarray(yf[t])),
+                                    D, L, _dp(zt)), "series_add")
+        z[t] = zt
+    return z.reshape(x.shape)
+
+
+def series_inv(x) -> np.ndarray:
+    x = _f64(x)
+    _, L, D = x.shape
+    y = np.zeros_like(x)
+    _check(lib().mdo_series_inv(_dp(x), D, L, _dp(y)), "series_inv")
+    return y
+
+
+# ---- eval/diff -------------------------------------------------------------------
+def eval_entries(si, entries: Sequence[Tuple[int, int]], nthreads: Optional[int] = None,
+                 limbs: Optional[int] = None) -> Tuple[np.ndarray, int]:
+    """Oracle values (col < 0) and Jacobian entries (row, col) of system `si`
+    (an mdinputs.SystemInputs).  Returns (out[n_entries][2][L][D], products).
+
+    `limbs` > si.limbs evaluates the same inputs (zero-padded limbs) at a
+    higher precision (the oracle's self-consistency pin)."""
+    L = limbs or si.limbs
+    coeffs, x = si.coeffs, si.x
+    if L != si.limbs:
+        assert L > si.limbs
+        pad = [(0, 0), (0, 0), (0, L - si.limbs), (0, 0)]
+        coeffs, x = np.pad(coeffs, pad), np.pad(x, pad)
+    coeffs, x = _f64(coeffs), _f64(x)
+    rows = _i32([e[0] for e in entries])
+    cols = _i32([e[1] for e in entries])
+    out = np.zeros((len(entries), 2, L, si.degree + 1))
+    prods = ctypes.c_longlong(0)
+    n_polys = int(si.poly_ptr.shape[0] - 1)
+    nt = nthreads or os.cpu_count() or 1
+    rc = lib().mdo_eval_entries(n_polys, si.n, _ip(_i32(si.poly_ptr)), _ip(_i32(si.mono_ptr)),
+                                _ip(_i32(si.vars)), _ip(_i32(si.exps)), _dp(coeffs), _dp(x),
+                                si.degree, L, len(entries), _ip(rows), _ip(cols), _dp(out), nt,
+                                ctypes.byref(prods))
+    _check(rc, "eval_entries")
+    return out, int(prods.value)
+
+
+def eval_diff(si, nthreads: Optional[int] = None, limbs: Optional[int] = None):
+    """Full naive evaluation: (values[n_polys][2][L][D], jac[n_polys][n][2][L][D], products)."""
+    n_polys = int(si.poly_ptr.shape[0] - 1)
+    entries = [(i, -1) for i in range(n_polys)] + [(i, j) for i in range(n_polys) for j in range(si.n)]
+    out, prods = eval_entries(si, entries, nthreads, limbs)
+    vals = out[:n_polys]
+    jac = out[n_polys:].reshape((n_polys, si.n) + out.shape[1:])
+    return vals, jac, prods
+
+
+def series_err(a, b) -> np.ndarray:
+    """Per-series error e_s = max_k |a-b| / max(max_k |b|, 1), differences exact.
+    a, b: [..., 2, L, D]; returns an array of the leading shape."""
+    a, b = _f64(a), _f64(b)
+    assert a.shape == b.shape
+    lead = a.shape[:-3]
+    _, L, D = a.shape[-3:]
+    count = int(np.prod(lead)) if lead else 1
+    err = np.zeros(count)
+    _check(lib().mdo_series_err(_dp(a), _dp(b), count, D, L, _dp(err)), "series_err")
+    return err.reshape(lead)
