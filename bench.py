@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""bench.py — mdps_eval_diff throughput on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config od]
+                  [--impl mdps|reference] [--algo 0|1|2] [--no-cpu-baseline]
+
+A step is one mdps_eval_diff of the whole workload (every product level and
+the addition jobs) with the inputs resident in HBM.  Default workload:
+BASELINE.json configs[2] (octo double: n = 64, 128 monomials of 8..16
+variables, degree 63) — the configuration the north_star's >= 50% FP64
+roofline target is quoted on.  Under torchrun each rank runs an independent
+replica on its own GPU (the path needs no exchange: "replicas only",
+DESIGN.md); time is the max over ranks.  --impl reference times the CPU
+oracle (the reference arm of this tier) on a bounded sample of the same
+workload; rank 0 only.
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import mdinputs  # noqa: E402
+
+CONFIG_TEXT = {
+    "dd": "BASELINE configs[0]: double double, n=8, 16 monomials x 3 vars, degree 15",
+    "qd": "BASELINE configs[1]: quad double, n=32, 64 monomials x 4..8 vars, exponents {1,2}, degree 31",
+    "od": "BASELINE configs[2]: octo double, n=64, 128 monomials x 8..16 vars, degree 63",
+    "deca": "BASELINE configs[3]: deca double, n=128, 128 monomials x 16 vars, degree 63",
+}
+TOL = {2: 1e-29, 3: 1e-45, 4: 1e-61, 5: 1e-77, 8: 1e-124, 10: 1e-156}
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def workload(name: str):
+    if name.startswith("sweep_"):
+        _, d, L = name.split("_")
+        return mdinputs.sweep_cell(int(d[1:]), int(L[1:]))
+    return mdinputs.make_config(name)
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.dev)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = []
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(f[1]), smmax=float(f[2]), power=float(f[3]) if f[3] not in ("[N/A]", "") else 0.0,
+                                 hw=f[5], hwth=f[6], swth=f[7], swpc=f[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        reasons = set()
+        for r in rows:
+            for key, name in (("hw", "hw_slowdown"), ("hwth", "hw_thermal_slowdown"),
+                              ("swth", "sw_thermal_slowdown"), ("swpc", "sw_power_cap")):
+                if r[key].lower().startswith("active"):
+                    reasons.add(name)
+        loaded = [r["sm"] for r in rows if r["power"] > 200.0] or [r["sm"] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r["smmax"] for r in rows),
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w_max": max(r["power"] for r in rows)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_baseline(si, budget_entries: int = 8):
+    """The oracle as it stands on a bounded sample of the same workload:
+    f_0 and the first nonzero Jacobian entries of row 0, one worker per entry
+    (the paper's job queue), naive per-monomial products."""
+    import oracle
+    entries = mdinputs.first_entries(si, budget_entries)
+    cores = min(os.cpu_count() or 1, len(entries))
+    t0 = time.perf_counter()
+    _, prods = oracle.eval_entries(si, entries, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": prods / dt, "unit": "products/s", "cores": cores, "kind": "oracle",
+            "sample": f"{len(entries)} outputs of {si.name} (f_0 and row-0 Jacobian entries), "
+                      f"{prods} naive series products in {dt:.1f} s",
+            "seconds": dt}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle, bounded sample per step (rank 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    si = workload(args.config)
+    entries = mdinputs.first_entries(si, 1 + args.steps + args.warmup)[1:]  # one Jacobian entry per step
+    cores = 1
+    for e in entries[:args.warmup]:
+        oracle.eval_entries(si, [e], nthreads=1)
+    t0 = time.perf_counter()
+    prods = 0
+    for e in entries[args.warmup:args.warmup + args.steps]:
+        _, p = oracle.eval_entries(si, [e], nthreads=1)
+        prods += p
+    dt = time.perf_counter() - t0
+    value = prods / dt
+    line = {"impl": "reference", "metric": "series products/s", "value": value, "unit": "products/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * dt / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64 (exact superaccumulator)", "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT.get(args.config, args.config), "name": args.config},
+            "cpu_baseline": {"value": value, "unit": "products/s", "cores": cores, "kind": "oracle",
+                             "sample": f"one Jacobian entry of {si.name} per step (naive products)"},
+            "e2e": {"value": value, "unit": "products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="od")
+    ap.add_argument("--impl", default="mdps", choices=["mdps", "reference"])
+    ap.add_argument("--algo", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "mdps" else args.warmup
+
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_2012_06607_b200 as mdps
+    from paper_2012_06607_b200 import build as mdps_build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if rank == 0:
+        mdps_build.build()
+    if dist:
+        dist.barrier()
+    mdps.lib()
+
+    si = workload(args.config)
+    peaks = load_peaks()
+    sys_ = mdps.System.from_inputs(si, algo=args.algo)
+    st = sys_.stats()
+    stream = torch.cuda.current_stream()
+    x = torch.from_numpy(si.x).cuda()
+    vals = torch.empty((si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
+    jac = torch.empty((si.n, si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+
+    fp64_peak_measured = mdps.fp64_peak(20000)
+
+    for _ in range(args.warmup):
+        sys_.eval_diff(x, vals, jac)
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
+                           else local_rank)
+    sys_.set_timing(True)
+    sys_.timing(reset=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for s in range(args.steps):
+        flush.zero_()                      # outside the timed events: L2 holds no inputs
+        ev[s][0].record(stream)
+        sys_.eval_diff(x, vals, jac)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    sys_.set_timing(False)
+    tim = sys_.timing(reset=True)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    products_per_step = st["products"]
+    value = products_per_step * world * args.steps / (ms * 1e-3)
+    fp64_per_s = st["fp64_ops_total"] * world * args.steps / (ms * 1e-3)
+
+    # dominant kernel: the product jobs (all levels), live CUDA-event durations
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    peak_nominal = n_sm * 64 * sm_max * 1e6  # FP64 instr/s: 64 FP64 lanes per SM
+    conv_launch_ms = tim["conv_ms"] / max(1, tim["conv_launches"])
+    conv_ops_per_launch = st["fp64_ops_conv"] * args.steps / max(1, tim["conv_launches"])
+    achieved = st["fp64_ops_conv"] * args.steps / (tim["conv_ms"] * 1e-3) if tim["conv_ms"] > 0 else 0.0
+    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_nominal / 1e12,
+                "unit": "T FP64 instr/s (DADD/DMUL/DFMA = 1)", "frac": achieved / peak_nominal,
+                "traffic": None,
+                "peak_measured_in_run": fp64_peak_measured / 1e12,
+                "frac_of_measured": achieved / fp64_peak_measured if fp64_peak_measured > 0 else None,
+                "kernel": "conv_dig_kernel" if st["algo"] == 2 else "conv_eft_kernel",
+                "ops_per_launch": conv_ops_per_launch, "avg_launch_ms": conv_launch_ms,
+                "share_of_step": tim["conv_ms"] / max(1e-9, tim["conv_ms"] + tim["accum_ms"] + tim["convert_ms"]),
+                "peak_source": f"{n_sm} SMs x 64 FP64 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
+    tprof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_algo{st['algo']}.json")
+    if os.path.exists(tprof):
+        try:
+            roofline["traffic"] = json.load(open(tprof))["dram_bytes_per_launch"]
+        except Exception:
+            pass
+
+    # end to end through the public C API with HOST buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.from_numpy(si.x).pin_memory()
+        hv = torch.empty(tuple(vals.shape), dtype=torch.float64).pin_memory()
+        hj = torch.empty(tuple(jac.shape), dtype=torch.float64).pin_memory()
+        h = sys_.handle
+        lib = mdps.lib()
+        sh = stream.cuda_stream
+        lib.mdps_eval_diff_host(h, hx.data_ptr(), hv.data_ptr(), hj.data_ptr(), sh)  # warm (allocates)
+        e2e_steps = max(3, args.steps // 2)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            rc = lib.mdps_eval_diff_host(h, hx.data_ptr(), hv.data_ptr(), hj.data_ptr(), sh)
+            if rc != 0:
+                raise RuntimeError(mdps.mdps_last_error())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": products_per_step * world * e2e_steps / (ems * 1e-3), "unit": "products/s",
+               "h2d_bytes_per_step": int(hx.numel() * 8), "d2h_bytes_per_step": int((hv.numel() + hj.numel()) * 8),
+               "steps": e2e_steps, "ms_per_step": ems / e2e_steps, "api": "mdps_eval_diff_host (pinned host buffers)"}
+        # the host-buffer outputs must equal the device path's outputs
+        if not (torch.equal(hv, vals.cpu()) and torch.equal(hj, jac.cpu())):
+            raise RuntimeError("e2e outputs differ from the device-path outputs")
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(si)
+
+    if rank == 0:
+        line = {
+            "metric": "series products/s (mdps_eval_diff)",
+            "value": value, "unit": "products/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT.get(args.config, args.config), "name": args.config,
+                       "n": si.n, "monomials": si.M, "degree": si.degree, "limbs": si.limbs,
+                       "algo": {1: "eft", 2: "digits"}[st["algo"]], "digits": st["digits"],
+                       "products_per_step": products_per_step, "levels": st["levels"],
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "256 MiB buffer written between timed steps (L2 flushed)",
+                       "seed": mdinputs.CONFIGS[si.name].seed if si.name in mdinputs.CONFIGS else None,
+                       "input_sha256": si.sha256()[:16]},
+            "fp64_ops_per_s": fp64_per_s,
+            "fp64_ops_per_step": st["fp64_ops_total"],
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": st["launches"] * args.steps,
+            "kernel_ms_per_step": {"conv": tim["conv_ms"] / args.steps, "accum": tim["accum_ms"] / args.steps,
+                                   "convert": tim["convert_ms"] / args.steps},
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    sys_.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,138 @@
+/*
+ * libmdps.h — C ABI of the B200-native evaluation and differentiation of a
+ * polynomial system at a vector of truncated power series in complex
+ * multiple-double precision (arXiv 2012.06607, "Parallel Software to Offset
+ * the Cost of Higher Precision", J. Verschelde).
+ *
+ * The operation (§4): given a system
+ *   f = (f_0, ..., f_{N-1}) of polynomials in x = (x_0, ..., x_{n-1}) whose
+ * coefficients are truncated power series in t, and a point x(t) whose
+ * components are truncated power series, compute
+ *   values[i]      = f_i(x(t))                 mod t^(degree+1)
+ *   jacobian[i][j] = (d f_i / d x_j)(x(t))     mod t^(degree+1)
+ * with every coefficient a complex multiple-double number of `limbs` doubles
+ * (§2).  Series products are truncated convolutions
+ * z_k = sum_{i<=k} x_i y_{k-i} (§3); the Jacobian is
+ * computed by algorithmic differentiation at about 3x the cost of the
+ * evaluation: forward, backward and cross products per
+ * monomial.  In v1, N must equal n (square systems).
+ *
+ * Series layout (all series arguments): float64, [part][limb][coefficient]
+ * per series — part 0 = real, 1 = imaginary; limb 0 most significant
+ * (non-overlapping expansion); coefficient k = 0..degree (D = degree+1).
+ * One series is 2*limbs*D doubles; arrays of series are contiguous.
+ *
+ * Threading: calls on different systems are independent.  One eval_diff may
+ * be in flight per system (the system owns its workspace).
+ */
+#ifndef LIBMDPS_H
+#define LIBMDPS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDPS_OK 0
+#define MDPS_EINVAL (-1)   /* invalid argument (see mdps_last_error) */
+#define MDPS_ENOMEM (-2)   /* device or host allocation failed */
+#define MDPS_ECUDA (-3)    /* a CUDA call or kernel launch failed */
+
+/* A cudaStream_t (the same handle type; this header needs no CUDA headers). */
+typedef struct CUstream_st *mdps_stream_t;
+
+typedef struct mdps_system mdps_system; /* opaque; owns device memory */
+
+/* Supports of the system in CSR form (HOST pointers, read during create only).
+ * Polynomial i has monomials r in [poly_ptr[i], poly_ptr[i+1]); monomial r has
+ * variables vars[mono_ptr[r] .. mono_ptr[r+1]) — indices in [0, n), distinct
+ * within a monomial, in any order.  An empty monomial is a constant term.
+ * Duplicate monomials within a polynomial are allowed (they are summed). */
+typedef struct {
+    int32_t n_polys;          /* must equal n in v1 */
+    const int32_t *poly_ptr;  /* [n_polys+1], non-decreasing, poly_ptr[0] = 0 */
+    const int32_t *mono_ptr;  /* [M+1], non-decreasing, mono_ptr[0] = 0, M = poly_ptr[n_polys] */
+    const int32_t *vars;      /* [nnz], nnz = mono_ptr[M] */
+} mdps_supports;
+
+/* Convolution algorithm for the product jobs. */
+#define MDPS_ALGO_AUTO 0     /* digits for every limb count (default) */
+#define MDPS_ALGO_EFT 1      /* limb planes: TwoProd + TwoSum level bins */
+#define MDPS_ALGO_DIGITS 2   /* 22-bit digit planes, exact FP64 FMA products */
+
+typedef struct {
+    int32_t algo;        /* MDPS_ALGO_* */
+    int32_t use_graph;   /* 1: capture the launch sequence in a CUDA graph,
+                            re-captured when the pointers or stream change */
+} mdps_options;
+
+/* Create a system.  exponents: HOST [nnz] aligned with
+ * vars, each >= 1.  coefficients: HOST [M][2][limbs][degree+1], the series
+ * coefficient of each monomial.  n >= 1, 0 <= degree <= 255,
+ * limbs in {2,3,4,5,8,10}.  All host arrays are deep-copied; the caller may
+ * free them on return.  Returns NULL on error (mdps_last_error() says why):
+ * invalid sizes, NULL pointers, n_polys != n, non-monotone CSR, a variable
+ * out of range or repeated within a monomial, an exponent < 1, or a failed
+ * allocation.  Variables are sorted per monomial internally.  Requires a
+ * current CUDA device (the device of the caller's current context). */
+mdps_system *mdps_system_create(const mdps_supports *supports, const int32_t *exponents,
+                                const double *coefficients, int32_t n, int32_t degree,
+                                int32_t limbs);
+
+/* As mdps_system_create, with options (NULL = defaults). */
+mdps_system *mdps_system_create_ex(const mdps_supports *supports, const int32_t *exponents,
+                                   const double *coefficients, int32_t n, int32_t degree,
+                                   int32_t limbs, const mdps_options *options);
+
+/* Evaluate and differentiate (the hot path).  DEVICE pointers:
+ *   series_in    [n][2][limbs][D]      read only
+ *   values_out   [n][2][limbs][D]      fully overwritten
+ *   jacobian_out [n][n][2][limbs][D]   fully overwritten; row i = polynomial,
+ *                                      column j = variable; entries with no
+ *                                      monomial of f_i containing x_j are 0.
+ * Asynchronous: enqueues kernels on `stream` (NULL = legacy default stream)
+ * and returns.  The outputs must not alias each other or series_in.
+ * Returns MDPS_OK, MDPS_EINVAL (NULL/aliased pointers) or MDPS_ECUDA (a
+ * launch failed); asynchronous faults surface at the caller's next
+ * synchronisation.  Non-finite inputs propagate; nothing is checked on the
+ * hot path. */
+int mdps_eval_diff(mdps_system *sys, const double *series_in, double *values_out,
+                   double *jacobian_out, mdps_stream_t stream);
+
+/* End-to-end variant with HOST buffers (same layouts): copies series_in to the
+ * device, evaluates, copies both outputs back and synchronises `stream`.
+ * Host buffers may be pageable or pinned (pinned is faster). */
+int mdps_eval_diff_host(mdps_system *sys, const double *series_in_host, double *values_host,
+                        double *jacobian_host, mdps_stream_t stream);
+
+/* Frees all device memory of the system (synchronises the device first). */
+void mdps_system_destroy(mdps_system *sys);
+
+/* Thread-local message for the last failure of a call on this thread. */
+const char *mdps_last_error(void);
+
+typedef struct {
+    int64_t products;          /* series product jobs per eval (forward/backward/cross/common) */
+    int64_t add_terms;         /* series added by the accumulation jobs */
+    int64_t fp64_ops_conv;     /* algorithmic FP64 instructions of the product jobs */
+    int64_t fp64_ops_total;    /* ... of the whole eval (conversions, products, sums) */
+    int64_t compulsory_bytes;  /* inputs + coefficients + outputs, bytes */
+    int32_t levels;            /* product levels (one launch each) */
+    int32_t algo;              /* MDPS_ALGO_EFT or MDPS_ALGO_DIGITS */
+    int32_t digits;            /* digits per part (digits algo), else 0 */
+    int32_t launches;          /* kernel launches per eval */
+    size_t workspace_bytes;    /* device memory owned by the system */
+} mdps_stats;
+
+/* Statistics of a system (for the measurement). */
+int mdps_system_stats(const mdps_system *sys, mdps_stats *out);
+
+/* Per-level job counts (levels entries) for diagnostics; returns levels or <0. */
+int mdps_system_level_jobs(const mdps_system *sys, int64_t *jobs_per_level, int32_t max_levels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LIBMDPS_H */

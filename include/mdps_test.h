@@ -1,0 +1,64 @@
+/*
+ * mdps_test.h — diagnostic entry points of libmdps: the device kernels of the
+ * hot path exposed one at a time for unit parity tests and measurement.
+ * Same conventions as libmdps.h (layouts, error codes, asynchronous on
+ * `stream`, DEVICE pointers unless stated).
+ */
+#ifndef MDPS_TEST_H
+#define MDPS_TEST_H
+
+#include "libmdps.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* count independent truncated products z[c] = x[c] * y[c] mod t^(degree+1)
+ * with the product kernel of `algo` (MDPS_ALGO_EFT or
+ * MDPS_ALGO_DIGITS), the same launch configuration as mdps_eval_diff.
+ * x, y, z: [count][2][limbs][degree+1]; z must not alias x or y. */
+int mdps_test_series_mul(const double *x, const double *y, double *z, int32_t count,
+                         int32_t degree, int32_t limbs, int32_t algo, mdps_stream_t stream);
+
+/* Device md arithmetic on arrays of real md numbers a[count][limbs],
+ * b[count][limbs] -> c[count][limbs]: op 0 = add, 1 = mul (md.cuh). */
+int mdps_test_md_op(int32_t op, const double *a, const double *b, double *c, int32_t count,
+                    int32_t limbs, mdps_stream_t stream);
+
+/* Device sum of squares of a complex md vector v[count][2][limbs]:
+ * out[limbs] = sum_j re_j^2 + im_j^2 (PAPER.md:82-95 without the sqrt). */
+int mdps_test_norm2sq(const double *v, int32_t count, int32_t limbs, double *out,
+                      mdps_stream_t stream);
+
+/* Round trip through the digit format: limbs -> digits -> limbs for
+ * count series [count][2][limbs][degree+1] (digits algo staging). */
+int mdps_test_digits_roundtrip(const double *x, double *y, int32_t count, int32_t degree,
+                               int32_t limbs, mdps_stream_t stream);
+
+/* FP64 peak microbenchmark: independent DFMA chains on every SM for about
+ * `iters` iterations; writes the measured FP64 instructions per second
+ * (host pointer) — the roofline denominator measured in the same run. */
+int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t stream);
+
+/* Per-kernel timing of mdps_eval_diff (measurement only): when enabled, each
+ * launch group is bracketed by CUDA events on the caller's stream (the CUDA
+ * graph path is bypassed while enabled).  mdps_system_timing synchronises
+ * the recorded events and returns the summed device durations since the
+ * last reset. */
+typedef struct {
+    double conv_ms;         /* product kernels (all levels) */
+    double accum_ms;        /* addition-job kernel */
+    double convert_ms;      /* input staging (copy or limbs -> digits) */
+    int64_t conv_launches;
+    int64_t accum_launches;
+    int64_t convert_launches;
+    int64_t evals;
+} mdps_timing;
+
+int mdps_system_set_timing(mdps_system *sys, int32_t enable);
+int mdps_system_timing(mdps_system *sys, mdps_timing *out, int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MDPS_TEST_H */

@@ -276,3 +276,18 @@ def random_system(seed: int, n: int, monos: int, m_range: Tuple[int, int], exps:
     """A small seeded random system in the same recipe (tests)."""
     cfg = Config(f"rand{seed}", n, monos, m_range, exps, degree, limbs, lower, seed)
     return make_system(cfg)
+
+
+def first_entries(si: SystemInputs, count: int):
+    """A deterministic bounded sample of outputs: (0, -1) = f_0, then the
+    nonzero Jacobian entries of row 0, then of row 1, ... (`count` in all)."""
+    out = [(0, -1)]
+    n_polys = len(si.poly_ptr) - 1
+    for i in range(n_polys):
+        cols = sorted({int(v) for r in range(si.poly_ptr[i], si.poly_ptr[i + 1])
+                       for v in si.vars[si.mono_ptr[r]:si.mono_ptr[r + 1]]})
+        for j in cols:
+            if len(out) >= count:
+                return out
+            out.append((i, j))
+    return out[:count]

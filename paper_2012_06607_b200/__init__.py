@@ -1,0 +1,297 @@
+"""libmdps — B200-native evaluation and differentiation of a polynomial system
+at a vector of truncated power series in complex multiple-double precision
+(arXiv 2012.06607).  Thin Python binding of the C ABI in include/libmdps.h:
+argument marshalling only; every step of the computation runs in the CUDA
+kernels of libmdps.so (built in-tree by paper_2012_06607_b200/build.py).
+
+There is no CPU fallback: if libmdps.so is missing or no CUDA device is
+present, the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "MDPS_OK", "MDPS_EINVAL", "MDPS_ENOMEM", "MDPS_ECUDA", "MDPS_ALGO_AUTO", "MDPS_ALGO_EFT",
+    "MDPS_ALGO_DIGITS", "MdpsError", "lib", "library_path", "System",
+    "mdps_system_create", "mdps_eval_diff", "mdps_eval_diff_host", "mdps_system_destroy",
+    "mdps_last_error", "mdps_system_stats", "EXPORTED_SYMBOLS",
+]
+
+MDPS_OK, MDPS_EINVAL, MDPS_ENOMEM, MDPS_ECUDA = 0, -1, -2, -3
+MDPS_ALGO_AUTO, MDPS_ALGO_EFT, MDPS_ALGO_DIGITS = 0, 1, 2
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+library_path = os.path.join(_HERE, "libmdps.so")
+
+# every extern "C" symbol declared in include/libmdps.h and include/mdps_test.h
+EXPORTED_SYMBOLS = (
+    "mdps_system_create", "mdps_system_create_ex", "mdps_eval_diff", "mdps_eval_diff_host",
+    "mdps_system_destroy", "mdps_last_error", "mdps_system_stats", "mdps_system_level_jobs",
+    "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
+    "mdps_fp64_peak", "mdps_system_set_timing", "mdps_system_timing",
+)
+
+
+class MdpsError(RuntimeError):
+    pass
+
+
+class _Supports(ctypes.Structure):
+    _fields_ = [("n_polys", ctypes.c_int32), ("poly_ptr", ctypes.POINTER(ctypes.c_int32)),
+                ("mono_ptr", ctypes.POINTER(ctypes.c_int32)), ("vars", ctypes.POINTER(ctypes.c_int32))]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("algo", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("products", ctypes.c_int64), ("add_terms", ctypes.c_int64),
+                ("fp64_ops_conv", ctypes.c_int64), ("fp64_ops_total", ctypes.c_int64),
+                ("compulsory_bytes", ctypes.c_int64), ("levels", ctypes.c_int32),
+                ("algo", ctypes.c_int32), ("digits", ctypes.c_int32), ("launches", ctypes.c_int32),
+                ("workspace_bytes", ctypes.c_size_t)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class Timing(ctypes.Structure):
+    _fields_ = [("conv_ms", ctypes.c_double), ("accum_ms", ctypes.c_double), ("convert_ms", ctypes.c_double),
+                ("conv_launches", ctypes.c_int64), ("accum_launches", ctypes.c_int64),
+                ("convert_launches", ctypes.c_int64), ("evals", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libmdps.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(library_path):
+        raise MdpsError(f"{library_path} not built: run `python -m paper_2012_06607_b200.build` "
+                        "or __graft_entry__.build()")
+    L = ctypes.CDLL(library_path)
+    P, vp = ctypes.POINTER, ctypes.c_void_p
+    i32, i64 = ctypes.c_int32, ctypes.c_int64
+    L.mdps_system_create.restype = vp
+    L.mdps_system_create.argtypes = [P(_Supports), P(i32), P(ctypes.c_double), i32, i32, i32]
+    L.mdps_system_create_ex.restype = vp
+    L.mdps_system_create_ex.argtypes = [P(_Supports), P(i32), P(ctypes.c_double), i32, i32, i32, P(_Options)]
+    L.mdps_eval_diff.argtypes = [vp, vp, vp, vp, vp]
+    L.mdps_eval_diff_host.argtypes = [vp, vp, vp, vp, vp]
+    L.mdps_system_destroy.argtypes = [vp]
+    L.mdps_system_destroy.restype = None
+    L.mdps_last_error.restype = ctypes.c_char_p
+    L.mdps_system_stats.argtypes = [vp, P(Stats)]
+    L.mdps_system_level_jobs.argtypes = [vp, P(i64), i32]
+    L.mdps_test_series_mul.argtypes = [vp, vp, vp, i32, i32, i32, i32, vp]
+    L.mdps_test_md_op.argtypes = [i32, vp, vp, vp, i32, i32, vp]
+    L.mdps_test_norm2sq.argtypes = [vp, i32, i32, vp, vp]
+    L.mdps_test_digits_roundtrip.argtypes = [vp, vp, i32, i32, i32, vp]
+    L.mdps_fp64_peak.argtypes = [i64, P(ctypes.c_double), vp]
+    L.mdps_system_set_timing.argtypes = [vp, i32]
+    L.mdps_system_timing.argtypes = [vp, P(Timing), i32]
+    _lib = L
+    return L
+
+
+def mdps_last_error() -> str:
+    return lib().mdps_last_error().decode()
+
+
+def _check(rc: int, what: str):
+    if rc != MDPS_OK:
+        raise MdpsError(f"{what} failed (rc={rc}): {mdps_last_error()}")
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.int32))
+
+
+def _ptr_i32(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dptr(t) -> int:
+    """device pointer of a torch CUDA float64 contiguous tensor."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise MdpsError("expected a contiguous float64 CUDA tensor")
+    return t.data_ptr()
+
+
+def mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n: int, degree: int,
+                       limbs: int, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False) -> int:
+    """Create a system; returns the opaque handle (int).  Host numpy inputs."""
+    pp, mp, vv, ee = _i32(poly_ptr), _i32(mono_ptr), _i32(vars_), _i32(exponents)
+    coeffs = np.ascontiguousarray(np.asarray(coefficients, dtype=np.float64))
+    sup = _Supports(len(pp) - 1, _ptr_i32(pp), _ptr_i32(mp), _ptr_i32(vv))
+    opts = _Options(algo, 1 if use_graph else 0)
+    h = lib().mdps_system_create_ex(ctypes.byref(sup), _ptr_i32(ee),
+                                    coeffs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                    n, degree, limbs, ctypes.byref(opts))
+    if not h:
+        raise MdpsError(f"mdps_system_create failed: {mdps_last_error()}")
+    return h
+
+
+def mdps_eval_diff(handle: int, series_in, values_out, jacobian_out, stream=None) -> None:
+    """Asynchronous eval/diff on device tensors (libmdps.h)."""
+    _check(lib().mdps_eval_diff(handle, _dptr(series_in), _dptr(values_out), _dptr(jacobian_out),
+                                _stream_handle(stream)), "mdps_eval_diff")
+
+
+def mdps_eval_diff_host(handle: int, series_in: np.ndarray, values_out: np.ndarray,
+                        jacobian_out: np.ndarray, stream=None) -> None:
+    """End-to-end eval/diff with HOST numpy buffers (synchronous)."""
+    for a in (series_in, values_out, jacobian_out):
+        if not (a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
+            raise MdpsError("expected C-contiguous float64 host arrays")
+    _check(lib().mdps_eval_diff_host(handle, series_in.ctypes.data, values_out.ctypes.data,
+                                     jacobian_out.ctypes.data, _stream_handle(stream)),
+           "mdps_eval_diff_host")
+
+
+def mdps_system_destroy(handle: int) -> None:
+    lib().mdps_system_destroy(handle)
+
+
+def mdps_system_stats(handle: int) -> dict:
+    st = Stats()
+    _check(lib().mdps_system_stats(handle, ctypes.byref(st)), "mdps_system_stats")
+    return st.as_dict()
+
+
+class System:
+    """RAII wrapper: a polynomial system on the device (see libmdps.h)."""
+
+    def __init__(self, poly_ptr, mono_ptr, vars_, exponents, coefficients, n, degree, limbs,
+                 algo: int = MDPS_ALGO_AUTO, use_graph: bool = False):
+        self.n, self.degree, self.limbs = int(n), int(degree), int(limbs)
+        self.handle = mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n,
+                                         degree, limbs, algo, use_graph)
+
+    @classmethod
+    def from_inputs(cls, si, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False) -> "System":
+        """From an mdinputs.SystemInputs-like object (poly_ptr, mono_ptr, vars, exps, coeffs)."""
+        return cls(si.poly_ptr, si.mono_ptr, si.vars, si.exps, si.coeffs, si.n, si.degree, si.limbs,
+                   algo, use_graph)
+
+    @property
+    def series_shape(self):
+        return (2, self.limbs, self.degree + 1)
+
+    def eval_diff(self, series_in, values_out=None, jacobian_out=None, stream=None):
+        import torch
+        if values_out is None:
+            values_out = torch.empty((self.n,) + self.series_shape, dtype=torch.float64, device=series_in.device)
+        if jacobian_out is None:
+            jacobian_out = torch.empty((self.n, self.n) + self.series_shape, dtype=torch.float64,
+                                       device=series_in.device)
+        mdps_eval_diff(self.handle, series_in, values_out, jacobian_out, stream)
+        return values_out, jacobian_out
+
+    def eval_diff_host(self, series_in: np.ndarray, stream=None):
+        vals = np.empty((self.n,) + self.series_shape)
+        jac = np.empty((self.n, self.n) + self.series_shape)
+        mdps_eval_diff_host(self.handle, np.ascontiguousarray(series_in, dtype=np.float64), vals, jac, stream)
+        return vals, jac
+
+    def stats(self) -> dict:
+        return mdps_system_stats(self.handle)
+
+    def level_jobs(self):
+        buf = (ctypes.c_int64 * 4096)()
+        n = lib().mdps_system_level_jobs(self.handle, buf, 4096)
+        if n < 0:
+            raise MdpsError(mdps_last_error())
+        return list(buf[:n])
+
+    def set_timing(self, enable: bool = True) -> None:
+        _check(lib().mdps_system_set_timing(self.handle, 1 if enable else 0), "mdps_system_set_timing")
+
+    def timing(self, reset: bool = True) -> dict:
+        t = Timing()
+        _check(lib().mdps_system_timing(self.handle, ctypes.byref(t), 1 if reset else 0), "mdps_system_timing")
+        return t.as_dict()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            mdps_system_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+# ---- diagnostic entry points (include/mdps_test.h) -----------------------------
+def test_series_mul(x, y, algo: int = MDPS_ALGO_DIGITS, stream=None):
+    """z[c] = x[c] * y[c] mod t^D for device tensors [count][2][L][D]."""
+    import torch
+    z = torch.empty_like(x)
+    count, _, L, D = x.shape
+    _check(lib().mdps_test_series_mul(_dptr(x), _dptr(y), _dptr(z), count, D - 1, L, algo,
+                                      _stream_handle(stream)), "mdps_test_series_mul")
+    return z
+
+
+def test_md_op(op: int, a, b, stream=None):
+    import torch
+    c = torch.empty_like(a)
+    count, L = a.shape
+    _check(lib().mdps_test_md_op(op, _dptr(a), _dptr(b), _dptr(c), count, L, _stream_handle(stream)),
+           "mdps_test_md_op")
+    return c
+
+
+def test_norm2sq(v, stream=None):
+    import torch
+    count, _, L = v.shape
+    out = torch.empty(L, dtype=torch.float64, device=v.device)
+    _check(lib().mdps_test_norm2sq(_dptr(v), count, L, _dptr(out), _stream_handle(stream)), "mdps_test_norm2sq")
+    return out
+
+
+def test_digits_roundtrip(x, stream=None):
+    import torch
+    y = torch.empty_like(x)
+    count, _, L, D = x.shape
+    _check(lib().mdps_test_digits_roundtrip(_dptr(x), _dptr(y), count, D - 1, L, _stream_handle(stream)),
+           "mdps_test_digits_roundtrip")
+    return y
+
+
+def fp64_peak(iters: int = 20000, stream=None) -> float:
+    """Measured FP64 instructions/s (independent DFMA chains on every SM)."""
+    out = ctypes.c_double(0.0)
+    _check(lib().mdps_fp64_peak(iters, ctypes.byref(out), _stream_handle(stream)), "mdps_fp64_peak")
+    return out.value

@@ -1,0 +1,765 @@
+// libmdps.cu — the C ABI (include/libmdps.h): system creation, the leveled
+// launcher of the product jobs and the addition jobs, statistics.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/libmdps.h"
+#include "../../include/mdps_test.h"
+#include "kernels_dig.cuh"
+#include "kernels_eft.cuh"
+#include "schedule.hpp"
+
+using namespace mdps;
+
+static thread_local std::string g_err;
+
+static void set_err(const std::string &s) { g_err = s; }
+
+#define CUDA_TRY(call, code)                                                          \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess) {                                                      \
+            set_err(std::string(#call) + ": " + cudaGetErrorString(e_));              \
+            return code;                                                              \
+        }                                                                             \
+    } while (0)
+
+extern "C" const char *mdps_last_error(void) { return g_err.c_str(); }
+
+static bool valid_limbs(int L) { return L == 2 || L == 3 || L == 4 || L == 5 || L == 8 || L == 10; }
+
+// dispatch a templated functor on L
+template <template <int> class Fn, typename... Args>
+static int dispatch_L(int L, Args &&...args) {
+    switch (L) {
+        case 2: return Fn<2>::run(args...);
+        case 3: return Fn<3>::run(args...);
+        case 4: return Fn<4>::run(args...);
+        case 5: return Fn<5>::run(args...);
+        case 8: return Fn<8>::run(args...);
+        case 10: return Fn<10>::run(args...);
+    }
+    set_err("unsupported limb count");
+    return MDPS_EINVAL;
+}
+
+// ---------------------------------------------------------------------------
+// launch geometry
+struct EftGeom {
+    int T, P, threads;
+    size_t smem;
+};
+static EftGeom eft_geom(int L, int D) {
+    EftGeom g;
+    g.T = (D + 1) / 2;
+    g.P = std::max(1, 128 / g.T);
+    g.threads = g.P * g.T;
+    const size_t JS = (size_t)2 * (2 * L * D) + 2;
+    g.smem = ((size_t)g.P * JS + (size_t)g.threads * 2 * (L + 1)) * sizeof(double);
+    return g;
+}
+
+struct DigGeom {
+    int T, F, P, threads;
+    size_t smem;
+};
+static DigGeom dig_geom(int L, int D) {
+    const int S = digits_for(L);
+    DigGeom g;
+    g.T = (D + 1) / 2;
+    int F = 1;
+    while (g.T * F * 2 <= 128 && (D + 1) / (F * 2) >= 8) F *= 2;
+    g.F = F;
+    g.P = std::max(1, 128 / (g.T * g.F));
+    for (;;) {
+        g.threads = g.P * g.T * g.F;
+        g.smem = conv_dig_smem(S, D, g.P, g.threads);
+        if (g.smem <= 110 * 1024 || g.P == 1) break;
+        g.P /= 2;
+    }
+    return g;
+}
+
+// ---------------------------------------------------------------------------
+template <int L>
+struct ConvEft {
+    static int run(double *pool, const int *jobs, int njobs, int D, cudaStream_t st) {
+        if (njobs <= 0) return MDPS_OK;
+        EftGeom g = eft_geom(L, D);
+        auto kern = conv_eft_kernel<L>;
+        if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+        const int blocks = (njobs + g.P - 1) / g.P;
+        kern<<<blocks, g.threads, g.smem, st>>>(pool, jobs, njobs, D, g.T, g.P);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+template <int L>
+struct ConvDig {
+    static int run(double *dpool, int *epool, const int *jobs, int njobs, int D, cudaStream_t st) {
+        if (njobs <= 0) return MDPS_OK;
+        DigGeom g = dig_geom(L, D);
+        auto kern = conv_dig_kernel<L>;
+        if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+        const int blocks = (njobs + g.P - 1) / g.P;
+        kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, jobs, njobs, D, g.T, g.F, g.P);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+template <int L>
+struct AccumEft {
+    static int run(const double *pool, const int *tp, const int *es, const int *ew, int ntasks, int n, int D,
+                   double *values, double *jac, cudaStream_t st) {
+        const long long total = (long long)ntasks * D;
+        const int blocks = (int)((total + 127) / 128);
+        accum_eft_kernel<L><<<blocks, 128, 0, st>>>(pool, tp, es, ew, ntasks, n, D, values, jac);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+template <int L>
+struct AccumDig {
+    static int run(const double *dpool, const int *epool, const int *tp, const int *es, const int *ew, int ntasks,
+                   int n, int D, double *values, double *jac, cudaStream_t st) {
+        const long long total = (long long)ntasks * D;
+        const int blocks = (int)((total + 127) / 128);
+        accum_dig_kernel<L><<<blocks, 128, 0, st>>>(dpool, epool, tp, es, ew, ntasks, n, D, values, jac);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+template <int L>
+struct ToDigits {
+    static int run(const double *src, int count, int D, double *dpool, int *epool, int slot0, cudaStream_t st) {
+        if (count <= 0) return MDPS_OK;
+        const long long total = (long long)count * D;
+        const int blocks = (int)((total + 127) / 128);
+        to_digits_kernel<L><<<blocks, 128, 0, st>>>(src, count, D, dpool, epool, slot0);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+// ---------------------------------------------------------------------------
+struct mdps_system {
+    int n = 0, D = 0, L = 0, M = 0, algo = MDPS_ALGO_DIGITS, S = 0;
+    int use_graph = 0;
+    int64_t nslots = 0, products = 0, add_terms = 0;
+    std::vector<int64_t> level_off, level_cnt;  // in jobs
+    int ntasks = 0;
+    // device
+    double *pool = nullptr;  // EFT: limb planes [slot][2][L][D]; DIGITS: digit planes [slot][2][S][D]
+    int *epool = nullptr;    // DIGITS: exponents [slot][2][D]
+    int *jobs = nullptr;     // all levels, (in1, in2, out) triples
+    int *task_ptr = nullptr, *ent_slot = nullptr, *ent_w = nullptr;
+    double *host_in = nullptr;  // staging for the _host variant (device buffers)
+    double *dev_in = nullptr, *dev_vals = nullptr, *dev_jac = nullptr;
+    size_t device_bytes = 0;
+    // CUDA graph cache
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph = nullptr;
+    const void *g_in = nullptr, *g_vals = nullptr, *g_jac = nullptr;
+    cudaStream_t g_stream = nullptr;
+    // measurement: event pairs per launch group (kind 0 conv, 1 accum, 2 convert)
+    int timing = 0;
+    struct Mark { cudaEvent_t a, b; int kind; };
+    std::vector<Mark> marks;
+    int64_t timed_evals = 0;
+};
+
+static void drop_marks(mdps_system *s) {
+    for (auto &m : s->marks) {
+        cudaEventDestroy(m.a);
+        cudaEventDestroy(m.b);
+    }
+    s->marks.clear();
+}
+
+// begin/end a timed launch group (no-op unless timing is enabled)
+struct TimedGroup {
+    mdps_system *s;
+    cudaStream_t st;
+    int kind;
+    cudaEvent_t a = nullptr, b = nullptr;
+    TimedGroup(mdps_system *s_, cudaStream_t st_, int kind_) : s(s_), st(st_), kind(kind_) {
+        if (s->timing && cudaEventCreate(&a) == cudaSuccess && cudaEventCreate(&b) == cudaSuccess)
+            cudaEventRecord(a, st);
+    }
+    ~TimedGroup() {
+        if (a && b) {
+            cudaEventRecord(b, st);
+            s->marks.push_back({a, b, kind});
+        }
+    }
+};
+
+static void free_system(mdps_system *s) {
+    if (!s) return;
+    drop_marks(s);
+    if (s->gexec) cudaGraphExecDestroy(s->gexec);
+    if (s->graph) cudaGraphDestroy(s->graph);
+    cudaFree(s->pool);
+    cudaFree(s->epool);
+    cudaFree(s->jobs);
+    cudaFree(s->task_ptr);
+    cudaFree(s->ent_slot);
+    cudaFree(s->ent_w);
+    cudaFree(s->dev_in);
+    cudaFree(s->dev_vals);
+    cudaFree(s->dev_jac);
+    delete s;
+}
+
+template <typename T>
+static bool dalloc(mdps_system *s, T **p, size_t count) {
+    if (count == 0) count = 1;
+    if (cudaMalloc((void **)p, count * sizeof(T)) != cudaSuccess) {
+        cudaGetLastError();
+        set_err("cudaMalloc of " + std::to_string(count * sizeof(T)) + " bytes failed");
+        return false;
+    }
+    s->device_bytes += count * sizeof(T);
+    return true;
+}
+
+extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const int32_t *exponents,
+                                              const double *coefficients, int32_t n, int32_t degree,
+                                              int32_t limbs, const mdps_options *opt) {
+    if (!sup) { set_err("NULL supports"); return nullptr; }
+    if (n < 1) { set_err("n must be >= 1"); return nullptr; }
+    if (degree < 0 || degree > 255) { set_err("degree must be in [0, 255]"); return nullptr; }
+    if (!valid_limbs(limbs)) { set_err("limbs must be one of 2, 3, 4, 5, 8, 10"); return nullptr; }
+    int algo = opt ? opt->algo : MDPS_ALGO_AUTO;
+    if (algo != MDPS_ALGO_AUTO && algo != MDPS_ALGO_EFT && algo != MDPS_ALGO_DIGITS) {
+        set_err("unknown algo");
+        return nullptr;
+    }
+    const int D = degree + 1;
+    if (algo == MDPS_ALGO_AUTO) algo = (D <= 128) ? MDPS_ALGO_DIGITS : MDPS_ALGO_EFT;
+    if (algo == MDPS_ALGO_DIGITS && D > 128) { set_err("the digits algorithm supports degree <= 127"); return nullptr; }
+
+    Schedule S;
+    std::string err;
+    if (!build_schedule(sup->n_polys, sup->poly_ptr, sup->mono_ptr, sup->vars, exponents, n, S, err)) {
+        set_err(err);
+        return nullptr;
+    }
+    if (S.M > 0 && !coefficients) { set_err("NULL coefficients"); return nullptr; }
+
+    mdps_system *s = new (std::nothrow) mdps_system();
+    if (!s) { set_err("host allocation failed"); return nullptr; }
+    s->n = n;
+    s->D = D;
+    s->L = limbs;
+    s->M = S.M;
+    s->algo = algo;
+    s->S = algo == MDPS_ALGO_DIGITS ? digits_for(limbs) : 0;
+    s->use_graph = opt ? opt->use_graph : 0;
+    s->nslots = S.nslots;
+    s->products = S.products;
+    s->add_terms = (int64_t)S.ent_slot.size();
+    s->ntasks = n + n * n;
+
+    std::vector<int32_t> alljobs;
+    for (auto &lv : S.levels) {
+        s->level_off.push_back((int64_t)alljobs.size() / 3);
+        s->level_cnt.push_back((int64_t)lv.size() / 3);
+        alljobs.insert(alljobs.end(), lv.begin(), lv.end());
+    }
+    const size_t ser = (size_t)2 * (algo == MDPS_ALGO_DIGITS ? s->S : limbs) * D;  // doubles per slot
+    if (!dalloc(s, &s->pool, ser * (size_t)s->nslots) ||
+        (algo == MDPS_ALGO_DIGITS && !dalloc(s, &s->epool, (size_t)2 * D * s->nslots)) ||
+        !dalloc(s, &s->jobs, alljobs.size()) || !dalloc(s, &s->task_ptr, S.task_ptr.size()) ||
+        !dalloc(s, &s->ent_slot, S.ent_slot.size()) || !dalloc(s, &s->ent_w, S.ent_w.size())) {
+        free_system(s);
+        return nullptr;
+    }
+    auto up = [&](void *dst, const void *src, size_t bytes) {
+        return bytes == 0 || cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    const size_t limb_ser = (size_t)2 * limbs * D;
+    bool ok = up(s->jobs, alljobs.data(), alljobs.size() * 4) &&
+              up(s->task_ptr, S.task_ptr.data(), S.task_ptr.size() * 4) &&
+              up(s->ent_slot, S.ent_slot.data(), S.ent_slot.size() * 4) &&
+              up(s->ent_w, S.ent_w.data(), S.ent_w.size() * 4);
+    if (ok && S.M > 0) {
+        if (algo == MDPS_ALGO_EFT) {
+            ok = up(s->pool + (size_t)n * ser, coefficients, (size_t)S.M * limb_ser * 8);
+        } else {
+            double *tmp = nullptr;
+            ok = cudaMalloc((void **)&tmp, (size_t)S.M * limb_ser * 8) == cudaSuccess &&
+                 up(tmp, coefficients, (size_t)S.M * limb_ser * 8);
+            if (ok) {
+                const int rc = dispatch_L<ToDigits>(limbs, (const double *)tmp, S.M, D, s->pool, s->epool, n,
+                                                    (cudaStream_t)0);
+                ok = rc == MDPS_OK && cudaDeviceSynchronize() == cudaSuccess;
+            }
+            cudaFree(tmp);
+        }
+    }
+    if (!ok) {
+        cudaGetLastError();
+        if (g_err.empty()) set_err("uploading the system to the device failed");
+        free_system(s);
+        return nullptr;
+    }
+    return s;
+}
+
+extern "C" mdps_system *mdps_system_create(const mdps_supports *sup, const int32_t *exponents,
+                                           const double *coefficients, int32_t n, int32_t degree,
+                                           int32_t limbs) {
+    return mdps_system_create_ex(sup, exponents, coefficients, n, degree, limbs, nullptr);
+}
+
+extern "C" void mdps_system_destroy(mdps_system *s) {
+    if (!s) return;
+    cudaDeviceSynchronize();
+    free_system(s);
+}
+
+// the launch sequence of one eval (also what the CUDA graph captures)
+static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, cudaStream_t st) {
+    const int L = s->L, D = s->D, n = s->n;
+    int rc;
+    if (s->timing) s->timed_evals++;
+    if (s->algo == MDPS_ALGO_EFT) {
+        {
+            TimedGroup tg(s, st, 2);
+            CUDA_TRY(cudaMemcpyAsync(s->pool, in, (size_t)n * 2 * L * D * 8, cudaMemcpyDeviceToDevice, st),
+                     MDPS_ECUDA);
+        }
+        for (size_t lv = 0; lv < s->level_cnt.size(); lv++) {
+            TimedGroup tg(s, st, 0);
+            rc = dispatch_L<ConvEft>(L, s->pool, (const int *)(s->jobs + 3 * s->level_off[lv]),
+                                     (int)s->level_cnt[lv], D, st);
+            if (rc) return rc;
+        }
+        TimedGroup tg(s, st, 1);
+        return dispatch_L<AccumEft>(L, (const double *)s->pool, (const int *)s->task_ptr,
+                                    (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, n, D, vals, jac, st);
+    }
+    {
+        TimedGroup tg(s, st, 2);
+        rc = dispatch_L<ToDigits>(L, in, n, D, s->pool, s->epool, 0, st);
+        if (rc) return rc;
+    }
+    for (size_t lv = 0; lv < s->level_cnt.size(); lv++) {
+        TimedGroup tg(s, st, 0);
+        rc = dispatch_L<ConvDig>(L, s->pool, s->epool, (const int *)(s->jobs + 3 * s->level_off[lv]),
+                                 (int)s->level_cnt[lv], D, st);
+        if (rc) return rc;
+    }
+    TimedGroup tg(s, st, 1);
+    return dispatch_L<AccumDig>(L, (const double *)s->pool, (const int *)s->epool, (const int *)s->task_ptr,
+                                (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, n, D, vals, jac, st);
+}
+
+extern "C" int mdps_system_set_timing(mdps_system *s, int32_t enable) {
+    if (!s) {
+        set_err("NULL argument");
+        return MDPS_EINVAL;
+    }
+    s->timing = enable ? 1 : 0;
+    return MDPS_OK;
+}
+
+extern "C" int mdps_system_timing(mdps_system *s, mdps_timing *out, int32_t reset) {
+    if (!s || !out) {
+        set_err("NULL argument");
+        return MDPS_EINVAL;
+    }
+    memset(out, 0, sizeof *out);
+    for (auto &m : s->marks) {
+        CUDA_TRY(cudaEventSynchronize(m.b), MDPS_ECUDA);
+        float ms = 0.f;
+        CUDA_TRY(cudaEventElapsedTime(&ms, m.a, m.b), MDPS_ECUDA);
+        if (m.kind == 0) { out->conv_ms += ms; out->conv_launches++; }
+        else if (m.kind == 1) { out->accum_ms += ms; out->accum_launches++; }
+        else { out->convert_ms += ms; out->convert_launches++; }
+    }
+    out->evals = s->timed_evals;
+    if (reset) {
+        drop_marks(s);
+        s->timed_evals = 0;
+    }
+    return MDPS_OK;
+}
+
+static bool overlaps(const void *a, size_t na, const void *b, size_t nb) {
+    const char *x = (const char *)a, *y = (const char *)b;
+    return x < y + nb && y < x + na;
+}
+
+extern "C" int mdps_eval_diff(mdps_system *s, const double *in, double *vals, double *jac, mdps_stream_t stream) {
+    if (!s || !in || !vals || !jac) {
+        set_err("NULL argument");
+        return MDPS_EINVAL;
+    }
+    const size_t ser = (size_t)2 * s->L * s->D * 8;
+    const size_t nin = ser * s->n, njac = ser * s->n * s->n;
+    if (overlaps(in, nin, vals, nin) || overlaps(in, nin, jac, njac) || overlaps(vals, nin, jac, njac)) {
+        set_err("outputs alias each other or the input");
+        return MDPS_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!s->use_graph || s->timing) return enqueue(s, in, vals, jac, st);
+    if (!s->gexec || s->g_in != in || s->g_vals != vals || s->g_jac != jac || s->g_stream != st) {
+        if (s->gexec) { cudaGraphExecDestroy(s->gexec); s->gexec = nullptr; }
+        if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
+        CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), MDPS_ECUDA);
+        const int rc = enqueue(s, in, vals, jac, st);
+        cudaGraph_t g = nullptr;
+        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        if (rc != MDPS_OK) { if (g) cudaGraphDestroy(g); return rc; }
+        if (ce != cudaSuccess) { set_err(std::string("graph capture: ") + cudaGetErrorString(ce)); return MDPS_ECUDA; }
+        s->graph = g;
+        CUDA_TRY(cudaGraphInstantiate(&s->gexec, g, 0), MDPS_ECUDA);
+        s->g_in = in;
+        s->g_vals = vals;
+        s->g_jac = jac;
+        s->g_stream = st;
+    }
+    CUDA_TRY(cudaGraphLaunch(s->gexec, st), MDPS_ECUDA);
+    return MDPS_OK;
+}
+
+extern "C" int mdps_eval_diff_host(mdps_system *s, const double *in_h, double *vals_h, double *jac_h,
+                                   mdps_stream_t stream) {
+    if (!s || !in_h || !vals_h || !jac_h) {
+        set_err("NULL argument");
+        return MDPS_EINVAL;
+    }
+    const size_t ser = (size_t)2 * s->L * s->D;
+    if (!s->dev_in) {
+        if (!dalloc(s, &s->dev_in, ser * s->n) || !dalloc(s, &s->dev_vals, ser * s->n) ||
+            !dalloc(s, &s->dev_jac, ser * s->n * s->n))
+            return MDPS_ENOMEM;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaMemcpyAsync(s->dev_in, in_h, ser * s->n * 8, cudaMemcpyHostToDevice, st), MDPS_ECUDA);
+    int rc = mdps_eval_diff(s, s->dev_in, s->dev_vals, s->dev_jac, stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(vals_h, s->dev_vals, ser * s->n * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
+    CUDA_TRY(cudaMemcpyAsync(jac_h, s->dev_jac, ser * s->n * s->n * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
+    CUDA_TRY(cudaStreamSynchronize(st), MDPS_ECUDA);
+    return MDPS_OK;
+}
+
+// FP64 instruction counts
+static int64_t conv_ops_per_product(int algo, int L, int D) {
+    const int64_t terms = (int64_t)D * (D + 1) / 2;
+    if (algo == MDPS_ALGO_EFT) return terms * 4 * ops_bins_fma(L);
+    const int64_t S = digits_for(L);
+    return terms * 2 * S * (S + 1);  // one DFMA per digit pair, 2 real products per part
+}
+
+extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
+    if (!s || !out) {
+        set_err("NULL argument");
+        return MDPS_EINVAL;
+    }
+    memset(out, 0, sizeof *out);
+    out->products = s->products;
+    out->add_terms = s->add_terms;
+    out->fp64_ops_conv = s->products * conv_ops_per_product(s->algo, s->L, s->D);
+    int64_t add_ops;
+    if (s->algo == MDPS_ALGO_EFT)
+        add_ops = s->add_terms * s->D * 2 * ops_bins_add(s->L);
+    else
+        add_ops = s->add_terms * s->D * 2 * (digits_for(s->L) + 1);
+    out->fp64_ops_total = out->fp64_ops_conv + add_ops;
+    const int64_t ser = (int64_t)2 * s->L * s->D * 8;
+    out->compulsory_bytes = ser * ((int64_t)s->n + s->M + s->n + (int64_t)s->n * s->n);
+    out->levels = (int32_t)s->level_cnt.size();
+    out->algo = s->algo;
+    out->digits = s->S;
+    out->launches = (int32_t)s->level_cnt.size() + 2;
+    out->workspace_bytes = s->device_bytes;
+    return MDPS_OK;
+}
+
+extern "C" int mdps_system_level_jobs(const mdps_system *s, int64_t *jobs, int32_t maxl) {
+    if (!s || !jobs) {
+        set_err("NULL argument");
+        return MDPS_EINVAL;
+    }
+    const int nl = (int)s->level_cnt.size();
+    for (int i = 0; i < nl && i < maxl; i++) jobs[i] = s->level_cnt[i];
+    return nl;
+}
+
+// ---------------------------------------------------------------------------
+// test entry points (include/mdps_test.h)
+template <int L>
+struct MdOp {
+    static int run(int op, const double *a, const double *b, double *c, int count, cudaStream_t st);
+};
+
+template <int L>
+__global__ void md_op_kernel(int op, const double *a, const double *b, double *c, int count) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= count) return;
+    double x[L], y[L], z[L];
+#pragma unroll
+    for (int p = 0; p < L; p++) {
+        x[p] = a[(size_t)g * L + p];
+        y[p] = b[(size_t)g * L + p];
+    }
+    if (op == 0) md_add<L>(x, y, z);
+    else md_mul<L>(x, y, z);
+#pragma unroll
+    for (int p = 0; p < L; p++) c[(size_t)g * L + p] = z[p];
+}
+
+template <int L>
+int MdOp<L>::run(int op, const double *a, const double *b, double *c, int count, cudaStream_t st) {
+    md_op_kernel<L><<<(count + 127) / 128, 128, 0, st>>>(op, a, b, c, count);
+    CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+    return MDPS_OK;
+}
+
+template <int L>
+__global__ void norm2sq_kernel(const double *v, int count, double *out) {
+    // one warp: lane j accumulates entries j, j+32, ... in level bins, then
+    // lane 0 merges the 32 partial bins in order (deterministic)
+    __shared__ double part[32][L + 1];
+    double B[L + 1];
+    md_zero(B);
+    for (int j = threadIdx.x; j < count; j += 32) {
+        double re[L], im[L];
+#pragma unroll
+        for (int p = 0; p < L; p++) {
+            re[p] = v[((size_t)j * 2 + 0) * L + p];
+            im[p] = v[((size_t)j * 2 + 1) * L + p];
+        }
+        bins_fma<L>(B, re, re);
+        bins_fma<L>(B, im, im);
+    }
+#pragma unroll
+    for (int p = 0; p <= L; p++) part[threadIdx.x][p] = B[p];
+    __syncwarp();
+    if (threadIdx.x == 0) {
+        double C[L + 1];
+        md_zero(C);
+        for (int w = 0; w < 32; w++) {
+            double t[L + 1], lim[L];
+#pragma unroll
+            for (int p = 0; p <= L; p++) t[p] = part[w][p];
+            md_renorm(t, lim);
+            bins_add<L>(C, lim);
+        }
+        double r[L];
+        md_renorm(C, r);
+#pragma unroll
+        for (int p = 0; p < L; p++) out[p] = r[p];
+    }
+}
+
+template <int L>
+struct Norm2sq {
+    static int run(const double *v, int count, double *out, cudaStream_t st) {
+        norm2sq_kernel<L><<<1, 32, 0, st>>>(v, count, out);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+template <int L>
+struct Roundtrip {
+    static int run(const double *x, double *y, int count, int D, cudaStream_t st) {
+        const long long total = (long long)count * 2 * D;
+        digits_roundtrip_kernel<L><<<(int)((total + 127) / 128), 128, 0, st>>>(x, y, count, D);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+template <int L>
+struct SeriesMulDig {
+    // stage x and y into a scratch digit pool, run the product kernel, convert back
+    static int run(const double *x, const double *y, double *z, int count, int D, cudaStream_t st) {
+        constexpr int S = digits_for(L);
+        double *dp = nullptr;
+        int *ep = nullptr, *jobs = nullptr;
+        double *vals_dummy = nullptr;
+        int *tp = nullptr, *es = nullptr, *ew = nullptr;
+        const size_t slots = (size_t)3 * count;
+        int rc = MDPS_OK;
+        std::vector<int> hj(3 * (size_t)count), htp((size_t)count + 1), hes(count), hew(count, 1);
+        for (int c = 0; c < count; c++) {
+            hj[3 * c] = c;
+            hj[3 * c + 1] = count + c;
+            hj[3 * c + 2] = 2 * count + c;
+            htp[c] = c;
+            hes[c] = 2 * count + c;
+        }
+        htp[count] = count;
+        if (cudaMalloc((void **)&dp, slots * 2 * S * D * 8) != cudaSuccess ||
+            cudaMalloc((void **)&ep, slots * 2 * D * 4) != cudaSuccess ||
+            cudaMalloc((void **)&jobs, hj.size() * 4) != cudaSuccess ||
+            cudaMalloc((void **)&tp, htp.size() * 4) != cudaSuccess ||
+            cudaMalloc((void **)&es, hes.size() * 4) != cudaSuccess ||
+            cudaMalloc((void **)&ew, hew.size() * 4) != cudaSuccess) {
+            cudaGetLastError();
+            set_err("cudaMalloc failed");
+            rc = MDPS_ENOMEM;
+        }
+        if (!rc) {
+            cudaMemcpyAsync(jobs, hj.data(), hj.size() * 4, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(tp, htp.data(), htp.size() * 4, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(es, hes.data(), hes.size() * 4, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(ew, hew.data(), hew.size() * 4, cudaMemcpyHostToDevice, st);
+            rc = ToDigits<L>::run(x, count, D, dp, ep, 0, st);
+            if (!rc) rc = ToDigits<L>::run(y, count, D, dp, ep, count, st);
+            if (!rc) rc = ConvDig<L>::run(dp, ep, jobs, count, D, st);
+            // the n = count "values" tasks of a count x count system would
+            // need n*n Jacobian outputs: use ntasks = count with n = count
+            if (!rc) rc = AccumDig<L>::run(dp, ep, tp, es, ew, count, count, D, z, vals_dummy, st);
+            if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
+                set_err("series_mul kernel failed");
+                rc = MDPS_ECUDA;
+            }
+        }
+        cudaFree(dp);
+        cudaFree(ep);
+        cudaFree(jobs);
+        cudaFree(tp);
+        cudaFree(es);
+        cudaFree(ew);
+        return rc;
+    }
+};
+
+template <int L>
+struct SeriesMulEft {
+    static int run(const double *x, const double *y, double *z, int count, int D, cudaStream_t st) {
+        const size_t ser = (size_t)2 * L * D;
+        double *pool = nullptr;
+        int *jobs = nullptr;
+        std::vector<int> hj(3 * (size_t)count);
+        for (int c = 0; c < count; c++) {
+            hj[3 * c] = c;
+            hj[3 * c + 1] = count + c;
+            hj[3 * c + 2] = 2 * count + c;
+        }
+        if (cudaMalloc((void **)&pool, 3 * ser * count * 8) != cudaSuccess ||
+            cudaMalloc((void **)&jobs, hj.size() * 4) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFree(pool);
+            set_err("cudaMalloc failed");
+            return MDPS_ENOMEM;
+        }
+        cudaMemcpyAsync(jobs, hj.data(), hj.size() * 4, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(pool, x, ser * count * 8, cudaMemcpyDeviceToDevice, st);
+        cudaMemcpyAsync(pool + ser * count, y, ser * count * 8, cudaMemcpyDeviceToDevice, st);
+        int rc = ConvEft<L>::run(pool, jobs, count, D, st);
+        if (!rc) cudaMemcpyAsync(z, pool + 2 * ser * count, ser * count * 8, cudaMemcpyDeviceToDevice, st);
+        if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
+            set_err("series_mul kernel failed");
+            rc = MDPS_ECUDA;
+        }
+        cudaFree(pool);
+        cudaFree(jobs);
+        return rc;
+    }
+};
+
+extern "C" int mdps_test_series_mul(const double *x, const double *y, double *z, int32_t count, int32_t degree,
+                                    int32_t limbs, int32_t algo, mdps_stream_t stream) {
+    if (!x || !y || !z || count < 0 || degree < 0 || degree > 255 || !valid_limbs(limbs)) {
+        set_err("invalid argument");
+        return MDPS_EINVAL;
+    }
+    if (count == 0) return MDPS_OK;
+    const int D = degree + 1;
+    if (algo == MDPS_ALGO_EFT) return dispatch_L<SeriesMulEft>(limbs, x, y, z, (int)count, D, (cudaStream_t)stream);
+    if (D > 128) { set_err("digits: degree <= 127"); return MDPS_EINVAL; }
+    return dispatch_L<SeriesMulDig>(limbs, x, y, z, (int)count, D, (cudaStream_t)stream);
+}
+
+extern "C" int mdps_test_md_op(int32_t op, const double *a, const double *b, double *c, int32_t count,
+                               int32_t limbs, mdps_stream_t stream) {
+    if (!a || !b || !c || count < 0 || (op != 0 && op != 1) || !valid_limbs(limbs)) {
+        set_err("invalid argument");
+        return MDPS_EINVAL;
+    }
+    if (count == 0) return MDPS_OK;
+    return dispatch_L<MdOp>(limbs, (int)op, a, b, c, (int)count, (cudaStream_t)stream);
+}
+
+extern "C" int mdps_test_norm2sq(const double *v, int32_t count, int32_t limbs, double *out, mdps_stream_t stream) {
+    if (!v || !out || count < 0 || !valid_limbs(limbs)) {
+        set_err("invalid argument");
+        return MDPS_EINVAL;
+    }
+    return dispatch_L<Norm2sq>(limbs, v, (int)count, out, (cudaStream_t)stream);
+}
+
+extern "C" int mdps_test_digits_roundtrip(const double *x, double *y, int32_t count, int32_t degree, int32_t limbs,
+                                          mdps_stream_t stream) {
+    if (!x || !y || count < 0 || degree < 0 || !valid_limbs(limbs)) {
+        set_err("invalid argument");
+        return MDPS_EINVAL;
+    }
+    if (count == 0) return MDPS_OK;
+    return dispatch_L<Roundtrip>(limbs, x, y, (int)count, (int)degree + 1, (cudaStream_t)stream);
+}
+
+// FP64 peak: 8 independent DFMA chains per thread, 4 blocks of 256 per SM
+__global__ void fp64_peak_kernel(int64_t iters, double *sink) {
+    double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+    double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+    const double m = 0.999999999, c = 1e-12;
+    for (int64_t i = 0; i < iters; i++) {
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+            a0 = __fma_rn(a0, m, c); a1 = __fma_rn(a1, m, c); a2 = __fma_rn(a2, m, c); a3 = __fma_rn(a3, m, c);
+            a4 = __fma_rn(a4, m, c); a5 = __fma_rn(a5, m, c); a6 = __fma_rn(a6, m, c); a7 = __fma_rn(a7, m, c);
+        }
+    }
+    const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (s == 12345.678) sink[0] = s;
+}
+
+extern "C" int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t stream) {
+    if (!inst_per_s || iters < 1) {
+        set_err("invalid argument");
+        return MDPS_EINVAL;
+    }
+    int dev = 0, sms = 0;
+    CUDA_TRY(cudaGetDevice(&dev), MDPS_ECUDA);
+    CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), MDPS_ECUDA);
+    double *sink = nullptr;
+    CUDA_TRY(cudaMalloc((void **)&sink, 8), MDPS_ECUDA);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = sms * 4, threads = 256;
+    fp64_peak_kernel<<<blocks, threads, 0, st>>>(iters / 8 + 1, sink);  // warm-up
+    cudaEventRecord(e0, st);
+    fp64_peak_kernel<<<blocks, threads, 0, st>>>(iters, sink);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+    const double inst = (double)blocks * threads * (double)iters * 16.0 * 8.0;
+    *inst_per_s = inst / (ms * 1e-3);
+    return MDPS_OK;
+}

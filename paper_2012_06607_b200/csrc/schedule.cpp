@@ -1,0 +1,126 @@
+// schedule.cpp — builds the leveled product DAG and the addition lists.
+// See schedule.hpp for the scheme and its citations.
+#include "schedule.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <utility>
+
+namespace mdps {
+
+namespace {
+
+struct Builder {
+    Schedule &S;
+    std::vector<int32_t> level;  // per slot
+    explicit Builder(Schedule &s) : S(s) {}
+
+    int32_t job(int32_t a, int32_t b) {
+        const int32_t out = (int32_t)level.size();
+        const int32_t lev = 1 + std::max(level[a], level[b]);
+        level.push_back(lev);
+        if ((int)S.levels.size() < lev) S.levels.resize(lev);
+        auto &v = S.levels[lev - 1];
+        v.push_back(a);
+        v.push_back(b);
+        v.push_back(out);
+        S.products++;
+        return out;
+    }
+};
+
+}  // namespace
+
+bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mono_ptr,
+                    const int32_t *vars, const int32_t *exps, int32_t n, Schedule &S,
+                    std::string &err) {
+    if (n < 1) { err = "n must be >= 1"; return false; }
+    if (n_polys != n) { err = "n_polys must equal n (square systems only in v1)"; return false; }
+    if (!poly_ptr || !mono_ptr) { err = "NULL poly_ptr or mono_ptr"; return false; }
+    if (poly_ptr[0] != 0) { err = "poly_ptr[0] must be 0"; return false; }
+    for (int i = 0; i < n_polys; i++)
+        if (poly_ptr[i + 1] < poly_ptr[i]) { err = "poly_ptr is not non-decreasing"; return false; }
+    const int32_t M = poly_ptr[n_polys];
+    if (mono_ptr[0] != 0) { err = "mono_ptr[0] must be 0"; return false; }
+    for (int r = 0; r < M; r++)
+        if (mono_ptr[r + 1] < mono_ptr[r]) { err = "mono_ptr is not non-decreasing"; return false; }
+    const int32_t nnz = mono_ptr[M];
+    if (nnz > 0 && (!vars || !exps)) { err = "NULL vars or exponents"; return false; }
+    if ((int64_t)n + (int64_t)n * n + 1 > INT32_MAX) { err = "n too large"; return false; }
+
+    S.n = n;
+    S.M = M;
+    S.levels.clear();
+    S.products = 0;
+    Builder B(S);
+    B.level.assign((size_t)n + M, 0);
+    const int64_t ntasks = (int64_t)n + (int64_t)n * n;
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> lists((size_t)ntasks);
+    auto jac = [&](int i, int j) -> std::vector<std::pair<int32_t, int32_t>> & {
+        return lists[(size_t)n + (size_t)i * n + j];
+    };
+
+    std::vector<std::pair<int32_t, int32_t>> mono;
+    std::vector<int32_t> f, Bk;
+    for (int i = 0; i < n_polys; i++) {
+        for (int r = poly_ptr[i]; r < poly_ptr[i + 1]; r++) {
+            mono.clear();
+            for (int t = mono_ptr[r]; t < mono_ptr[r + 1]; t++) {
+                if (vars[t] < 0 || vars[t] >= n) { err = "variable index out of range"; return false; }
+                if (exps[t] < 1) { err = "exponent < 1"; return false; }
+                if (exps[t] > (1 << 20)) { err = "exponent too large"; return false; }
+                mono.emplace_back(vars[t], exps[t]);
+            }
+            std::sort(mono.begin(), mono.end());
+            for (size_t t = 1; t < mono.size(); t++)
+                if (mono[t].first == mono[t - 1].first) {
+                    err = "variable repeated within a monomial";
+                    return false;
+                }
+            const int m = (int)mono.size();
+            const int32_t c = n + r;
+            if (m == 0) {  // constant term
+                lists[i].emplace_back(c, 1);
+                continue;
+            }
+            // common factor c' = c * prod x^(a-1)
+            int32_t cp = c;
+            for (int l = 0; l < m; l++)
+                for (int a = 1; a < mono[l].second; a++) cp = B.job(cp, mono[l].first);
+            for (int l = 0; l < m; l++) S.max_weight = std::max(S.max_weight, mono[l].second);
+            if (m == 1) {
+                lists[i].emplace_back(B.job(cp, mono[0].first), 1);
+                jac(i, mono[0].first).emplace_back(cp, mono[0].second);
+                continue;
+            }
+            f.assign(m + 1, -1);
+            f[1] = B.job(cp, mono[0].first);
+            for (int l = 2; l <= m; l++) f[l] = B.job(f[l - 1], mono[l - 1].first);
+            lists[i].emplace_back(f[m], 1);
+            Bk.assign(m - 1, -1);
+            Bk[0] = mono[m - 1].first;  // B_0 = x_{v_m}
+            for (int k = 1; k <= m - 2; k++) Bk[k] = B.job(Bk[k - 1], mono[m - 1 - k].first);
+            // d_1 = c' * B_{m-2}
+            jac(i, mono[0].first).emplace_back(B.job(cp, Bk[m - 2]), mono[0].second);
+            for (int l = 2; l <= m - 1; l++)
+                jac(i, mono[l - 1].first).emplace_back(B.job(f[l - 1], Bk[m - l - 1]), mono[l - 1].second);
+            jac(i, mono[m - 1].first).emplace_back(f[m - 1], mono[m - 1].second);
+        }
+    }
+    S.nslots = (int64_t)B.level.size();
+    if (S.nslots > INT32_MAX) { err = "too many series (slots overflow int32)"; return false; }
+    S.task_ptr.assign((size_t)ntasks + 1, 0);
+    S.ent_slot.clear();
+    S.ent_w.clear();
+    for (int64_t t = 0; t < ntasks; t++) {
+        for (auto &e : lists[(size_t)t]) {
+            S.ent_slot.push_back(e.first);
+            S.ent_w.push_back(e.second);
+        }
+        if (S.ent_slot.size() > (size_t)INT32_MAX) { err = "too many addition terms"; return false; }
+        S.task_ptr[(size_t)t + 1] = (int32_t)S.ent_slot.size();
+    }
+    return true;
+}
+
+}  // namespace mdps

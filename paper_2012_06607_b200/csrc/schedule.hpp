@@ -1,0 +1,39 @@
+// schedule.hpp — host-side job DAG for mdps_eval_diff.
+//
+// Per monomial c * prod_l x_{v_l}^{a_l} (variables ascending)
+// the product jobs of algorithmic differentiation (all n
+// partials at ~3x the cost of one evaluation):
+//   common factor  c' = c * prod_l x_{v_l}^{a_l - 1}     (only when some a_l >= 2)
+//   forward        f_1 = c' x_{v_1},  f_l = f_{l-1} x_{v_l};  value = f_m
+//   backward       B_0 = x_{v_m} (alias),  B_k = B_{k-1} x_{v_{m-k}},  k = 1..m-2
+//   cross          d_1 = c' B_{m-2},  d_l = f_{l-1} B_{m-l-1} (l = 2..m-1),  d_m = f_{m-1}
+//   weights        J[i][v_l] += a_l * d_l                  (folded into the sums)
+// 3(m-1) + sum_l (a_l - 1) products for m >= 2 (1 + sum for m = 1).  A job's
+// level is 1 + the max level of its inputs (x and c are level 0); each level
+// is one launch (the GPU analogue of the paper's stage synchronisation,
+// PAPER.md:420-424).  The addition jobs are a CSR list per
+// output series: n values then n*n Jacobian entries (row-major).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace mdps {
+
+struct Schedule {
+    int n = 0, D = 0, L = 0, M = 0;
+    int64_t nslots = 0;                         // n + M + jobs
+    std::vector<std::vector<int32_t>> levels;   // per level: (in1, in2, out) triples
+    std::vector<int32_t> task_ptr;              // [n + n*n + 1]
+    std::vector<int32_t> ent_slot, ent_w;       // addition terms
+    int64_t products = 0;
+    int32_t max_weight = 1;
+};
+
+// Validates the inputs (libmdps.h) and builds the schedule.  Pool slots:
+// [0, n) = x, [n, n+M) = coefficients, then one slot per product job.
+bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mono_ptr,
+                    const int32_t *vars, const int32_t *exps, int32_t n, Schedule &S,
+                    std::string &err);
+
+}  // namespace mdps
