@@ -1,0 +1,276 @@
+// conv_dig.cuh — the product-job kernel on digit planes (MDPS_ALGO_DIGITS):
+// z = x * y mod t^D for every job of one DAG level.
+//
+// See kernels_dig.cuh for the digit representation.  Mapping:
+//  * P jobs per block; per job T = ceil(D/2) output pairs x F splits.  Thread
+//    (t, f) owns outputs k1 = t and k2 = D-1-t — the folded triangle has
+//    exactly D+1 terms per pair, so no lane idles — and the fold iterations
+//    j = f, f+F, ... (the F lanes of a pair are adjacent lanes of one warp).
+//  * Two passes (real part, imaginary part): each keeps S digit accumulators
+//    and the 2S digits of the operand x_i in registers and streams the 2S
+//    digits of y_{k-i} from shared memory: per digit pair one DFMA.
+//  * Alignment: a term whose exponent is delta digits below the accumulator
+//    anchor reads y's digit plane l - delta.  Shared memory holds PADZ zero
+//    planes in front of y's planes, so for delta <= PADZ (the common case,
+//    checked warp-uniformly) every load is base + compile-time offset; larger
+//    shifts take a select-based path.  A term with a zero operand part is
+//    read at delta = 0 (its product is zero anyway).
+//  * Partials: the k1 partial is parked in shared memory when a lane crosses
+//    the fold (lanes cross at different iterations); the k2 partials are
+//    added with warp shuffles.  All additions are exact (integer digits).
+//  * Shared memory per job: x planes [S][2][D], y planes [PADZ+S][2][D]
+//    (part-interleaved so the zero planes are shared), exponents [2][2][D];
+//    per thread a parking slot of S doubles.
+#pragma once
+#include "kernels_dig.cuh"
+
+namespace mdps {
+
+constexpr int PADZ = 4;
+
+__host__ __device__ inline size_t conv_dig_smem(int S, int D, int P, int threads) {
+    const size_t per_job = (size_t)2 * S * D + (size_t)2 * (PADZ + S) * D;  // doubles
+    return (size_t)P * per_job * sizeof(double) + (size_t)threads * S * sizeof(double) +
+           (size_t)P * 4 * D * sizeof(int);
+}
+
+// one product pass over this thread's fold iterations
+template <int L, int DT, int PART>
+__device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, const double *__restrict__ sy,
+                                              const int *__restrict__ ex, const int *__restrict__ ey, int Drt,
+                                              int t, int f, int F, int eacc1, int eacc2, double (&A)[digits_for(L)],
+                                              double *park) {
+    constexpr int S = digits_for(L);
+    constexpr int NORM = norm_every(S);
+    const int D = DT > 0 ? DT : Drt;
+    const int D2 = 2 * D;
+    // PART 0 (re): Ur*Wr - Ui*Wi ;  PART 1 (im): Ur*Wi + Ui*Wr
+    constexpr int w1part = PART == 0 ? 0 : 1, w2part = PART == 0 ? 1 : 0;
+    md_zero(A);
+    int cnt = 0;
+    bool switched = false;
+    for (int j = f; j <= D; j += F) {
+        const bool first = j <= t;
+        if (!first && !switched) {  // k1 partial complete: park it, start k2
+            switched = true;
+            carry_normalize(A);
+#pragma unroll
+            for (int s = 0; s < S; s++) {
+                park[s] = A[s];
+                A[s] = 0.0;
+            }
+            cnt = 0;
+        }
+        const int i = first ? j : j - t - 1;
+        const int kk = (first ? t : D - 1 - t) - i;
+        const int eacc = first ? eacc1 : eacc2;
+        double Ur[S], Ui[S];
+        const double *ux = sx + i;
+#pragma unroll
+        for (int s = 0; s < S; s++) {
+            Ur[s] = ux[(2 * s) * D];
+            Ui[s] = ux[(2 * s + 1) * D];
+        }
+        const int exr = ex[i], exi = ex[D + i];
+        const int ey1 = ey[w1part * D + kk], ey2 = ey[w2part * D + kk];
+        int d1 = eacc - exr - ey1, d2 = eacc - exi - ey2;
+        if (exr + ey1 <= ZERO_E / 2) d1 = 0;  // zero product: any plane will do
+        if (exi + ey2 <= ZERO_E / 2) d2 = 0;
+        const bool fast = d1 <= PADZ && d2 <= PADZ;
+        if (__all_sync(__activemask(), fast)) {
+            const double *W1 = sy + (PADZ - d1) * D2 + w1part * D + kk;
+            const double *W2 = sy + (PADZ - d2) * D2 + w2part * D + kk;
+#pragma unroll
+            for (int l = 0; l < S; l++) {
+                const double w1 = W1[l * D2];
+                const double w2 = W2[l * D2];
+#pragma unroll
+                for (int u = 0; u < S - l; u++) {
+                    A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
+                    A[u + l] = __fma_rn(PART == 0 ? -Ui[u] : Ui[u], w2, A[u + l]);
+                }
+            }
+        } else {
+            const double *W1 = sy + w1part * D + kk;
+            const double *W2 = sy + w2part * D + kk;
+#pragma unroll
+            for (int l = 0; l < S; l++) {
+                const double w1 = (l >= d1) ? W1[(PADZ + l - d1) * D2] : 0.0;
+                const double w2 = (l >= d2) ? W2[(PADZ + l - d2) * D2] : 0.0;
+#pragma unroll
+                for (int u = 0; u < S - l; u++) {
+                    A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
+                    A[u + l] = __fma_rn(PART == 0 ? -Ui[u] : Ui[u], w2, A[u + l]);
+                }
+            }
+        }
+        if (++cnt == NORM) {
+            carry_normalize(A);
+            cnt = 0;
+        }
+    }
+    carry_normalize(A);
+    if (!switched) {  // no k2 iterations on this lane: everything belongs to k1
+#pragma unroll
+        for (int s = 0; s < S; s++) {
+            park[s] = A[s];
+            A[s] = 0.0;
+        }
+    }
+}
+
+// normalise, leading-zero shift, write digits and exponent of one (k, part)
+template <int L>
+__device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int eacc, double *zd, int *ze, int D,
+                                              int k, int part) {
+    constexpr int S = digits_for(L);
+    carry_normalize(A);
+    // Z = [c2, c1, c0, A_1 .. A_{S-1}], Z_u has weight R^(eacc - u)
+    double Z[S + 2];
+    {
+        double a0 = A[0];
+        const double c2 = rint_magic(__dmul_rn(a0, INV_RADIX * INV_RADIX));
+        a0 = __fma_rn(-c2, RADIX * RADIX, a0);
+        const double c1 = rint_magic(__dmul_rn(a0, INV_RADIX));
+        const double c0 = __fma_rn(-c1, RADIX, a0);
+        Z[0] = c2;
+        Z[1] = c1;
+        Z[2] = c0;
+#pragma unroll
+        for (int s = 1; s < S; s++) Z[s + 2] = A[s];
+    }
+    int z0 = S + 2;
+#pragma unroll
+    for (int u = S + 1; u >= 0; u--)
+        if (Z[u] != 0.0) z0 = u;
+#pragma unroll
+    for (int b = 0; b < 6; b++) {  // shift left by z0 (< 64)
+        const int sh = 1 << b;
+        if (z0 & sh) {
+#pragma unroll
+            for (int u = 0; u < S + 2; u++) Z[u] = (u + sh < S + 2) ? Z[u + sh] : 0.0;
+        }
+    }
+    const int e = (z0 >= S + 2 || eacc <= ZERO_E / 2) ? ZERO_E : eacc + 1 - z0;
+#pragma unroll
+    for (int s = 0; s < S; s++) zd[(part * S + s) * D + k] = (e == ZERO_E) ? 0.0 : Z[s];
+    ze[part * D + k] = e;
+}
+
+template <int L, int DT>
+__global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
+                                                      const int *__restrict__ jobs, int njobs, int Drt, int T,
+                                                      int F, int P) {
+    constexpr int S = digits_for(L);
+    const int D = DT > 0 ? DT : Drt;
+    const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
+    const int threads_per_job = T * F;
+    extern __shared__ double sm[];
+    double *sdig = sm;                                        // [P][SX + SY]
+    double *spark = sm + (size_t)P * (SX + SY);               // [threads][S]
+    int *sexp = (int *)(spark + (size_t)blockDim.x * S);      // [P][2 series][2][D]
+
+    const int job0 = blockIdx.x * P;
+    // stage: x planes -> [s][part][D], y planes -> [PADZ + s][part][D], zero planes
+    for (int idx = threadIdx.x; idx < P * 2 * 2 * S * D; idx += blockDim.x) {
+        const int per_job = 2 * 2 * S * D;
+        const int jl = idx / per_job, r = idx - jl * per_job;
+        const int which = r / (2 * S * D), r2 = r - which * 2 * S * D;  // r2 = (part*S + s)*D + k
+        const int ps = r2 / D, k = r2 - ps * D;
+        const int part = ps / S, s = ps - part * S;
+        const int job = min(job0 + jl, njobs - 1);
+        const int src = jobs[3 * job + which];
+        const double v = dpool[(size_t)src * 2 * S * D + r2];
+        double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
+                                                               : (s * 2 + part) * D);
+        dst[k] = v;
+    }
+    for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {
+        const int jl = idx / (2 * PADZ * D), r = idx - jl * 2 * PADZ * D;
+        sdig[(size_t)jl * (SX + SY) + SX + r] = 0.0;
+    }
+    for (int idx = threadIdx.x; idx < P * 2 * 2 * D; idx += blockDim.x) {
+        const int jl = idx / (4 * D), r = idx - jl * 4 * D;
+        const int which = r / (2 * D), r2 = r - which * 2 * D;
+        const int job = min(job0 + jl, njobs - 1);
+        sexp[idx] = epool[(size_t)jobs[3 * job + which] * 2 * D + r2];
+    }
+    __syncthreads();
+
+    const int jl = threadIdx.x / threads_per_job;
+    const int r = threadIdx.x - jl * threads_per_job;
+    const int t = r / F, f = r - t * F;
+    const double *sx = sdig + (size_t)jl * (SX + SY), *sy = sx + SX;
+    const int *ex = sexp + jl * 4 * D, *ey = ex + 2 * D;
+
+    // exponent pre-pass (split over the F lanes, max-reduced by shuffles):
+    // anchors e_acc of (k1, k2) x (re, im) over ALL terms of each output
+    int ea1r = ZERO_E, ea1i = ZERO_E, ea2r = ZERO_E, ea2i = ZERO_E;
+    for (int j = f; j <= D; j += F) {
+        const bool first = j <= t;
+        const int i = first ? j : j - t - 1;
+        const int kk = (first ? t : D - 1 - t) - i;
+        const int xr = ex[i], xi = ex[D + i], yr = ey[kk], yi = ey[D + kk];
+        const int er = max(xr + yr, xi + yi), ei = max(xr + yi, xi + yr);
+        if (first) {
+            ea1r = max(ea1r, er);
+            ea1i = max(ea1i, ei);
+        } else {
+            ea2r = max(ea2r, er);
+            ea2i = max(ea2i, ei);
+        }
+    }
+    for (int off = F >> 1; off > 0; off >>= 1) {
+        ea1r = max(ea1r, __shfl_xor_sync(0xffffffffu, ea1r, off));
+        ea1i = max(ea1i, __shfl_xor_sync(0xffffffffu, ea1i, off));
+        ea2r = max(ea2r, __shfl_xor_sync(0xffffffffu, ea2r, off));
+        ea2i = max(ea2i, __shfl_xor_sync(0xffffffffu, ea2i, off));
+    }
+    ea1r = max(ea1r, ZERO_E);
+    ea1i = max(ea1i, ZERO_E);
+    ea2r = max(ea2r, ZERO_E);
+    ea2i = max(ea2i, ZERO_E);
+
+    double *park = spark + (size_t)threadIdx.x * S;
+    const int job = job0 + jl;
+    const bool writer = job < njobs;
+    double *zd = dpool;
+    int *ze = epool;
+    if (writer) {
+        const int out = jobs[3 * job + 2];
+        zd = dpool + (size_t)out * 2 * S * D;
+        ze = epool + (size_t)out * 2 * D;
+    }
+    const int k1 = t, k2 = D - 1 - t;
+#pragma unroll 1
+    for (int part = 0; part < 2; part++) {
+        double A[S];
+        const int e1 = part ? ea1i : ea1r, e2 = part ? ea2i : ea2r;
+        if (part == 0)
+            conv_dig_pass<L, DT, 0>(sx, sy, ex, ey, D, t, f, F, e1, e2, A, park);
+        else
+            conv_dig_pass<L, DT, 1>(sx, sy, ex, ey, D, t, f, F, e1, e2, A, park);
+        // k2: sum the F lanes' partials (exact) with shuffles
+        for (int off = F >> 1; off > 0; off >>= 1) {
+#pragma unroll
+            for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
+        }
+        __syncwarp();
+        if (writer) {
+            if (f == (F > 1 ? 1 : 0) && k2 != k1) conv_dig_emit<L>(A, e2, zd, ze, D, k2, part);
+            if (f == 0) {  // k1: the F parked partials of this pair
+                double B[S];
+#pragma unroll
+                for (int s = 0; s < S; s++) B[s] = park[s];
+                for (int g = 1; g < F; g++) {
+#pragma unroll
+                    for (int s = 0; s < S; s++) B[s] = __dadd_rn(B[s], park[g * S + s]);
+                }
+                conv_dig_emit<L>(B, e1, zd, ze, D, k1, part);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace mdps

@@ -165,232 +165,6 @@ __global__ void __launch_bounds__(128) to_digits_kernel(const double *__restrict
 }
 
 // ---------------------------------------------------------------------------
-// conv_dig: product jobs z = x * y mod t^D on digit planes.
-// Threads: P jobs per block; per job T = ceil(D/2) output pairs x F splits.
-// Thread (t, f) owns outputs k1 = t and k2 = D-1-t (the folded triangle has
-// D+1 terms for every t) and the fold iterations j = f, f+F, ...; the F
-// partial accumulators of an output are added exactly at the end.
-// Shared memory per job: x and y digit planes [2][S][D+1] (+1 skews banks),
-// exponents [2][2][D]; then per thread parking (k1) and final (k2) partials.
-struct ConvDigGeom {
-    int T, F, P, threads;
-};
-
-__host__ __device__ inline size_t conv_dig_smem(int S, int D, int P, int threads) {
-    const size_t ser = (size_t)2 * S * (D + 1);
-    return (size_t)P * (2 * ser) * sizeof(double) + (size_t)threads * 2 * S * sizeof(double) +
-           (size_t)P * 4 * D * sizeof(int) + 16;
-}
-
-template <int L, int PART>
-__device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, const double *__restrict__ sy,
-                                              const int *__restrict__ ex, const int *__restrict__ ey,
-                                              const double *zero, int D, int t, int f, int F, int eacc1,
-                                              int eacc2, double *park, double *fin) {
-    constexpr int S = digits_for(L);
-    constexpr int NORM = norm_every(S);
-    const int PD = D + 1;
-    double A[S];
-    md_zero(A);
-    int cnt = 0;
-    bool switched = false;
-    for (int j = f; j <= D; j += F) {
-        const bool first = j <= t;
-        if (!first && !switched) {  // k1 partial complete: park it, start k2
-            switched = true;
-            carry_normalize(A);
-#pragma unroll
-            for (int s = 0; s < S; s++) {
-                park[s] = A[s];
-                A[s] = 0.0;
-            }
-            cnt = 0;
-        }
-        const int i = first ? j : j - t - 1;
-        const int k = first ? t : D - 1 - t;
-        const int kk = k - i;
-        const int eacc = first ? eacc1 : eacc2;
-        // operand U = x_i (registers), W = y_{k-i} (shifted through addresses)
-        double Ur[S], Ui[S];
-#pragma unroll
-        for (int s = 0; s < S; s++) {
-            Ur[s] = sx[s * PD + i];
-            Ui[s] = sx[(S + s) * PD + i];
-        }
-        // PART 0 (re): Ur*Wr - Ui*Wi ;  PART 1 (im): Ur*Wi + Ui*Wr
-        const int w1part = PART == 0 ? 0 : 1, w2part = PART == 0 ? 1 : 0;
-        const int d1 = eacc - ex[i] - ey[w1part * D + kk];
-        const int d2 = eacc - ex[D + i] - ey[w2part * D + kk];
-        const double *W1 = sy + w1part * S * PD + kk;
-        const double *W2 = sy + w2part * S * PD + kk;
-#pragma unroll
-        for (int l = 0; l < S; l++) {
-            const double w1 = *((l >= d1) ? W1 + (l - d1) * PD : zero);
-            const double w2 = *((l >= d2) ? W2 + (l - d2) * PD : zero);
-#pragma unroll
-            for (int u = 0; u < S - l; u++) {
-                A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
-                A[u + l] = __fma_rn(PART == 0 ? -Ui[u] : Ui[u], w2, A[u + l]);
-            }
-        }
-        if (++cnt == NORM) {
-            carry_normalize(A);
-            cnt = 0;
-        }
-    }
-    carry_normalize(A);
-    if (!switched) {  // no k2 iterations: everything belongs to k1
-#pragma unroll
-        for (int s = 0; s < S; s++) {
-            park[s] = A[s];
-            fin[s] = 0.0;
-        }
-    } else {
-#pragma unroll
-        for (int s = 0; s < S; s++) fin[s] = A[s];
-    }
-}
-
-// sum the F partials (stride 2S*? handled by caller), normalise, write the
-// output digits (leading-zero shift) and exponent of one (k, part)
-template <int L>
-__device__ __forceinline__ void conv_dig_emit(const double *parts, int pstride, int F, int eacc,
-                                              double *zd, int *ze, int D, int k, int part) {
-    constexpr int S = digits_for(L);
-    double A[S];
-#pragma unroll
-    for (int s = 0; s < S; s++) A[s] = parts[s];
-    for (int g = 1; g < F; g++) {
-#pragma unroll
-        for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], parts[g * pstride + s]);
-    }
-    carry_normalize(A);
-    // Z = [c2, c1, c0, A_1 .. A_{S-1}], Z_u has weight R^(eacc - u)
-    double Z[S + 2];
-    {
-        double a0 = A[0];
-        const double c2 = rint_magic(__dmul_rn(a0, INV_RADIX * INV_RADIX));
-        a0 = __fma_rn(-c2, RADIX * RADIX, a0);
-        const double c1 = rint_magic(__dmul_rn(a0, INV_RADIX));
-        const double c0 = __fma_rn(-c1, RADIX, a0);
-        Z[0] = c2;
-        Z[1] = c1;
-        Z[2] = c0;
-#pragma unroll
-        for (int s = 1; s < S; s++) Z[s + 2] = A[s];
-    }
-    int z0 = S + 2;
-#pragma unroll
-    for (int u = S + 1; u >= 0; u--)
-        if (Z[u] != 0.0) z0 = u;
-    // shift left by z0 (barrel: z0 < 64)
-#pragma unroll
-    for (int b = 0; b < 6; b++) {
-        const int sh = 1 << b;
-        if (z0 & sh) {
-#pragma unroll
-            for (int u = 0; u < S + 2; u++) Z[u] = (u + sh < S + 2) ? Z[u + sh] : 0.0;
-        }
-    }
-    const int e = (z0 >= S + 2 || eacc <= ZERO_E / 2) ? ZERO_E : eacc + 1 - z0;
-#pragma unroll
-    for (int s = 0; s < S; s++) zd[(part * S + s) * D + k] = (e == ZERO_E) ? 0.0 : Z[s];
-    ze[part * D + k] = e;
-}
-
-template <int L>
-__global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
-                                                      const int *__restrict__ jobs, int njobs, int D,
-                                                      int T, int F, int P) {
-    constexpr int S = digits_for(L);
-    const int PD = D + 1;
-    const int SER = 2 * S * PD;  // doubles per staged series
-    const int threads_per_job = T * F;
-    extern __shared__ double sm[];
-    double *sdig = sm;                                              // [P][2][SER]
-    double *spart = sm + (size_t)P * 2 * SER;                       // [threads][2][S]
-    int *sexp = (int *)(spart + (size_t)blockDim.x * 2 * S);        // [P][2 series][2][D]
-    double *zero = (double *)(sexp + (size_t)P * 4 * D);            // one zero (aligned: D ints * 4P)
-
-    const int job0 = blockIdx.x * P;
-    // stage digit planes and exponents of both inputs of every job
-    for (int idx = threadIdx.x; idx < P * 2 * 2 * S * D; idx += blockDim.x) {
-        const int per_job = 2 * 2 * S * D;
-        const int jl = idx / per_job, r = idx - jl * per_job;
-        const int which = r / (2 * S * D), r2 = r - which * 2 * S * D;  // r2 = plane * D + k
-        const int plane = r2 / D, k = r2 - plane * D;
-        const int job = min(job0 + jl, njobs - 1);
-        const int src = jobs[3 * job + which];
-        sdig[(size_t)jl * 2 * SER + which * SER + plane * PD + k] = dpool[(size_t)src * 2 * S * D + r2];
-    }
-    for (int idx = threadIdx.x; idx < P * 2 * 2 * D; idx += blockDim.x) {
-        const int jl = idx / (4 * D), r = idx - jl * 4 * D;
-        const int which = r / (2 * D), r2 = r - which * 2 * D;
-        const int job = min(job0 + jl, njobs - 1);
-        const int src = jobs[3 * job + which];
-        sexp[idx] = epool[(size_t)src * 2 * D + r2];
-    }
-    if (threadIdx.x == 0) *zero = 0.0;
-    __syncthreads();
-
-    const int jl = threadIdx.x / threads_per_job;
-    const int r = threadIdx.x - jl * threads_per_job;
-    const int t = r / F, f = r - t * F;
-    const bool valid = jl < P && t < T;
-    const int jlc = valid ? jl : 0;
-    const double *sx = sdig + (size_t)jlc * 2 * SER, *sy = sx + SER;
-    const int *ex = sexp + jlc * 4 * D, *ey = ex + 2 * D;
-    const int tt = valid ? t : 0;
-
-    // exponent pre-pass: e_acc of (k1, k2) x (re, im) over ALL terms
-    int ea1r = ZERO_E, ea1i = ZERO_E, ea2r = ZERO_E, ea2i = ZERO_E;
-    for (int j = 0; j <= D; j++) {
-        const bool first = j <= tt;
-        const int i = first ? j : j - tt - 1;
-        const int k = first ? tt : D - 1 - tt;
-        const int kk = k - i;
-        const int xr = ex[i], xi = ex[D + i], yr = ey[kk], yi = ey[D + kk];
-        const int er = max(xr + yr, xi + yi), ei = max(xr + yi, xi + yr);
-        if (first) {
-            ea1r = max(ea1r, er);
-            ea1i = max(ea1i, ei);
-        } else {
-            ea2r = max(ea2r, er);
-            ea2i = max(ea2i, ei);
-        }
-    }
-
-    double *park = spart + (size_t)threadIdx.x * 2 * S;
-    double *fin = park + S;
-    const int job = job0 + jl;
-    double *zd = nullptr;
-    int *ze = nullptr;
-    if (valid && job < njobs) {
-        const int out = jobs[3 * job + 2];
-        zd = dpool + (size_t)out * 2 * S * D;
-        ze = epool + (size_t)out * 2 * D;
-    }
-#pragma unroll 1
-    for (int part = 0; part < 2; part++) {
-        if (valid) {
-            if (part == 0)
-                conv_dig_pass<L, 0>(sx, sy, ex, ey, zero, D, tt, f, F, ea1r, ea2r, park, fin);
-            else
-                conv_dig_pass<L, 1>(sx, sy, ex, ey, zero, D, tt, f, F, ea1i, ea2i, park, fin);
-        }
-        __syncthreads();
-        if (valid && job < njobs) {
-            // thread f == 0 emits k1, f == F-1 (or the same thread) emits k2
-            const double *base = spart + (size_t)(threadIdx.x - f) * 2 * S;
-            if (f == 0) conv_dig_emit<L>(base, 2 * S, F, part ? ea1i : ea1r, zd, ze, D, tt, part);
-            if (f == F - 1 && D - 1 - tt != tt)
-                conv_dig_emit<L>(base + S, 2 * S, F, part ? ea2i : ea2r, zd, ze, D, D - 1 - tt, part);
-        }
-        __syncthreads();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // accum_dig: addition jobs on digit planes -> limb outputs.
 // one thread per (task, k); two parts.
 template <int L>

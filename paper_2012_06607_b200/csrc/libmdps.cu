@@ -11,6 +11,7 @@
 
 #include "../../include/libmdps.h"
 #include "../../include/mdps_test.h"
+#include "conv_dig.cuh"
 #include "kernels_dig.cuh"
 #include "kernels_eft.cuh"
 #include "schedule.hpp"
@@ -106,7 +107,10 @@ struct ConvDig {
     static int run(double *dpool, int *epool, const int *jobs, int njobs, int D, cudaStream_t st) {
         if (njobs <= 0) return MDPS_OK;
         DigGeom g = dig_geom(L, D);
-        auto kern = conv_dig_kernel<L>;
+        // compile-time D for the configs' degrees: shared-memory offsets become immediates
+        void (*kern)(double *, int *, const int *, int, int, int, int, int) =
+            D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> :
+            D == 64 ? conv_dig_kernel<L, 64> : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
         kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, jobs, njobs, D, g.T, g.F, g.P);
