@@ -35,17 +35,20 @@ __host__ __device__ inline size_t conv_dig_smem(int S, int D, int P, int threads
 }
 
 // one product pass over this thread's fold iterations
-template <int L, int DT, int PART>
+template <int L, int DT>
 __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, const double *__restrict__ sy,
                                               const int *__restrict__ ex, const int *__restrict__ ey, int Drt,
-                                              int t, int f, int F, int eacc1, int eacc2, double (&A)[digits_for(L)],
-                                              double *park) {
+                                              int part, int t, int f, int F, int eacc1, int eacc2,
+                                              double (&A)[digits_for(L)], double *park) {
     constexpr int S = digits_for(L);
     constexpr int NORM = norm_every(S);
     const int D = DT > 0 ? DT : Drt;
     const int D2 = 2 * D;
-    // PART 0 (re): Ur*Wr - Ui*Wi ;  PART 1 (im): Ur*Wi + Ui*Wr
-    constexpr int w1part = PART == 0 ? 0 : 1, w2part = PART == 0 ? 1 : 0;
+    // part 0 (re): Ur*Wr - Ui*Wi ;  part 1 (im): Ur*Wi + Ui*Wr.  One code
+    // copy serves both passes (instruction-cache footprint): the part only
+    // selects the y planes and the sign applied to Ui (a sign-bit flip).
+    const int w1part = part, w2part = 1 - part;
+    const long long sgn = part == 0 ? (long long)0x8000000000000000ULL : 0LL;
     md_zero(A);
     int cnt = 0;
     bool switched = false;
@@ -69,7 +72,7 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
 #pragma unroll
         for (int s = 0; s < S; s++) {
             Ur[s] = ux[(2 * s) * D];
-            Ui[s] = ux[(2 * s + 1) * D];
+            Ui[s] = __longlong_as_double(__double_as_longlong(ux[(2 * s + 1) * D]) ^ sgn);
         }
         const int exr = ex[i], exi = ex[D + i];
         const int ey1 = ey[w1part * D + kk], ey2 = ey[w2part * D + kk];
@@ -87,7 +90,7 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
-                    A[u + l] = __fma_rn(PART == 0 ? -Ui[u] : Ui[u], w2, A[u + l]);
+                    A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
             }
         } else {
@@ -100,7 +103,7 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
-                    A[u + l] = __fma_rn(PART == 0 ? -Ui[u] : Ui[u], w2, A[u + l]);
+                    A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
             }
         }
@@ -165,25 +168,34 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
     const int D = DT > 0 ? DT : Drt;
     const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
     const int threads_per_job = T * F;
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
     double *sdig = sm;                                        // [P][SX + SY]
     double *spark = sm + (size_t)P * (SX + SY);               // [threads][S]
     int *sexp = (int *)(spark + (size_t)blockDim.x * S);      // [P][2 series][2][D]
 
     const int job0 = blockIdx.x * P;
-    // stage: x planes -> [s][part][D], y planes -> [PADZ + s][part][D], zero planes
-    for (int idx = threadIdx.x; idx < P * 2 * 2 * S * D; idx += blockDim.x) {
-        const int per_job = 2 * 2 * S * D;
-        const int jl = idx / per_job, r = idx - jl * per_job;
-        const int which = r / (2 * S * D), r2 = r - which * 2 * S * D;  // r2 = (part*S + s)*D + k
-        const int ps = r2 / D, k = r2 - ps * D;
-        const int part = ps / S, s = ps - part * S;
-        const int job = min(job0 + jl, njobs - 1);
-        const int src = jobs[3 * job + which];
-        const double v = dpool[(size_t)src * 2 * S * D + r2];
-        double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
-                                                               : (s * 2 + part) * D);
-        dst[k] = v;
+    // stage: x planes -> [s][part][D], y planes -> [PADZ + s][part][D], zero
+    // planes.  One warp per plane row (the source slot is warp-uniform),
+    // 16-byte vector loads when D is even.
+    {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+        const int nrows = P * 4 * S;  // (job, which, part*S + s)
+#pragma unroll 2
+        for (int row = warp; row < nrows; row += nwarps) {
+            const int jl = row / (4 * S), rem = row - jl * 4 * S;
+            const int which = rem / (2 * S), ps = rem - which * 2 * S;
+            const int part = ps / S, s = ps - part * S;
+            const int job = min(job0 + jl, njobs - 1);
+            const double *g = dpool + (size_t)jobs[3 * job + which] * 2 * S * D + (size_t)ps * D;
+            double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
+                                                                   : (s * 2 + part) * D);
+            if ((D & 1) == 0) {
+                for (int k = 2 * lane; k < D; k += 64)
+                    *reinterpret_cast<double2 *>(dst + k) = __ldg(reinterpret_cast<const double2 *>(g + k));
+            } else {
+                for (int k = lane; k < D; k += 32) dst[k] = __ldg(g + k);
+            }
+        }
     }
     for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {
         const int jl = idx / (2 * PADZ * D), r = idx - jl * 2 * PADZ * D;
@@ -200,8 +212,9 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
     const int jl = threadIdx.x / threads_per_job;
     const int r = threadIdx.x - jl * threads_per_job;
     const int t = r / F, f = r - t * F;
-    const double *sx = sdig + (size_t)jl * (SX + SY), *sy = sx + SX;
-    const int *ex = sexp + jl * 4 * D, *ey = ex + 2 * D;
+    const int jlc = min(jl, P - 1);  // padding lanes (blockDim rounded to whole warps) shadow the last job
+    const double *sx = sdig + (size_t)jlc * (SX + SY), *sy = sx + SX;
+    const int *ex = sexp + jlc * 4 * D, *ey = ex + 2 * D;
 
     // exponent pre-pass (split over the F lanes, max-reduced by shuffles):
     // anchors e_acc of (k1, k2) x (re, im) over ALL terms of each output
@@ -233,7 +246,7 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
 
     double *park = spark + (size_t)threadIdx.x * S;
     const int job = job0 + jl;
-    const bool writer = job < njobs;
+    const bool writer = jl < P && job < njobs;
     double *zd = dpool;
     int *ze = epool;
     if (writer) {
@@ -246,10 +259,7 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
     for (int part = 0; part < 2; part++) {
         double A[S];
         const int e1 = part ? ea1i : ea1r, e2 = part ? ea2i : ea2r;
-        if (part == 0)
-            conv_dig_pass<L, DT, 0>(sx, sy, ex, ey, D, t, f, F, e1, e2, A, park);
-        else
-            conv_dig_pass<L, DT, 1>(sx, sy, ex, ey, D, t, f, F, e1, e2, A, park);
+        conv_dig_pass<L, DT>(sx, sy, ex, ey, D, part, t, f, F, e1, e2, A, park);
         // k2: sum the F lanes' partials (exact) with shuffles
         for (int off = F >> 1; off > 0; off >>= 1) {
 #pragma unroll

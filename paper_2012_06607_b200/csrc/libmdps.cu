@@ -79,7 +79,8 @@ static DigGeom dig_geom(int L, int D) {
     g.F = F;
     g.P = std::max(1, 128 / (g.T * g.F));
     for (;;) {
-        g.threads = g.P * g.T * g.F;
+        // whole warps: the kernel's shuffles and votes use full-warp masks
+        g.threads = (g.P * g.T * g.F + 31) / 32 * 32;
         g.smem = conv_dig_smem(S, D, g.P, g.threads);
         if (g.smem <= 110 * 1024 || g.P == 1) break;
         g.P /= 2;
