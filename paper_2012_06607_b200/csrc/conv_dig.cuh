@@ -31,7 +31,40 @@ constexpr int PADZ = 4;
 __host__ __device__ inline size_t conv_dig_smem(int S, int D, int P, int threads) {
     const size_t per_job = (size_t)2 * S * D + (size_t)2 * (PADZ + S) * D;  // doubles
     return (size_t)P * per_job * sizeof(double) + (size_t)threads * S * sizeof(double) +
-           (size_t)P * 4 * D * sizeof(int);
+           (size_t)P * 4 * D * sizeof(int) + 16;  // + mbarrier
+}
+
+// ---- TMA bulk copies (cp.async.bulk) with an mbarrier, single CTA ----------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
 }
 
 // one product pass over this thread's fold iterations
@@ -175,9 +208,31 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
 
     const int job0 = blockIdx.x * P;
     // stage: x planes -> [s][part][D], y planes -> [PADZ + s][part][D], zero
-    // planes.  One warp per plane row (the source slot is warp-uniform),
-    // 16-byte vector loads when D is even.
-    {
+    // planes.  Even D: every plane row is a 16-byte aligned contiguous run in
+    // both places, so warp 0 issues one TMA bulk copy (cp.async.bulk) per row
+    // against an mbarrier while the other warps write the zero planes and
+    // exponents.  Odd D: one warp per row, scalar loads.
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sexp + (size_t)P * 4 * D);
+    const bool use_tma = (D & 1) == 0;
+    if (use_tma) {
+        if (threadIdx.x == 0) mbar_init(bar, 1);
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int nrows = P * 4 * S;
+            if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(nrows * D * 8));
+            __syncwarp();
+            for (int row = threadIdx.x; row < nrows; row += 32) {
+                const int jl = row / (4 * S), rem = row - jl * 4 * S;
+                const int which = rem / (2 * S), ps = rem - which * 2 * S;
+                const int part = ps / S, s = ps - part * S;
+                const int job = min(job0 + jl, njobs - 1);
+                const double *g = dpool + (size_t)jobs[3 * job + which] * 2 * S * D + (size_t)ps * D;
+                double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
+                                                                       : (s * 2 + part) * D);
+                bulk_g2s(dst, g, (unsigned)(D * 8), bar);
+            }
+        }
+    } else {
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
         const int nrows = P * 4 * S;  // (job, which, part*S + s)
 #pragma unroll 2
@@ -207,6 +262,7 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
         const int job = min(job0 + jl, njobs - 1);
         sexp[idx] = epool[(size_t)jobs[3 * job + which] * 2 * D + r2];
     }
+    if (use_tma) mbar_wait(bar, 0);
     __syncthreads();
 
     const int jl = threadIdx.x / threads_per_job;

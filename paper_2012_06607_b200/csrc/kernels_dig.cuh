@@ -51,9 +51,12 @@ __host__ __device__ constexpr int digits_for(int L) {
     while ((S - 2) * BETA < 53 * L + 8) S++;
     return S;
 }
-// terms between carry normalisations: 2 S (2^BETA)^2 per term per digit,
-// accumulators balanced to R/2 after normalisation, exact below 2^53.
-__host__ __device__ constexpr int norm_every(int S) { return 256 / S - 1; }
+// terms between carry normalisations.  Stored digits satisfy |d_0| <= R+1 and
+// |d_j| <= R/2 (j >= 1), so one term adds at most
+// 2 * [ (R+1) R/2 * 2 + (t-1) (R/2)^2 ] <= 2 R^2 (1.01 + (S-2)/4) to an
+// accumulator digit t <= S-1 (two real products per part); accumulators are
+// balanced to R/2 after a normalisation, and must stay below 2^53.
+__host__ __device__ constexpr int norm_every(int S) { return 102400 / ((S + 2) * 100 + 4) - 1; }
 
 // 2^(BETA*q) as a double: exact in the normal range, else formed by two
 // scalings (rounds into the subnormal range / saturates)
