@@ -30,7 +30,7 @@ constexpr int PADZ = 4;
 
 __host__ __device__ inline size_t conv_dig_smem(int S, int D, int P, int threads) {
     const size_t per_job = (size_t)2 * S * D + (size_t)2 * (PADZ + S) * D;  // doubles
-    return (size_t)P * per_job * sizeof(double) + (size_t)threads * S * sizeof(double) +
+    return (size_t)P * per_job * sizeof(double) + (size_t)threads * (S + 2) * sizeof(double) +
            (size_t)P * 4 * D * sizeof(int) + 16;  // + mbarrier
 }
 
@@ -116,15 +116,22 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
         if (__all_sync(__activemask(), fast)) {
             const double *W1 = sy + (PADZ - d1) * D2 + w1part * D + kk;
             const double *W2 = sy + (PADZ - d2) * D2 + w2part * D + kk;
+            // software pipelined: row l+1's two digits load while row l's FMAs run
+            double w1 = W1[0], w2 = W2[0];
 #pragma unroll
             for (int l = 0; l < S; l++) {
-                const double w1 = W1[l * D2];
-                const double w2 = W2[l * D2];
+                double w1n = 0.0, w2n = 0.0;
+                if (l + 1 < S) {
+                    w1n = W1[(l + 1) * D2];
+                    w2n = W2[(l + 1) * D2];
+                }
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
                     A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
+                w1 = w1n;
+                w2 = w2n;
             }
         } else {
             const double *W1 = sy + w1part * D + kk;
@@ -155,41 +162,37 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     }
 }
 
-// normalise, leading-zero shift, write digits and exponent of one (k, part)
+// normalise, leading-zero shift, write digits and exponent of one (k, part).
+// scratch: S+2 doubles of this thread's shared-memory slot (the shift by the
+// data-dependent z0 goes through a store/reload instead of a select network).
 template <int L>
 __device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int eacc, double *zd, int *ze, int D,
-                                              int k, int part) {
+                                              int k, int part, double *scratch) {
     constexpr int S = digits_for(L);
     carry_normalize(A);
     // Z = [c2, c1, c0, A_1 .. A_{S-1}], Z_u has weight R^(eacc - u)
-    double Z[S + 2];
-    {
-        double a0 = A[0];
-        const double c2 = rint_magic(__dmul_rn(a0, INV_RADIX * INV_RADIX));
-        a0 = __fma_rn(-c2, RADIX * RADIX, a0);
-        const double c1 = rint_magic(__dmul_rn(a0, INV_RADIX));
-        const double c0 = __fma_rn(-c1, RADIX, a0);
-        Z[0] = c2;
-        Z[1] = c1;
-        Z[2] = c0;
-#pragma unroll
-        for (int s = 1; s < S; s++) Z[s + 2] = A[s];
-    }
+    double a0 = A[0];
+    const double c2 = rint_magic(__dmul_rn(a0, INV_RADIX * INV_RADIX));
+    a0 = __fma_rn(-c2, RADIX * RADIX, a0);
+    const double c1 = rint_magic(__dmul_rn(a0, INV_RADIX));
+    const double c0 = __fma_rn(-c1, RADIX, a0);
+    scratch[0] = c2;
+    scratch[1] = c1;
+    scratch[2] = c0;
     int z0 = S + 2;
 #pragma unroll
-    for (int u = S + 1; u >= 0; u--)
-        if (Z[u] != 0.0) z0 = u;
-#pragma unroll
-    for (int b = 0; b < 6; b++) {  // shift left by z0 (< 64)
-        const int sh = 1 << b;
-        if (z0 & sh) {
-#pragma unroll
-            for (int u = 0; u < S + 2; u++) Z[u] = (u + sh < S + 2) ? Z[u + sh] : 0.0;
-        }
+    for (int s = S - 1; s >= 1; s--) {
+        scratch[s + 2] = A[s];
+        if (A[s] != 0.0) z0 = s + 2;
     }
+    if (c0 != 0.0) z0 = 2;
+    if (c1 != 0.0) z0 = 1;
+    if (c2 != 0.0) z0 = 0;
     const int e = (z0 >= S + 2 || eacc <= ZERO_E / 2) ? ZERO_E : eacc + 1 - z0;
+    const double *src = scratch + z0;
+    const int avail = S + 2 - z0;
 #pragma unroll
-    for (int s = 0; s < S; s++) zd[(part * S + s) * D + k] = (e == ZERO_E) ? 0.0 : Z[s];
+    for (int s = 0; s < S; s++) zd[(part * S + s) * D + k] = (s < avail && e != ZERO_E) ? src[s] : 0.0;
     ze[part * D + k] = e;
 }
 
@@ -204,7 +207,8 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
     extern __shared__ __align__(16) double sm[];
     double *sdig = sm;                                        // [P][SX + SY]
     double *spark = sm + (size_t)P * (SX + SY);               // [threads][S]
-    int *sexp = (int *)(spark + (size_t)blockDim.x * S);      // [P][2 series][2][D]
+    constexpr int PSTR = S + 2;                               // parking / emit scratch slot
+    int *sexp = (int *)(spark + (size_t)blockDim.x * PSTR);   // [P][2 series][2][D]
 
     const int job0 = blockIdx.x * P;
     // stage: x planes -> [s][part][D], y planes -> [PADZ + s][part][D], zero
@@ -300,7 +304,7 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
     ea2r = max(ea2r, ZERO_E);
     ea2i = max(ea2i, ZERO_E);
 
-    double *park = spark + (size_t)threadIdx.x * S;
+    double *park = spark + (size_t)threadIdx.x * PSTR;
     const int job = job0 + jl;
     const bool writer = jl < P && job < njobs;
     double *zd = dpool;
@@ -316,24 +320,30 @@ __global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpoo
         double A[S];
         const int e1 = part ? ea1i : ea1r, e2 = part ? ea2i : ea2r;
         conv_dig_pass<L, DT>(sx, sy, ex, ey, D, part, t, f, F, e1, e2, A, park);
-        // k2: sum the F lanes' partials (exact) with shuffles
+        // k2: sum the F lanes' partials (exact) with shuffles; every lane has it
         for (int off = F >> 1; off > 0; off >>= 1) {
 #pragma unroll
             for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
         }
-        __syncwarp();
-        if (writer) {
-            if (f == (F > 1 ? 1 : 0) && k2 != k1) conv_dig_emit<L>(A, e2, zd, ze, D, k2, part);
-            if (f == 0) {  // k1: the F parked partials of this pair
-                double B[S];
+        if (F == 1) {
+            double B[S];
 #pragma unroll
-                for (int s = 0; s < S; s++) B[s] = park[s];
+            for (int s = 0; s < S; s++) B[s] = park[s];
+            if (writer && k2 != k1) conv_dig_emit<L>(A, e2, zd, ze, D, k2, part, park);
+            if (writer) conv_dig_emit<L>(B, e1, zd, ze, D, k1, part, park);
+        } else {
+            if (f == 0) {  // k1: lane 0 sums the F parked partials of its pair
+#pragma unroll
+                for (int s = 0; s < S; s++) A[s] = park[s];
                 for (int g = 1; g < F; g++) {
 #pragma unroll
-                    for (int s = 0; s < S; s++) B[s] = __dadd_rn(B[s], park[g * S + s]);
+                    for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], park[g * PSTR + s]);
                 }
-                conv_dig_emit<L>(B, e1, zd, ze, D, k1, part);
             }
+            __syncwarp();  // parked partials consumed before the emit scratch reuses them
+            // lanes 0 and 1 emit k1 and k2 in one (lane-dependent) call
+            if (writer && f < 2 && (f == 0 || k2 != k1))
+                conv_dig_emit<L>(A, f == 0 ? e1 : e2, zd, ze, D, f == 0 ? k1 : k2, part, park);
         }
         __syncwarp();
     }
