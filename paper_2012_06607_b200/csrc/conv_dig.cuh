@@ -89,7 +89,7 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
         const bool first = j <= t;
         if (!first && !switched) {  // k1 partial complete: park it, start k2
             switched = true;
-            carry_normalize(A);
+            carry_pass(A);
 #pragma unroll
             for (int s = 0; s < S; s++) {
                 park[s] = A[s];
@@ -148,11 +148,11 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
             }
         }
         if (++cnt == NORM) {
-            carry_normalize(A);
+            carry_pass(A);
             cnt = 0;
         }
     }
-    carry_normalize(A);
+    carry_pass(A);
     if (!switched) {  // no k2 iterations on this lane: everything belongs to k1
 #pragma unroll
         for (int s = 0; s < S; s++) {
@@ -197,7 +197,7 @@ __device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int ea
 }
 
 template <int L, int DT>
-__global__ void __launch_bounds__(128) conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
+__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
                                                       const int *__restrict__ jobs, int njobs, int Drt, int T,
                                                       int F, int P) {
     constexpr int S = digits_for(L);

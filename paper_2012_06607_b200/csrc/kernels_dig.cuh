@@ -71,15 +71,28 @@ __device__ __forceinline__ double radix_pow(int q) {
 
 __device__ __forceinline__ double rint_magic(double x) { return __dsub_rn(__dadd_rn(x, MAGIC), MAGIC); }
 
-// balance digits 1..N-1 into [-R/2, R/2], carrying into digit 0 (exact)
+// One parallel carry pass (exact): every digit t >= 1 hands rint(A_t / R) to
+// digit t-1 at once — S independent 5-instruction chains instead of one
+// serial chain.  From |A_t| < 2^53 one pass leaves |A_t| <= R/2 + 2^31, a
+// second <= R/2 + 2^9, a third <= R/2 + 1.
 template <int N>
-__device__ __forceinline__ void carry_normalize(double (&A)[N]) {
+__device__ __forceinline__ void carry_pass(double (&A)[N]) {
+    double q[N];
+#pragma unroll
+    for (int t = N - 1; t >= 1; t--) q[t] = rint_magic(__dmul_rn(A[t], INV_RADIX));
 #pragma unroll
     for (int t = N - 1; t >= 1; t--) {
-        const double q = rint_magic(__dmul_rn(A[t], INV_RADIX));
-        A[t] = __fma_rn(-q, RADIX, A[t]);
-        A[t - 1] = __dadd_rn(A[t - 1], q);
+        A[t] = __fma_rn(-q[t], RADIX, A[t]);
+        A[t - 1] = __dadd_rn(A[t - 1], q[t]);
     }
+}
+
+// balance digits 1..N-1 into [-R/2 - 1, R/2 + 1], carrying into digit 0 (exact)
+template <int N>
+__device__ __forceinline__ void carry_normalize(double (&A)[N]) {
+    carry_pass(A);
+    carry_pass(A);
+    carry_pass(A);
 }
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); }

@@ -70,22 +70,45 @@ struct DigGeom {
     int T, F, P, threads;
     size_t smem;
 };
-static DigGeom dig_geom(int L, int D) {
+// Launch geometry of the product kernel: F lanes per output pair and P jobs
+// per block, chosen by modelled throughput — resident warps per SM (limited
+// by registers, shared memory and 64 warps), lane balance of the folded
+// triangle ((D+1) terms over F lanes) and the per-lane term count that
+// amortises the per-output epilogue.  MDPS_CONV_F / MDPS_CONV_P override.
+static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads) {
     const int S = digits_for(L);
-    DigGeom g;
-    g.T = (D + 1) / 2;
-    int F = 1;
-    while (g.T * F * 2 <= 128 && (D + 1) / (F * 2) >= 8) F *= 2;
-    g.F = F;
-    g.P = std::max(1, 128 / (g.T * g.F));
-    for (;;) {
-        // whole warps: the kernel's shuffles and votes use full-warp masks
-        g.threads = (g.P * g.T * g.F + 31) / 32 * 32;
-        g.smem = conv_dig_smem(S, D, g.P, g.threads);
-        if (g.smem <= 110 * 1024 || g.P == 1) break;
-        g.P /= 2;
+    const int T = (D + 1) / 2;
+    DigGeom best{T, 1, 1, 32, 0};
+    double best_score = -1.0;
+    const char *ef = getenv("MDPS_CONV_F"), *ep = getenv("MDPS_CONV_P");
+    for (int F = 1; F <= 8; F *= 2) {
+        if (ef && atoi(ef) != F) continue;
+        for (int P = 1; P <= 32; P *= 2) {
+            if (ep && atoi(ep) != P) continue;
+            DigGeom g;
+            g.T = T;
+            g.F = F;
+            g.P = P;
+            g.threads = (P * T * F + 31) / 32 * 32;  // whole warps (full-mask shuffles)
+            if (g.threads > max_threads) continue;
+            g.smem = conv_dig_smem(S, D, P, g.threads);
+            if (g.smem > 227 * 1024) continue;
+            const int blocks_smem = (int)(228 * 1024 / (g.smem + 1024));
+            const int blocks_regs = 65536 / (std::max(regs_per_thread, 32) * g.threads);
+            const int blocks = std::min(std::min(blocks_smem, blocks_regs), 32);
+            if (blocks < 1) continue;
+            const int warps = std::min(blocks * g.threads / 32, 64);
+            const int iters = (D + 1 + F - 1) / F;
+            const double balance = (double)(D + 1) / (F * iters) * (double)(P * T * F) / g.threads;
+            const double amort = (double)iters / (iters + 3.0);
+            const double score = std::min(warps, 16) * balance * amort;
+            if (score > best_score) {
+                best_score = score;
+                best = g;
+            }
+        }
     }
-    return g;
+    return best;
 }
 
 // ---------------------------------------------------------------------------
@@ -107,11 +130,24 @@ template <int L>
 struct ConvDig {
     static int run(double *dpool, int *epool, const int *jobs, int njobs, int D, cudaStream_t st) {
         if (njobs <= 0) return MDPS_OK;
-        DigGeom g = dig_geom(L, D);
         // compile-time D for the configs' degrees: shared-memory offsets become immediates
         void (*kern)(double *, int *, const int *, int, int, int, int, int) =
             D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> :
             D == 64 ? conv_dig_kernel<L, 64> : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
+        // geometry per D, computed once (benign race: every writer stores the same value)
+        static DigGeom cache[257];
+        static bool cached[257];
+        if (!cached[D]) {
+            cudaFuncAttributes fa;
+            int regs = 255, maxt = 128;
+            if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
+                regs = fa.numRegs;
+                maxt = std::min(fa.maxThreadsPerBlock, 256);
+            }
+            cache[D] = dig_geom(L, D, regs, maxt);
+            cached[D] = true;
+        }
+        const DigGeom g = cache[D];
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
         kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, jobs, njobs, D, g.T, g.F, g.P);
