@@ -162,14 +162,33 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     }
 }
 
-// normalise, leading-zero shift, write digits and exponent of one (k, part).
-// scratch: S+2 doubles of this thread's shared-memory slot (the shift by the
-// data-dependent z0 goes through a store/reload instead of a select network).
 template <int L>
-__device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int eacc, double *zd, int *ze, int D,
-                                              int k, int part, double *scratch) {
+__device__ __forceinline__ void conv_dig_emit_digits(const double (&A)[digits_for(L)], int eacc, double *zd, int *ze,
+                                                     int D, int k, int part, double *scratch);
+
+// normalise and write one output (k, part): limbs (zl != null) for the
+// addition jobs and/or digits with their exponent (zd != null) for later
+// products.  scratch: S+2 doubles of this thread's shared-memory slot (the
+// leading-zero shift by the data-dependent z0 goes through a store/reload).
+template <int L>
+__device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int eacc, double *zd, int *ze, double *zl,
+                                              int D, int k, int part, double *scratch) {
     constexpr int S = digits_for(L);
     carry_normalize(A);
+    if (zd) conv_dig_emit_digits<L>(A, eacc, zd, ze, D, k, part, scratch);
+    if (zl) {  // limbs for the addition jobs: the exact accumulator rounded to L limbs
+        double out[L];
+        digits_to_limbs<L, S>(A, eacc - 1, out);  // A_t has weight R^(eacc-2-t); consumes A
+#pragma unroll
+        for (int p = 0; p < L; p++) zl[(part * L + p) * D + k] = out[p];
+    }
+}
+
+// digits of a normalised accumulator with the leading-zero shift
+template <int L>
+__device__ __forceinline__ void conv_dig_emit_digits(const double (&A)[digits_for(L)], int eacc, double *zd, int *ze,
+                                                     int D, int k, int part, double *scratch) {
+    constexpr int S = digits_for(L);
     // Z = [c2, c1, c0, A_1 .. A_{S-1}], Z_u has weight R^(eacc - u)
     double a0 = A[0];
     const double c2 = rint_magic(__dmul_rn(a0, INV_RADIX * INV_RADIX));
@@ -197,8 +216,13 @@ __device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int ea
 }
 
 template <int L, int DT>
-__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
-                                                      const int *__restrict__ jobs, int njobs, int Drt, int T,
+// register budget per SM: 4 blocks of 128 up to L = 4 (<= 128 registers),
+// 3 up to L = 8 (<= 170), 2 above; 256-thread blocks for D = 128 and the
+// generic-D build
+__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
+                                  DT == 128 || DT == 0 ? 1 : (L <= 4 ? 4 : (L <= 8 ? 3 : 2)))
+    conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
+                                                      double *__restrict__ lpool, const int *__restrict__ jobs, int njobs, int Drt, int T,
                                                       int F, int P) {
     constexpr int S = digits_for(L);
     const int D = DT > 0 ? DT : Drt;
@@ -230,7 +254,7 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_ker
                 const int which = rem / (2 * S), ps = rem - which * 2 * S;
                 const int part = ps / S, s = ps - part * S;
                 const int job = min(job0 + jl, njobs - 1);
-                const double *g = dpool + (size_t)jobs[3 * job + which] * 2 * S * D + (size_t)ps * D;
+                const double *g = dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D) + (size_t)ps * D;
                 double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
                                                                        : (s * 2 + part) * D);
                 bulk_g2s(dst, g, (unsigned)(D * 8), bar);
@@ -245,7 +269,7 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_ker
             const int which = rem / (2 * S), ps = rem - which * 2 * S;
             const int part = ps / S, s = ps - part * S;
             const int job = min(job0 + jl, njobs - 1);
-            const double *g = dpool + (size_t)jobs[3 * job + which] * 2 * S * D + (size_t)ps * D;
+            const double *g = dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D) + (size_t)ps * D;
             double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
                                                                    : (s * 2 + part) * D);
             if ((D & 1) == 0) {
@@ -264,7 +288,7 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_ker
         const int jl = idx / (4 * D), r = idx - jl * 4 * D;
         const int which = r / (2 * D), r2 = r - which * 2 * D;
         const int job = min(job0 + jl, njobs - 1);
-        sexp[idx] = epool[(size_t)jobs[3 * job + which] * 2 * D + r2];
+        sexp[idx] = epool[(size_t)jobs[4 * job + which] * 2 * D + r2];
     }
     if (use_tma) mbar_wait(bar, 0);
     __syncthreads();
@@ -309,10 +333,15 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_ker
     const bool writer = jl < P && job < njobs;
     double *zd = dpool;
     int *ze = epool;
+    double *zl = nullptr;  // limb output (the series is summed by the addition jobs)
+    int wdig = 0;          // digit output (the series is a product input)
     if (writer) {
-        const int out = jobs[3 * job + 2];
-        zd = dpool + (size_t)out * 2 * S * D;
+        const int out = jobs[4 * job + 2];
+        const int code = jobs[4 * job + 3];
+        zd = dpool + (size_t)out * dig_slot_stride(S, D);
         ze = epool + (size_t)out * 2 * D;
+        wdig = code & 1;
+        if (code & 2) zl = lpool + (size_t)(code >> 2) * 2 * L * D;
     }
     const int k1 = t, k2 = D - 1 - t;
 #pragma unroll 1
@@ -329,8 +358,8 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_ker
             double B[S];
 #pragma unroll
             for (int s = 0; s < S; s++) B[s] = park[s];
-            if (writer && k2 != k1) conv_dig_emit<L>(A, e2, zd, ze, D, k2, part, park);
-            if (writer) conv_dig_emit<L>(B, e1, zd, ze, D, k1, part, park);
+            if (writer && k2 != k1) conv_dig_emit<L>(A, e2, wdig ? zd : nullptr, ze, zl, D, k2, part, park);
+            if (writer) conv_dig_emit<L>(B, e1, wdig ? zd : nullptr, ze, zl, D, k1, part, park);
         } else {
             if (f == 0) {  // k1: lane 0 sums the F parked partials of its pair
 #pragma unroll
@@ -343,7 +372,7 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128) conv_dig_ker
             __syncwarp();  // parked partials consumed before the emit scratch reuses them
             // lanes 0 and 1 emit k1 and k2 in one (lane-dependent) call
             if (writer && f < 2 && (f == 0 || k2 != k1))
-                conv_dig_emit<L>(A, f == 0 ? e1 : e2, zd, ze, D, f == 0 ? k1 : k2, part, park);
+                conv_dig_emit<L>(A, f == 0 ? e1 : e2, wdig ? zd : nullptr, ze, zl, D, f == 0 ? k1 : k2, part, park);
         }
         __syncwarp();
     }

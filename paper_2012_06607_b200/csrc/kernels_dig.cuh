@@ -58,6 +58,9 @@ __host__ __device__ constexpr int digits_for(int L) {
 // balanced to R/2 after a normalisation, and must stay below 2^53.
 __host__ __device__ constexpr int norm_every(int S) { return 102400 / ((S + 2) * 100 + 4) - 1; }
 
+// doubles per digit-pool slot (one series: [2][S][D])
+__host__ __device__ constexpr size_t dig_slot_stride(int S, int D) { return (size_t)2 * S * D; }
+
 // 2^(BETA*q) as a double: exact in the normal range, else formed by two
 // scalings (rounds into the subnormal range / saturates)
 __device__ __forceinline__ double radix_pow(int q) {
@@ -166,7 +169,7 @@ __global__ void __launch_bounds__(128) to_digits_kernel(const double *__restrict
     if (g >= (long long)count * D) return;
     const int s = (int)(g / D), k = (int)(g - (long long)s * D);
     const double *x = src + (size_t)s * 2 * L * D;
-    double *dd = dpool + (size_t)(slot0 + s) * 2 * S * D;
+    double *dd = dpool + (size_t)(slot0 + s) * dig_slot_stride(S, D);
     int *ee = epool + (size_t)(slot0 + s) * 2 * D;
 #pragma unroll
     for (int part = 0; part < 2; part++) {
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(128) accum_dig_kernel(const double *__restrict
             const int slot = ent_slot[e];
             const double w = (double)ent_w[e];
             const int delta = eacc - epool[(size_t)slot * 2 * D + part * D + k] + 1;
-            const double *d = dpool + (size_t)slot * 2 * S * D + (size_t)part * S * D + k;
+            const double *d = dpool + (size_t)slot * dig_slot_stride(S, D) + (size_t)part * S * D + k;
 #pragma unroll
             for (int s = 0; s <= S; s++) {
                 const int src = s - delta;

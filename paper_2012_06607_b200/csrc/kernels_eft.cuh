@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(128) conv_eft_kernel(double *__restrict__ pool
         const int job = job0 + j2;
         if (job < njobs) {
             const int which = r >= LD2, off = r - which * LD2;
-            const int src = jobs[3 * job + which];
+            const int src = jobs[4 * job + which];
             sm[j2 * JS + r] = pool[(size_t)src * LD2 + off];
         }
     }
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(128) conv_eft_kernel(double *__restrict__ pool
             }
         }
     }
-    double *z = pool + (size_t)jobs[3 * job + 2] * LD2;
+    double *z = pool + (size_t)jobs[4 * job + 2] * LD2;
     double zr[L], zi[L], Fr[L + 1], Fi[L + 1];
 #pragma unroll
     for (int p = 0; p <= L; p++) {

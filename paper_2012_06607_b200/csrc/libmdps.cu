@@ -128,10 +128,10 @@ struct ConvEft {
 
 template <int L>
 struct ConvDig {
-    static int run(double *dpool, int *epool, const int *jobs, int njobs, int D, cudaStream_t st) {
+    static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, cudaStream_t st) {
         if (njobs <= 0) return MDPS_OK;
         // compile-time D for the configs' degrees: shared-memory offsets become immediates
-        void (*kern)(double *, int *, const int *, int, int, int, int, int) =
+        void (*kern)(double *, int *, double *, const int *, int, int, int, int, int) =
             D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> :
             D == 64 ? conv_dig_kernel<L, 64> : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
         // geometry per D, computed once (benign race: every writer stores the same value)
@@ -150,7 +150,7 @@ struct ConvDig {
         const DigGeom g = cache[D];
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
-        kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, jobs, njobs, D, g.T, g.F, g.P);
+        kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, lpool, jobs, njobs, D, g.T, g.F, g.P);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -163,18 +163,6 @@ struct AccumEft {
         const long long total = (long long)ntasks * D;
         const int blocks = (int)((total + 127) / 128);
         accum_eft_kernel<L><<<blocks, 128, 0, st>>>(pool, tp, es, ew, ntasks, n, D, values, jac);
-        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
-        return MDPS_OK;
-    }
-};
-
-template <int L>
-struct AccumDig {
-    static int run(const double *dpool, const int *epool, const int *tp, const int *es, const int *ew, int ntasks,
-                   int n, int D, double *values, double *jac, cudaStream_t st) {
-        const long long total = (long long)ntasks * D;
-        const int blocks = (int)((total + 127) / 128);
-        accum_dig_kernel<L><<<blocks, 128, 0, st>>>(dpool, epool, tp, es, ew, ntasks, n, D, values, jac);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -204,6 +192,9 @@ struct mdps_system {
     int *epool = nullptr;    // DIGITS: exponents [slot][2][D]
     int *jobs = nullptr;     // all levels, (in1, in2, out) triples
     int *task_ptr = nullptr, *ent_slot = nullptr, *ent_w = nullptr;
+    double *lpool = nullptr;  // DIGITS: limb planes of the series the addition jobs sum [lslot][2][L][D]
+    int *ent_lslot = nullptr; // DIGITS: addition terms indexed into lpool
+    std::vector<std::pair<int32_t, int32_t>> x_lslots;  // (x index, lslot) of inputs summed directly
     double *host_in = nullptr;  // staging for the _host variant (device buffers)
     double *dev_in = nullptr, *dev_vals = nullptr, *dev_jac = nullptr;
     size_t device_bytes = 0;
@@ -256,6 +247,8 @@ static void free_system(mdps_system *s) {
     cudaFree(s->task_ptr);
     cudaFree(s->ent_slot);
     cudaFree(s->ent_w);
+    cudaFree(s->lpool);
+    cudaFree(s->ent_lslot);
     cudaFree(s->dev_in);
     cudaFree(s->dev_vals);
     cudaFree(s->dev_jac);
@@ -312,17 +305,19 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->add_terms = (int64_t)S.ent_slot.size();
     s->ntasks = n + n * n;
 
-    std::vector<int32_t> alljobs;
-    for (auto &lv : S.levels) {
-        s->level_off.push_back((int64_t)alljobs.size() / 3);
-        s->level_cnt.push_back((int64_t)lv.size() / 3);
+    std::vector<int32_t> alljobs;  // (in1, in2, out, code) per job, level by level
+    for (auto &lv : S.levels4) {
+        s->level_off.push_back((int64_t)alljobs.size() / 4);
+        s->level_cnt.push_back((int64_t)lv.size() / 4);
         alljobs.insert(alljobs.end(), lv.begin(), lv.end());
     }
-    const size_t ser = (size_t)2 * (algo == MDPS_ALGO_DIGITS ? s->S : limbs) * D;  // doubles per slot
+    const size_t ser = algo == MDPS_ALGO_DIGITS ? dig_slot_stride(s->S, D) : (size_t)2 * limbs * D;  // doubles per slot
     if (!dalloc(s, &s->pool, ser * (size_t)s->nslots) ||
         (algo == MDPS_ALGO_DIGITS && !dalloc(s, &s->epool, (size_t)2 * D * s->nslots)) ||
         !dalloc(s, &s->jobs, alljobs.size()) || !dalloc(s, &s->task_ptr, S.task_ptr.size()) ||
-        !dalloc(s, &s->ent_slot, S.ent_slot.size()) || !dalloc(s, &s->ent_w, S.ent_w.size())) {
+        !dalloc(s, &s->ent_slot, S.ent_slot.size()) || !dalloc(s, &s->ent_w, S.ent_w.size()) ||
+        (algo == MDPS_ALGO_DIGITS && (!dalloc(s, &s->lpool, (size_t)2 * limbs * D * S.nlimb) ||
+                                      !dalloc(s, &s->ent_lslot, S.ent_lslot.size())))) {
         free_system(s);
         return nullptr;
     }
@@ -334,6 +329,20 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
               up(s->task_ptr, S.task_ptr.data(), S.task_ptr.size() * 4) &&
               up(s->ent_slot, S.ent_slot.data(), S.ent_slot.size() * 4) &&
               up(s->ent_w, S.ent_w.data(), S.ent_w.size() * 4);
+    if (ok && algo == MDPS_ALGO_DIGITS) {
+        ok = up(s->ent_lslot, S.ent_lslot.data(), S.ent_lslot.size() * 4);
+        // summed coefficient series (constant terms, m = 1 without common
+        // factor) are copied once into the limb pool; summed inputs x_j (none
+        // with the current DAG) are copied at every eval
+        for (int64_t slot = 0; ok && slot < (int64_t)n + S.M; slot++) {
+            const int32_t ls = S.limb_slot[(size_t)slot];
+            if (ls < 0) continue;
+            if (slot < n)
+                s->x_lslots.emplace_back((int32_t)slot, ls);
+            else
+                ok = up(s->lpool + (size_t)ls * limb_ser, coefficients + (size_t)(slot - n) * limb_ser, limb_ser * 8);
+        }
+    }
     if (ok && S.M > 0) {
         if (algo == MDPS_ALGO_EFT) {
             ok = up(s->pool + (size_t)n * ser, coefficients, (size_t)S.M * limb_ser * 8);
@@ -383,7 +392,7 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
         }
         for (size_t lv = 0; lv < s->level_cnt.size(); lv++) {
             TimedGroup tg(s, st, 0);
-            rc = dispatch_L<ConvEft>(L, s->pool, (const int *)(s->jobs + 3 * s->level_off[lv]),
+            rc = dispatch_L<ConvEft>(L, s->pool, (const int *)(s->jobs + 4 * s->level_off[lv]),
                                      (int)s->level_cnt[lv], D, st);
             if (rc) return rc;
         }
@@ -395,16 +404,22 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
         TimedGroup tg(s, st, 2);
         rc = dispatch_L<ToDigits>(L, in, n, D, s->pool, s->epool, 0, st);
         if (rc) return rc;
+        for (auto &xl : s->x_lslots)
+            CUDA_TRY(cudaMemcpyAsync(s->lpool + (size_t)xl.second * 2 * L * D, in + (size_t)xl.first * 2 * L * D,
+                                     (size_t)2 * L * D * 8, cudaMemcpyDeviceToDevice, st),
+                     MDPS_ECUDA);
     }
     for (size_t lv = 0; lv < s->level_cnt.size(); lv++) {
         TimedGroup tg(s, st, 0);
-        rc = dispatch_L<ConvDig>(L, s->pool, s->epool, (const int *)(s->jobs + 3 * s->level_off[lv]),
+        rc = dispatch_L<ConvDig>(L, s->pool, s->epool, s->lpool, (const int *)(s->jobs + 4 * s->level_off[lv]),
                                  (int)s->level_cnt[lv], D, st);
         if (rc) return rc;
     }
+    // the addition jobs read the limb pool (the product jobs wrote limbs for
+    // exactly the series they sum)
     TimedGroup tg(s, st, 1);
-    return dispatch_L<AccumDig>(L, (const double *)s->pool, (const int *)s->epool, (const int *)s->task_ptr,
-                                (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, n, D, vals, jac, st);
+    return dispatch_L<AccumEft>(L, (const double *)s->lpool, (const int *)s->task_ptr, (const int *)s->ent_lslot,
+                                (const int *)s->ent_w, s->ntasks, n, D, vals, jac, st);
 }
 
 extern "C" int mdps_system_set_timing(mdps_system *s, int32_t enable) {
@@ -629,45 +644,33 @@ struct Roundtrip {
 
 template <int L>
 struct SeriesMulDig {
-    // stage x and y into a scratch digit pool, run the product kernel, convert back
+    // stage x and y into a scratch digit pool; the product kernel writes the
+    // limbs of each product straight into z (job code: limb slot c, no digits)
     static int run(const double *x, const double *y, double *z, int count, int D, cudaStream_t st) {
         constexpr int S = digits_for(L);
         double *dp = nullptr;
         int *ep = nullptr, *jobs = nullptr;
-        double *vals_dummy = nullptr;
-        int *tp = nullptr, *es = nullptr, *ew = nullptr;
         const size_t slots = (size_t)3 * count;
         int rc = MDPS_OK;
-        std::vector<int> hj(3 * (size_t)count), htp((size_t)count + 1), hes(count), hew(count, 1);
+        std::vector<int> hj(4 * (size_t)count);
         for (int c = 0; c < count; c++) {
-            hj[3 * c] = c;
-            hj[3 * c + 1] = count + c;
-            hj[3 * c + 2] = 2 * count + c;
-            htp[c] = c;
-            hes[c] = 2 * count + c;
+            hj[4 * c] = c;
+            hj[4 * c + 1] = count + c;
+            hj[4 * c + 2] = 2 * count + c;
+            hj[4 * c + 3] = (c << 2) | 2;
         }
-        htp[count] = count;
-        if (cudaMalloc((void **)&dp, slots * 2 * S * D * 8) != cudaSuccess ||
+        if (cudaMalloc((void **)&dp, slots * dig_slot_stride(S, D) * 8) != cudaSuccess ||
             cudaMalloc((void **)&ep, slots * 2 * D * 4) != cudaSuccess ||
-            cudaMalloc((void **)&jobs, hj.size() * 4) != cudaSuccess ||
-            cudaMalloc((void **)&tp, htp.size() * 4) != cudaSuccess ||
-            cudaMalloc((void **)&es, hes.size() * 4) != cudaSuccess ||
-            cudaMalloc((void **)&ew, hew.size() * 4) != cudaSuccess) {
+            cudaMalloc((void **)&jobs, hj.size() * 4) != cudaSuccess) {
             cudaGetLastError();
             set_err("cudaMalloc failed");
             rc = MDPS_ENOMEM;
         }
         if (!rc) {
             cudaMemcpyAsync(jobs, hj.data(), hj.size() * 4, cudaMemcpyHostToDevice, st);
-            cudaMemcpyAsync(tp, htp.data(), htp.size() * 4, cudaMemcpyHostToDevice, st);
-            cudaMemcpyAsync(es, hes.data(), hes.size() * 4, cudaMemcpyHostToDevice, st);
-            cudaMemcpyAsync(ew, hew.data(), hew.size() * 4, cudaMemcpyHostToDevice, st);
             rc = ToDigits<L>::run(x, count, D, dp, ep, 0, st);
             if (!rc) rc = ToDigits<L>::run(y, count, D, dp, ep, count, st);
-            if (!rc) rc = ConvDig<L>::run(dp, ep, jobs, count, D, st);
-            // the n = count "values" tasks of a count x count system would
-            // need n*n Jacobian outputs: use ntasks = count with n = count
-            if (!rc) rc = AccumDig<L>::run(dp, ep, tp, es, ew, count, count, D, z, vals_dummy, st);
+            if (!rc) rc = ConvDig<L>::run(dp, ep, z, jobs, count, D, st);
             if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
                 set_err("series_mul kernel failed");
                 rc = MDPS_ECUDA;
@@ -676,9 +679,6 @@ struct SeriesMulDig {
         cudaFree(dp);
         cudaFree(ep);
         cudaFree(jobs);
-        cudaFree(tp);
-        cudaFree(es);
-        cudaFree(ew);
         return rc;
     }
 };
@@ -689,11 +689,12 @@ struct SeriesMulEft {
         const size_t ser = (size_t)2 * L * D;
         double *pool = nullptr;
         int *jobs = nullptr;
-        std::vector<int> hj(3 * (size_t)count);
+        std::vector<int> hj(4 * (size_t)count);
         for (int c = 0; c < count; c++) {
-            hj[3 * c] = c;
-            hj[3 * c + 1] = count + c;
-            hj[3 * c + 2] = 2 * count + c;
+            hj[4 * c] = c;
+            hj[4 * c + 1] = count + c;
+            hj[4 * c + 2] = 2 * count + c;
+            hj[4 * c + 3] = 0;
         }
         if (cudaMalloc((void **)&pool, 3 * ser * count * 8) != cudaSuccess ||
             cudaMalloc((void **)&jobs, hj.size() * 4) != cudaSuccess) {

@@ -108,7 +108,7 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
         }
     }
     S.nslots = (int64_t)B.level.size();
-    if (S.nslots > INT32_MAX) { err = "too many series (slots overflow int32)"; return false; }
+    if (S.nslots > INT32_MAX / 4) { err = "too many series (slots overflow int32)"; return false; }
     S.task_ptr.assign((size_t)ntasks + 1, 0);
     S.ent_slot.clear();
     S.ent_w.clear();
@@ -119,6 +119,35 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
         }
         if (S.ent_slot.size() > (size_t)INT32_MAX) { err = "too many addition terms"; return false; }
         S.task_ptr[(size_t)t + 1] = (int32_t)S.ent_slot.size();
+    }
+    // which series are product inputs (digit form) and which are summed by the
+    // addition jobs (limb form); the limb pool holds only the latter
+    std::vector<uint8_t> as_input((size_t)S.nslots, 0);
+    for (auto &lv : S.levels)
+        for (size_t q = 0; q < lv.size(); q += 3) {
+            as_input[(size_t)lv[q]] = 1;
+            as_input[(size_t)lv[q + 1]] = 1;
+        }
+    S.limb_slot.assign((size_t)S.nslots, -1);
+    S.nlimb = 0;
+    for (int32_t s : S.ent_slot)
+        if (S.limb_slot[(size_t)s] < 0) S.limb_slot[(size_t)s] = (int32_t)S.nlimb++;
+    S.ent_lslot.resize(S.ent_slot.size());
+    for (size_t e = 0; e < S.ent_slot.size(); e++) S.ent_lslot[e] = S.limb_slot[(size_t)S.ent_slot[e]];
+    S.levels4.clear();
+    for (auto &lv : S.levels) {
+        std::vector<int32_t> v;
+        v.reserve(lv.size() / 3 * 4);
+        for (size_t q = 0; q < lv.size(); q += 3) {
+            const int32_t out = lv[q + 2];
+            const int32_t ls = S.limb_slot[(size_t)out];
+            const int32_t code = (ls >= 0 ? ((ls << 2) | 2) : 0) | (as_input[(size_t)out] ? 1 : 0);
+            v.push_back(lv[q]);
+            v.push_back(lv[q + 1]);
+            v.push_back(out);
+            v.push_back(code);
+        }
+        S.levels4.push_back(std::move(v));
     }
     return true;
 }

@@ -28,6 +28,13 @@ struct Schedule {
     std::vector<int32_t> ent_slot, ent_w;       // addition terms
     int64_t products = 0;
     int32_t max_weight = 1;
+    // form of each series: product inputs are read as digit planes, summed
+    // series as limbs.  limb_slot[slot] = index in the limb pool or -1.
+    std::vector<int32_t> limb_slot, ent_lslot;  // ent_lslot: ent_slot remapped to the limb pool
+    int64_t nlimb = 0;
+    // per level: (in1, in2, out, code) with code = lslot << 2 | 2 (write limbs)
+    // | 1 (write digits: the output is a product input)
+    std::vector<std::vector<int32_t>> levels4;
 };
 
 // Validates the inputs (libmdps.h) and builds the schedule.  Pool slots:

@@ -14,7 +14,8 @@ ap.add_argument("--config", default="od")
 ap.add_argument("--algo", type=int, default=0)
 ap.add_argument("--evals", type=int, default=2)
 a = ap.parse_args()
-si = mdinputs.sweep_cell(*map(int, a.config.split("_")[1:])) if a.config.startswith("sweep") else mdinputs.make_config(a.config)
+si = (mdinputs.sweep_cell(int(a.config.split("_")[1][1:]), int(a.config.split("_")[2][1:]))
+      if a.config.startswith("sweep") else mdinputs.make_config(a.config))
 s = mdps.System.from_inputs(si, algo=a.algo)
 print("levels:", s.level_jobs(), "stats:", s.stats(), flush=True)
 x = torch.from_numpy(si.x).cuda()
