@@ -5,10 +5,10 @@
 // its FP64 instruction count.  The paper's md arithmetic (PAPER.md:76-80,
 // Table 1) spends most of it on TwoSum cascades that keep every rounding
 // error.  Here each real md coefficient is split ONCE into S signed digits of
-// BETA = 22 bits on a radix-2^22 grid anchored at the coefficient's own
+// BETA = 23 bits on a radix-2^23 grid anchored at the coefficient's own
 // exponent (an error-free split in the sense of Dekker/Veltkamp: every digit
 // is an exact double).  A digit product is then exact (<= 44 bits), and the
-// sum of up to ~2^8 of them is exact too, so one DFMA per digit pair does
+// sum of a few hundred of them is exact too, so one DFMA per digit pair does
 // the work of a TwoProd plus its TwoSum cascade.  The truncated convolution
 // z_k = sum_{i<=k} x_i y_{k-i} is accumulated EXACTLY
 // into S integer-valued digit accumulators per output coefficient; the only
@@ -17,9 +17,9 @@
 //
 // Representation (pool slot s): digits [2][S][D] doubles (part, digit,
 // coefficient) and radix exponents [2][D] int32.  Part value
-//     v = sum_j  digit_j * R^(e - 1 - j),   R = 2^BETA,  |v| < R^e,
-// digits balanced (|digit_j| <= R/2 for j >= 1, |digit_0| <= R); a zero part
-// has e = ZERO_E.  Limb planes (the ABI layout) are converted to digits on
+//     v = sum_j  digit_j * R^(e - 1 - j),   R = 2^BETA,  |v| < R^e / 2,
+// every digit balanced (|digit_j| <= R/2 + 1, the top one included); a zero
+// part has e = ZERO_E.  Limb planes (the ABI layout) are converted to digits on
 // entry (x every call, coefficients at create) and back to limbs only for
 // values and Jacobian entries (the addition jobs), so the whole DAG runs on
 // digits.
@@ -38,9 +38,9 @@
 
 namespace mdps {
 
-constexpr int BETA = 22;
-constexpr double RADIX = 4194304.0;          // 2^22
-constexpr double INV_RADIX = 1.0 / 4194304.0;
+constexpr int BETA = 23;
+constexpr double RADIX = 8388608.0;          // 2^23
+constexpr double INV_RADIX = 1.0 / 8388608.0;
 constexpr double MAGIC = 6755399441055744.0;  // 1.5 * 2^52: rounds |x| < 2^51 to an integer
 constexpr int ZERO_E = -(1 << 24);
 
@@ -51,12 +51,13 @@ __host__ __device__ constexpr int digits_for(int L) {
     while ((S - 2) * BETA < 53 * L + 8) S++;
     return S;
 }
-// terms between carry normalisations.  Stored digits satisfy |d_0| <= R+1 and
-// |d_j| <= R/2 (j >= 1), so one term adds at most
-// 2 * [ (R+1) R/2 * 2 + (t-1) (R/2)^2 ] <= 2 R^2 (1.01 + (S-2)/4) to an
-// accumulator digit t <= S-1 (two real products per part); accumulators are
-// balanced to R/2 after a normalisation, and must stay below 2^53.
-__host__ __device__ constexpr int norm_every(int S) { return 102400 / ((S + 2) * 100 + 4) - 1; }
+// terms between carry normalisations.  Stored digits satisfy |d_j| <= R/2 + 1,
+// so one term adds at most 2 (t+1) (R/2+1)^2 <= 1.01 S R^2 / 2 to an
+// accumulator digit t <= S-1 (two real products per part); a carry pass
+// leaves |A_t| <= R/2 + 2^31, and accumulators must stay below 2^53:
+// NORM * 1.01 S 2^45 < 2^53 - 2^32.  The top accumulator digit is never
+// carried out of: it collects at most 2 D (R/2+1)^2 < 2^53 for D <= 128.
+__host__ __device__ constexpr int norm_every(int S) { return 25600 / (S * 101) - 1; }
 
 // doubles per digit-pool slot (one series: [2][S][D])
 __host__ __device__ constexpr size_t dig_slot_stride(int S, int D) { return (size_t)2 * S * D; }
@@ -115,8 +116,8 @@ __device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d
         for (int j = 0; j < S; j++) d[j] = (m == 0.0) ? 0.0 : m;
         return m == 0.0 ? ZERO_E : 0;
     }
-    const int emin = ilogb(m) + 1;  // |v| <= m < 2^emin
-    const int e = ceil_div(emin, BETA);
+    const int emin = ilogb(m) + 1;          // |v| <= m < 2^emin
+    const int e = ceil_div(emin + 1, BETA);  // |v| < R^e / 2: a balanced top digit
 #pragma unroll
     for (int j = 0; j < S; j++) {
         const double G = radix_pow(e - 1 - j);
