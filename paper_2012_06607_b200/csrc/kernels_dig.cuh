@@ -136,12 +136,13 @@ __device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d
 }
 
 // S digits (exponent e, digit j weight R^(e-1-j), any balance with
-// |digit| < 2^52 / R) -> L limbs, rounded (md_renorm of exact pairs)
-template <int L, int S>
+// |digit| < 2^52 / R; NORMALIZED = the caller already balanced digits 1..S-1)
+// -> L limbs, rounded (md_renorm of exact pairs)
+template <int L, int S, bool NORMALIZED = false>
 __device__ __forceinline__ void digits_to_limbs(double (&A)[S], int e, double (&out)[L]) {
     constexpr int NV = 1 + S / 2;
     double vals[NV];
-    carry_normalize(A);
+    if (!NORMALIZED) carry_normalize(A);
     if (e <= ZERO_E / 2) {
 #pragma unroll
         for (int p = 0; p < L; p++) out[p] = 0.0;
