@@ -204,25 +204,16 @@ __device__ __noinline__ void conv_g_output(const double *acc, const double *park
     if (emit) emit_z<L>(Z, eacc, zd, ze, zl, D, k, pass == 1 ? 1 : 0, scratch);
 }
 
-template <int L, int DT>
-__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
-                                  DT == 128 || DT == 0 ? 1 : (L <= 8 ? 3 : 2))
-    conv_g_kernel(double *__restrict__ dpool, int *__restrict__ epool, double *__restrict__ lpool,
-                  const int *__restrict__ jobs, int njobs, int Drt, int T, int F, int P) {
+// Stage the digit planes of both inputs of every job of the block (TMA bulk
+// copies for even D, plain loads otherwise), the PADZ zero planes and the
+// part exponents, then align each coefficient's two parts to the larger part
+// exponent (shx: aligned exponents [P][2 series][D]).  Ends with a block sync.
+template <int L>
+__device__ __forceinline__ void stage_aligned(const double *__restrict__ dpool, const int *__restrict__ epool,
+                                              const int *__restrict__ jobs, int njobs, int D, int P, int job0,
+                                              double *sdig, int *sexp, int *shx, uint64_t *bar) {
     constexpr int S = digits_for(L);
-    constexpr int ZS = S + 2;
-    const int D = DT > 0 ? DT : Drt;
     const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
-    const int threads_per_job = T * F;
-    extern __shared__ __align__(16) double sm[];
-    double *sdig = sm;                                   // [P][SX + SY]
-    double *sgrp = sm + (size_t)P * (SX + SY);           // [P*T][4][ZS]
-    int *sexp = (int *)(sgrp + ((size_t)P * T + 1) * 4 * ZS);  // [P][2 series][2 parts][D]
-    int *shx = sexp + (size_t)P * 4 * D;                 // [P][2 series][D] aligned exponents
-    uint64_t *bar = reinterpret_cast<uint64_t *>(shx + (size_t)P * 2 * D);
-    const int job0 = blockIdx.x * P;
-
-    // ---- stage (TMA bulk copies for even D), zero planes, part exponents
     const bool use_tma = (D & 1) == 0;
     if (use_tma) {
         if (threadIdx.x == 0) mbar_init(bar, 1);
@@ -284,6 +275,28 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
         }
     }
     __syncthreads();
+
+}
+
+template <int L, int DT>
+__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
+                                  DT == 128 || DT == 0 ? 1 : (L <= 8 ? 3 : 2))
+    conv_g_kernel(double *__restrict__ dpool, int *__restrict__ epool, double *__restrict__ lpool,
+                  const int *__restrict__ jobs, int njobs, int Drt, int T, int F, int P) {
+    constexpr int S = digits_for(L);
+    constexpr int ZS = S + 2;
+    const int D = DT > 0 ? DT : Drt;
+    const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
+    const int threads_per_job = T * F;
+    extern __shared__ __align__(16) double sm[];
+    double *sdig = sm;                                   // [P][SX + SY]
+    double *sgrp = sm + (size_t)P * (SX + SY);           // [P*T][4][ZS]
+    int *sexp = (int *)(sgrp + ((size_t)P * T + 1) * 4 * ZS);  // [P][2 series][2 parts][D]
+    int *shx = sexp + (size_t)P * 4 * D;                 // [P][2 series][D] aligned exponents
+    uint64_t *bar = reinterpret_cast<uint64_t *>(shx + (size_t)P * 2 * D);
+    const int job0 = blockIdx.x * P;
+
+    stage_aligned<L>(dpool, epool, jobs, njobs, D, P, job0, sdig, sexp, shx, bar);
 
     const int jl0 = threadIdx.x / threads_per_job;
     const int jl = min(jl0, P - 1);  // padding lanes shadow the last job

@@ -13,6 +13,7 @@
 #include "../../include/mdps_test.h"
 #include "conv_dig.cuh"
 #include "conv_gauss.cuh"
+#include "conv_single.cuh"
 #include "kernels_dig.cuh"
 #include "kernels_eft.cuh"
 #include "schedule.hpp"
@@ -76,7 +77,7 @@ struct DigGeom {
 // by registers, shared memory and 64 warps), lane balance of the folded
 // triangle ((D+1) terms over F lanes) and the per-lane term count that
 // amortises the per-output epilogue.  MDPS_CONV_F / MDPS_CONV_P override.
-static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool gauss) {
+static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int kind) {
     const int S = digits_for(L);
     const int T = (D + 1) / 2;
     DigGeom best{T, 1, 1, 32, 0};
@@ -92,7 +93,8 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool
             g.P = P;
             g.threads = (P * T * F + 31) / 32 * 32;  // whole warps (full-mask shuffles)
             if (g.threads > max_threads) continue;
-            g.smem = gauss ? conv_g_smem(S, D, P, T) : conv_dig_smem(S, D, P, g.threads);
+            g.smem = kind == 1 ? conv_g_smem(S, D, P, T)
+                               : kind == 2 ? conv_s_smem(S, D, P, T) : conv_dig_smem(S, D, P, g.threads);
             if (g.smem > 227 * 1024) continue;
             const int blocks_smem = (int)(228 * 1024 / (g.smem + 1024));
             const int blocks_regs = 65536 / (std::max(regs_per_thread, 32) * g.threads);
@@ -131,16 +133,22 @@ template <int L>
 struct ConvDig {
     static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, cudaStream_t st) {
         if (njobs <= 0) return MDPS_OK;
-        // four real products per complex term (conv_dig.cuh); MDPS_CONV_GAUSS=1
-        // selects the three-product kernel (conv_gauss.cuh: 16% fewer FP64
-        // instructions but shared-memory bound, measured 1.5x slower on od)
-        static const bool gauss = getenv("MDPS_CONV_GAUSS") && atoi(getenv("MDPS_CONV_GAUSS")) == 1;
-        // compile-time D for the configs' degrees: shared-memory offsets become immediates
-        void (*kern)(double *, int *, double *, const int *, int, int, int, int, int) =
-            gauss ? (D == 16 ? conv_g_kernel<L, 16> : D == 32 ? conv_g_kernel<L, 32> :
-                     D == 64 ? conv_g_kernel<L, 64> : D == 128 ? conv_g_kernel<L, 128> : conv_g_kernel<L, 0>)
-                  : (D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> :
-                     D == 64 ? conv_dig_kernel<L, 64> : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>);
+        // product kernel: 0 = two passes, one per part (conv_dig.cuh, default);
+        // opt-in variants via MDPS_CONV_KERNEL: 1 = three products per term
+        // (conv_gauss.cuh; shared-memory bound, od 72 ms vs 47 ms), 2 = one pass
+        // for both parts (conv_single.cuh; two blocks/SM, od 56 ms vs 47 ms)
+        static const int kind = getenv("MDPS_CONV_KERNEL") ? atoi(getenv("MDPS_CONV_KERNEL")) : 0;
+        using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
+        KernT kern;
+        if (kind == 1)
+            kern = D == 16 ? conv_g_kernel<L, 16> : D == 32 ? conv_g_kernel<L, 32> : D == 64 ? conv_g_kernel<L, 64>
+                 : D == 128 ? conv_g_kernel<L, 128> : conv_g_kernel<L, 0>;
+        else if (kind == 2)
+            kern = D == 16 ? conv_s_kernel<L, 16> : D == 32 ? conv_s_kernel<L, 32> : D == 64 ? conv_s_kernel<L, 64>
+                 : D == 128 ? conv_s_kernel<L, 128> : conv_s_kernel<L, 0>;
+        else
+            kern = D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> : D == 64 ? conv_dig_kernel<L, 64>
+                 : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
         // geometry per D, computed once (benign race: every writer stores the same value)
         static DigGeom cache[257];
         static bool cached[257];
@@ -151,7 +159,7 @@ struct ConvDig {
                 regs = fa.numRegs;
                 maxt = std::min(fa.maxThreadsPerBlock, 256);
             }
-            cache[D] = dig_geom(L, D, regs, maxt, gauss);
+            cache[D] = dig_geom(L, D, regs, maxt, kind);
             cached[D] = true;
         }
         const DigGeom g = cache[D];

@@ -1,5 +1,6 @@
 #!/bin/bash
-# full round check: all GPU tests, smoke, default bench (with cpu_baseline and e2e), launch list + ncu of the top kernel
+# full round check: smoke, all GPU tests, default bench (cpu_baseline, e2e), reference arm,
+# launch list of the bench command, ncu --set full of the product kernel (od)
 cd $GRAFT_REPO_ROOT
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 1800 python -m pytest tests -m gpu -q --durations=10 > gpurun_out/pytest_gpu_all.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_all.log
@@ -7,4 +8,6 @@ timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_reference.log
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_short.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launch.log 2>&1
+python scripts/prof_one.py --config od --evals 2 > gpurun_out/prof_plain_od.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:conv_ -s 24 -c 1 -o gpurun_out/prof_conv_od python scripts/prof_one.py --config od --evals 2 > gpurun_out/ncu_full_od.log 2>&1
 echo done
