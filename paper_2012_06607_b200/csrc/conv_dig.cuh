@@ -174,11 +174,14 @@ template <int L>
 __device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int eacc, double *zd, int *ze, double *zl,
                                               int D, int k, int part, double *scratch) {
     constexpr int S = digits_for(L);
-    carry_normalize(A);
+    // inputs: carry-passed partials (|A_t| <= R/2 + 2^31) summed over <= 8
+    // lanes, so two parallel carry passes balance every digit to R/2 + 1
+    carry_pass(A);
+    carry_pass(A);
     if (zd) conv_dig_emit_digits<L>(A, eacc, zd, ze, D, k, part, scratch);
     if (zl) {  // limbs for the addition jobs: the exact accumulator rounded to L limbs
         double out[L];
-        digits_to_limbs<L, S>(A, eacc - 1, out);  // A_t has weight R^(eacc-2-t); consumes A
+        digits_to_limbs<L, S, true>(A, eacc - 1, out);  // A_t has weight R^(eacc-2-t); consumes A
 #pragma unroll
         for (int p = 0; p < L; p++) zl[(part * L + p) * D + k] = out[p];
     }
