@@ -41,7 +41,7 @@ __all__ = [
 
 _MASK = (1 << 64) - 1
 _GAMMA = 0x9E3779B97F4A7C15
-_PURPOSE = {"structure": 1, "x": 2, "c": 3, "extra": 4}
+_PURPOSE = {"structure": 1, "x": 2, "c": 3, "extra": 4, "jac": 5, "rhs": 6}
 
 
 def _mix64(z: int) -> int:
@@ -291,3 +291,47 @@ def first_entries(si: SystemInputs, count: int):
                 return out
             out.append((i, j))
     return out[:count]
+
+
+# ---------------------------------------------------------------------------
+# Block lower-triangular Toeplitz systems (the linear solve of a Newton step,
+# PAPER.md:266-333).  Recipe: a dense n-by-n matrix
+# of series J and a right-hand side b(t), every coefficient of every series
+# cos(theta) + i sin(theta) with the lower-limb rule of the config — the
+# distribution of the configs' own data, at the configs' n, degree and limbs.
+@dataclasses.dataclass
+class ToeplitzInputs:
+    name: str
+    n: int
+    degree: int
+    limbs: int
+    jac: np.ndarray   # float64 [n][n][2][L][D]
+    rhs: np.ndarray   # float64 [n][2][L][D]
+
+    @property
+    def D(self) -> int:
+        return self.degree + 1
+
+    def truncate(self, degree: int) -> "ToeplitzInputs":
+        D = degree + 1
+        return ToeplitzInputs(f"{self.name}_d{degree}", self.n, degree, self.limbs,
+                              np.ascontiguousarray(self.jac[..., :D]), np.ascontiguousarray(self.rhs[..., :D]))
+
+
+def random_toeplitz(seed: int, n: int, degree: int, limbs: int, lower: str = "random",
+                    name: Optional[str] = None) -> ToeplitzInputs:
+    D = degree + 1
+    jac = unit_circle_series(SplitMix64(seed, "jac"), n * n, D, limbs, lower).reshape(n, n, 2, limbs, D)
+    rhs = unit_circle_series(SplitMix64(seed, "rhs"), n, D, limbs, lower)
+    return ToeplitzInputs(name or f"toeplitz{seed}_n{n}_d{degree}_L{limbs}", n, degree, limbs,
+                          np.ascontiguousarray(jac), rhs)
+
+
+def toeplitz_config(name: str) -> ToeplitzInputs:
+    """The solve that follows config `name`'s eval/diff: its n, degree, limbs,
+    lower-limb rule and seed (sweep: its largest cell)."""
+    key = ("toeplitz", name)
+    if key not in _CACHE:
+        cfg = CONFIGS[name]
+        _CACHE[key] = random_toeplitz(cfg.seed, cfg.n, cfg.degree, cfg.limbs, cfg.lower, f"toeplitz_{name}")
+    return _CACHE[key]

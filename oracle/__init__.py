@@ -53,6 +53,7 @@ def lib() -> ctypes.CDLL:
         L.mdo_eval_entries.argtypes = [i32, i32, P(i32), P(i32), P(i32), P(i32), P(d), P(d), i32, i32,
                                        i32, P(i32), P(i32), P(d), i32, P(ll)]
         L.mdo_series_err.argtypes = [P(d), P(d), i32, i32, i32, P(d)]
+        L.mdo_toeplitz_solve.argtypes = [i32, i32, i32, P(d), P(d), P(d), P(i32), i32]
         _lib = L
     return _lib
 
@@ -210,3 +211,31 @@ def series_err(a, b) -> np.ndarray:
     err = np.zeros(count)
     _check(lib().mdo_series_err(_dp(a), _dp(b), count, D, L, _dp(err)), "series_err")
     return err.reshape(lead)
+
+
+# ---- block lower-triangular Toeplitz forward substitution ------------------------
+class SingularError(ArithmeticError):
+    pass
+
+
+def toeplitz_solve(jac, rhs, nthreads: Optional[int] = None, limbs: Optional[int] = None):
+    """dx(t) with (A_0 + A_1 t + ...)(dx_0 + dx_1 t + ...) = b(t) mod t^D
+    (PAPER.md:266-333): jac [n][n][2][L][D] (A_k = coefficient k), rhs
+    [n][2][L][D].  Returns (dx [n][2][L][D], pivots [n]).  `limbs` > L solves
+    the same inputs (zero-padded limbs) at a higher precision."""
+    jac, rhs = _f64(jac), _f64(rhs)
+    n, n2, two, L0, D = jac.shape
+    assert n == n2 and two == 2 and rhs.shape == (n, 2, L0, D)
+    L = limbs or L0
+    if L != L0:
+        assert L > L0
+        jac = _f64(np.pad(jac, [(0, 0)] * 3 + [(0, L - L0), (0, 0)]))
+        rhs = _f64(np.pad(rhs, [(0, 0)] * 2 + [(0, L - L0), (0, 0)]))
+    dx = np.zeros((n, 2, L, D))
+    piv = np.zeros(n, dtype=np.int32)
+    nt = nthreads or os.cpu_count() or 1
+    rc = lib().mdo_toeplitz_solve(n, D, L, _dp(jac), _dp(rhs), _dp(dx), _ip(piv), nt)
+    if rc == -4:
+        raise SingularError("A_0 is singular (zero pivot column)")
+    _check(rc, "toeplitz_solve")
+    return dx, piv

@@ -674,3 +674,212 @@ int mdo_series_err(const double *a, const double *b, int count, int D, int L, do
     }
     return g_err ? -1 : 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Block lower-triangular Toeplitz forward substitution (§4):
+ *   (A_0 + A_1 t + ... + A_d t^d)(dx_0 + dx_1 t + ... + dx_d t^d) = b(t),
+ * A_k = the coefficient-k matrix of the series matrix J (J[p][q] a series).
+ * As the paper states it: factor A_0 once (LU with partial
+ * pivoting for N = n), then for j = 0..d
+ *     A_0 dx_j = b_j - sum_{i=1..j} A_i dx_{j-i}.
+ * Readings (R9-R12):
+ *   - pivot k = the row i >= k maximising |re_0(a_ik)| + |im_0(a_ik)| (leading
+ *     limbs, one double rounding), lowest index on ties; rows swapped whole;
+ *     a zero pivot column is "singular" (return -4);
+ *   - multipliers l_ik = a_ik / a_kk correctly rounded (cdiv); every Schur
+ *     update a_ij - l_ik u_kj formed exactly and rounded once;
+ *   - r_j = b_j - sum_{i,q} A_i[p][q] dx_{j-i}[q]: every entry formed exactly,
+ *     rounded once; forward substitution y_i = RN(r_i - sum_{q<i} l_iq y_q);
+ *     back substitution dx_i = RN_{L+3}(y_i - sum_{q>i} u_iq dx_q) / u_ii.
+ * J: [n][n][2][L][D] (row p, column q), b and dx: [n][2][L][D], piv: [n].
+ * The right-hand sides of one j are independent jobs over p (PAPER.md:410-413:
+ * "one job is the update of one right hand side vector"), run by nthreads
+ * workers claiming rows from a counter guarded by a binary semaphore.
+ * ------------------------------------------------------------------------- */
+#define EIDX(p, q, part, limb, k, n, L, D) (((((size_t)(p) * (n) + (q)) * 2 + (part)) * (L) + (limb)) * (D) + (k))
+
+typedef struct {
+    int n, D, L, j;
+    const double *J, *b;
+    double *dx, *r; /* r: [n][2][L] right-hand side of step j */
+    pthread_mutex_t lock;
+    int next, err;
+} ts_job_t;
+
+static void *ts_rhs_worker(void *arg) {
+    ts_job_t *T = (ts_job_t *)arg;
+    int n = T->n, D = T->D, L = T->L, j = T->j;
+    sa_t *s = (sa_t *)malloc(2 * sizeof(sa_t));
+    sa_init(&s[0]);
+    sa_init(&s[1]);
+    g_err = 0;
+    for (;;) {
+        pthread_mutex_lock(&T->lock);
+        int p = T->next++;
+        pthread_mutex_unlock(&T->lock);
+        if (p >= n) break;
+        for (int part = 0; part < 2; part++)
+            for (int l = 0; l < L; l++) sa_add_double(&s[part], T->b[SIDX(part, l, j, L, D) + (size_t)p * 2 * L * D]);
+        for (int i = 1; i <= j; i++)
+            for (int q = 0; q < n; q++)
+                for (int u = 0; u < L; u++)
+                    for (int v = 0; v < L; v++) {
+                        double ar = T->J[EIDX(p, q, 0, u, i, n, L, D)], ai = T->J[EIDX(p, q, 1, u, i, n, L, D)];
+                        const double *x = T->dx + (size_t)q * 2 * L * D;
+                        double xr = x[SIDX(0, v, j - i, L, D)], xi = x[SIDX(1, v, j - i, L, D)];
+                        sa_add_prod(&s[0], ar, xr, -1); /* re -= ar xr - ai xi */
+                        sa_add_prod(&s[0], ai, xi, 1);
+                        sa_add_prod(&s[1], ar, xi, -1); /* im -= ar xi + ai xr */
+                        sa_add_prod(&s[1], ai, xr, -1);
+                    }
+        for (int part = 0; part < 2; part++) sa_round_limbs(&s[part], L, T->r + ((size_t)p * 2 + part) * L, 1);
+    }
+    if (g_err) {
+        pthread_mutex_lock(&T->lock);
+        T->err = 1;
+        pthread_mutex_unlock(&T->lock);
+    }
+    free(s);
+    return NULL;
+}
+
+/* pivot magnitude: |re_0| + |im_0| rounded once (the same double on every
+ * implementation that adds the two absolute leading limbs) */
+static double piv_mag(const double *re, const double *im) { return fabs(re[0]) + fabs(im[0]); }
+
+int mdo_toeplitz_solve(int n, int D, int L, const double *J, const double *b, double *dx, int *piv,
+                       int nthreads) {
+    if (n < 1 || D < 1 || L < 1 || L > MDO_MAXL) return -3;
+    g_err = 0;
+    const size_t E = (size_t)2 * L; /* doubles per complex md element */
+    double *lu = (double *)malloc(sizeof(double) * (size_t)n * n * E);
+    double *r = (double *)malloc(sizeof(double) * (size_t)n * E);
+    double *y = (double *)malloc(sizeof(double) * (size_t)n * E);
+    sa_t *s = (sa_t *)malloc(2 * sizeof(sa_t));
+    if (!lu || !r || !y || !s) return -5;
+    sa_init(&s[0]);
+    sa_init(&s[1]);
+#define LU(i, q, part) (lu + (((size_t)(i) * n + (q)) * 2 + (part)) * L)
+    for (int p = 0; p < n; p++)
+        for (int q = 0; q < n; q++)
+            for (int part = 0; part < 2; part++)
+                for (int l = 0; l < L; l++) LU(p, q, part)[l] = J[EIDX(p, q, part, l, 0, n, L, D)];
+    int rc = 0;
+    /* LU with partial pivoting of A_0 (right-looking Gaussian elimination) */
+    for (int k = 0; k < n && !rc; k++) {
+        int best = k;
+        double bm = piv_mag(LU(k, k, 0), LU(k, k, 1));
+        for (int i = k + 1; i < n; i++) {
+            double m = piv_mag(LU(i, k, 0), LU(i, k, 1));
+            if (m > bm) { bm = m; best = i; }
+        }
+        piv[k] = best;
+        if (bm == 0.0) { rc = -4; break; }
+        if (best != k)
+            for (int q = 0; q < n; q++)
+                for (size_t t = 0; t < E; t++) {
+                    double tmp = LU(k, q, 0)[t];
+                    LU(k, q, 0)[t] = LU(best, q, 0)[t];
+                    LU(best, q, 0)[t] = tmp;
+                }
+        for (int i = k + 1; i < n; i++) {
+            double lr[BUF], li[BUF];
+            rc = cdiv(LU(i, k, 0), LU(i, k, 1), L, LU(k, k, 0), LU(k, k, 1), L, L, lr, li);
+            if (rc) break;
+            memcpy(LU(i, k, 0), lr, sizeof(double) * L);
+            memcpy(LU(i, k, 1), li, sizeof(double) * L);
+            for (int q = k + 1; q < n; q++) {
+                const double *ur = LU(k, q, 0), *ui = LU(k, q, 1);
+                for (int l = 0; l < L; l++) {
+                    sa_add_double(&s[0], LU(i, q, 0)[l]);
+                    sa_add_double(&s[1], LU(i, q, 1)[l]);
+                }
+                for (int u = 0; u < L; u++)
+                    for (int v = 0; v < L; v++) {
+                        sa_add_prod(&s[0], lr[u], ur[v], -1);
+                        sa_add_prod(&s[0], li[u], ui[v], 1);
+                        sa_add_prod(&s[1], lr[u], ui[v], -1);
+                        sa_add_prod(&s[1], li[u], ur[v], -1);
+                    }
+                sa_round_limbs(&s[0], L, LU(i, q, 0), 1);
+                sa_round_limbs(&s[1], L, LU(i, q, 1), 1);
+            }
+        }
+    }
+    /* forward substitution over the coefficients j = 0..d */
+    ts_job_t T;
+    memset(&T, 0, sizeof T);
+    T.n = n; T.D = D; T.L = L; T.J = J; T.b = b; T.dx = dx; T.r = r;
+    pthread_mutex_init(&T.lock, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > n) nthreads = n;
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int j = 0; j < D && !rc; j++) {
+        T.j = j;
+        T.next = 0;
+        if (nthreads == 1) ts_rhs_worker(&T);
+        else {
+            for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, ts_rhs_worker, &T);
+            for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+        }
+        if (T.err) { rc = -1; break; }
+#define RV(v, i, part) ((v) + ((size_t)(i) * 2 + (part)) * L)
+        for (int k = 0; k < n; k++)
+            if (piv[k] != k)
+                for (size_t t = 0; t < E; t++) {
+                    double tmp = RV(r, k, 0)[t];
+                    RV(r, k, 0)[t] = RV(r, piv[k], 0)[t];
+                    RV(r, piv[k], 0)[t] = tmp;
+                }
+        for (int i = 0; i < n; i++) { /* L y = P r, unit lower triangular */
+            for (int l = 0; l < L; l++) {
+                sa_add_double(&s[0], RV(r, i, 0)[l]);
+                sa_add_double(&s[1], RV(r, i, 1)[l]);
+            }
+            for (int q = 0; q < i; q++) {
+                const double *lr = LU(i, q, 0), *li = LU(i, q, 1), *yr = RV(y, q, 0), *yi = RV(y, q, 1);
+                for (int u = 0; u < L; u++)
+                    for (int v = 0; v < L; v++) {
+                        sa_add_prod(&s[0], lr[u], yr[v], -1);
+                        sa_add_prod(&s[0], li[u], yi[v], 1);
+                        sa_add_prod(&s[1], lr[u], yi[v], -1);
+                        sa_add_prod(&s[1], li[u], yr[v], -1);
+                    }
+            }
+            sa_round_limbs(&s[0], L, RV(y, i, 0), 1);
+            sa_round_limbs(&s[1], L, RV(y, i, 1), 1);
+        }
+        for (int i = n - 1; i >= 0; i--) { /* U dx_j = y */
+            for (int l = 0; l < L; l++) {
+                sa_add_double(&s[0], RV(y, i, 0)[l]);
+                sa_add_double(&s[1], RV(y, i, 1)[l]);
+            }
+            for (int q = i + 1; q < n; q++) {
+                const double *ur = LU(i, q, 0), *ui = LU(i, q, 1);
+                const double *x = dx + (size_t)q * 2 * L * D;
+                for (int u = 0; u < L; u++)
+                    for (int v = 0; v < L; v++) {
+                        double xr = x[SIDX(0, v, j, L, D)], xi = x[SIDX(1, v, j, L, D)];
+                        sa_add_prod(&s[0], ur[u], xr, -1);
+                        sa_add_prod(&s[0], ui[u], xi, 1);
+                        sa_add_prod(&s[1], ur[u], xi, -1);
+                        sa_add_prod(&s[1], ui[u], xr, -1);
+                    }
+            }
+            double nr[BUF], ni[BUF], qr[BUF], qi[BUF];
+            sa_round_limbs(&s[0], L + 3, nr, 1);
+            sa_round_limbs(&s[1], L + 3, ni, 1);
+            rc = cdiv(nr, ni, L + 3, LU(i, i, 0), LU(i, i, 1), L, L, qr, qi);
+            if (rc) break;
+            double *x = dx + (size_t)i * 2 * L * D;
+            for (int l = 0; l < L; l++) { x[SIDX(0, l, j, L, D)] = qr[l]; x[SIDX(1, l, j, L, D)] = qi[l]; }
+        }
+    }
+#undef RV
+#undef LU
+    pthread_mutex_destroy(&T.lock);
+    free(th);
+    free(lu); free(r); free(y); free(s);
+    if (rc) return rc;
+    return g_err ? -1 : 0;
+}

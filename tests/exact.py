@@ -75,3 +75,44 @@ def series_err_exact(approx: np.ndarray, exact) -> float:
         maxd = max(maxd, math.hypot(float(dr), float(di)))
         maxe = max(maxe, math.hypot(float(exact[k][0]), float(exact[k][1])))
     return maxd / max(maxe, 1.0)
+
+
+def csub(a, b):
+    return (a[0] - b[0], a[1] - b[1])
+
+
+def cdiv(a, b):
+    den = b[0] * b[0] + b[1] * b[1]
+    return ((a[0] * b[0] + a[1] * b[1]) / den, (a[1] * b[0] - a[0] * b[1]) / den)
+
+
+def solve_exact(A, b):
+    """x with A x = b over complex Fractions (Gauss-Jordan, any nonzero pivot)."""
+    n = len(A)
+    M = [list(A[i]) + [b[i]] for i in range(n)]
+    for k in range(n):
+        p = next(i for i in range(k, n) if M[i][k] != (0, 0))
+        M[k], M[p] = M[p], M[k]
+        for i in range(n):
+            if i != k and M[i][k] != (0, 0):
+                f = cdiv(M[i][k], M[k][k])
+                M[i] = [csub(M[i][c], cmul(f, M[k][c])) for c in range(n + 1)]
+    return [cdiv(M[i][n], M[i][i]) for i in range(n)]
+
+
+def toeplitz_exact(jac: np.ndarray, rhs: np.ndarray):
+    """Exact forward substitution on float inputs:
+    returns dx[q] = list of D complex Fractions."""
+    n, _, _, L, D = jac.shape
+    A = [[[(value(jac[p, q, 0, :, k]), value(jac[p, q, 1, :, k])) for q in range(n)] for p in range(n)]
+         for k in range(D)]
+    b = [[(value(rhs[p, 0, :, k]), value(rhs[p, 1, :, k])) for p in range(n)] for k in range(D)]
+    dx = []
+    for j in range(D):
+        r = list(b[j])
+        for i in range(1, j + 1):
+            for p in range(n):
+                for q in range(n):
+                    r[p] = csub(r[p], cmul(A[i][p][q], dx[j - i][q]))
+        dx.append(solve_exact(A[0], r))
+    return [[dx[j][q] for j in range(D)] for q in range(n)]
