@@ -132,6 +132,56 @@ int mdps_system_stats(const mdps_system *sys, mdps_stats *out);
 /* Per-level job counts (levels entries) for diagnostics; returns levels or <0. */
 int mdps_system_level_jobs(const mdps_system *sys, int64_t *jobs_per_level, int32_t max_levels);
 
+
+/* ---------------------------------------------------------------------------
+ * Block lower-triangular Toeplitz solver — the linear solve of one Newton step
+ * on power series (§4).
+ *
+ * With linearisation A(t) = A_0 + A_1 t + ... + A_d t^d, A_k the n-by-n
+ * matrix of coefficient k of the Jacobian series, solves
+ *     A(t) dx(t) = b(t)   mod t^(d+1)
+ * by forward substitution: A_0 dx_0 = b_0 and
+ *     A_0 dx_j = b_j - sum_{i=1..j} A_i dx_{j-i},   j = 1..d,
+ * factoring A_0 once (LU with partial pivoting, N = n: PAPER.md:260-262).
+ * The GPU applies the factorisation as the explicit inverse A_0^-1 (formed
+ * from the LU factors once), so that each of the d+1 solves is one parallel
+ * matrix-vector product.
+ *
+ * Layouts are those of mdps_eval_diff: jacobian [n][n][2][limbs][D] (row p,
+ * column q, series), rhs and dx [n][2][limbs][D]; D = degree + 1.
+ * ------------------------------------------------------------------------- */
+typedef struct mdps_solver mdps_solver; /* opaque; owns its device workspace */
+
+/* n in [1, 512], degree in [0, 255], limbs in {2,3,4,5,8,10}.  Allocates the
+ * workspace (about 2x the Jacobian) on the current device.  NULL on error. */
+mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t limbs);
+
+/* dx(t) with A(t) dx(t) = rhs(t) mod t^D.  DEVICE pointers: jacobian and rhs
+ * read only, dx_out fully overwritten; dx_out must not alias the inputs.
+ * Asynchronous on `stream`; one solve may be in flight per solver.  Returns
+ * MDPS_OK, MDPS_EINVAL or MDPS_ECUDA.  A singular A_0 (a zero pivot column)
+ * does not fail the call: it is reported by mdps_solver_status and dx_out is
+ * then unspecified. */
+int mdps_solve(mdps_solver *solver, const double *jacobian, const double *rhs, double *dx_out,
+               mdps_stream_t stream);
+
+/* After synchronising the last solve's stream: the pivot rows of the LU of
+ * A_0 (HOST [n], row k swapped with pivots[k] at step k; NULL to skip) and
+ * singular = 1 if some pivot column of A_0 was zero. */
+int mdps_solver_status(mdps_solver *solver, int32_t *pivots, int32_t *singular);
+
+typedef struct {
+    int64_t complex_fma;       /* complex md multiply-adds per solve (LU, inverse, substitution) */
+    int64_t fp64_ops;          /* algorithmic FP64 instructions per solve */
+    int32_t launches;          /* kernel launches per solve */
+    int32_t grid_blocks;       /* co-resident blocks of the persistent kernels */
+    size_t workspace_bytes;
+} mdps_solver_info;
+
+int mdps_solver_stats(const mdps_solver *solver, mdps_solver_info *out);
+
+void mdps_solver_destroy(mdps_solver *solver);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,7 @@ __all__ = [
     "MDPS_OK", "MDPS_EINVAL", "MDPS_ENOMEM", "MDPS_ECUDA", "MDPS_ALGO_AUTO", "MDPS_ALGO_EFT",
     "MDPS_ALGO_DIGITS", "MdpsError", "lib", "library_path", "System",
     "mdps_system_create", "mdps_eval_diff", "mdps_eval_diff_host", "mdps_system_destroy",
-    "mdps_last_error", "mdps_system_stats", "EXPORTED_SYMBOLS",
+    "mdps_last_error", "mdps_system_stats", "EXPORTED_SYMBOLS", "Solver",
 ]
 
 MDPS_OK, MDPS_EINVAL, MDPS_ENOMEM, MDPS_ECUDA = 0, -1, -2, -3
@@ -34,6 +34,7 @@ EXPORTED_SYMBOLS = (
     "mdps_system_destroy", "mdps_last_error", "mdps_system_stats", "mdps_system_level_jobs",
     "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
     "mdps_fp64_peak", "mdps_system_set_timing", "mdps_system_timing",
+    "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
 )
 
 
@@ -65,6 +66,14 @@ class Timing(ctypes.Structure):
     _fields_ = [("conv_ms", ctypes.c_double), ("accum_ms", ctypes.c_double), ("convert_ms", ctypes.c_double),
                 ("conv_launches", ctypes.c_int64), ("accum_launches", ctypes.c_int64),
                 ("convert_launches", ctypes.c_int64), ("evals", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class SolverInfo(ctypes.Structure):
+    _fields_ = [("complex_fma", ctypes.c_int64), ("fp64_ops", ctypes.c_int64), ("launches", ctypes.c_int32),
+                ("grid_blocks", ctypes.c_int32), ("workspace_bytes", ctypes.c_size_t)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -102,6 +111,13 @@ def lib() -> ctypes.CDLL:
     L.mdps_fp64_peak.argtypes = [i64, P(ctypes.c_double), vp]
     L.mdps_system_set_timing.argtypes = [vp, i32]
     L.mdps_system_timing.argtypes = [vp, P(Timing), i32]
+    L.mdps_solver_create.restype = vp
+    L.mdps_solver_create.argtypes = [i32, i32, i32]
+    L.mdps_solve.argtypes = [vp, vp, vp, vp, vp]
+    L.mdps_solver_status.argtypes = [vp, P(i32), P(i32)]
+    L.mdps_solver_stats.argtypes = [vp, P(SolverInfo)]
+    L.mdps_solver_destroy.argtypes = [vp]
+    L.mdps_solver_destroy.restype = None
     _lib = L
     return L
 
@@ -238,6 +254,55 @@ class System:
     def close(self):
         if getattr(self, "handle", None):
             mdps_system_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class Solver:
+    """RAII wrapper of the block lower-triangular Toeplitz solver (libmdps.h):
+    dx(t) with A(t) dx(t) = b(t) mod t^D, A(t) the n-by-n Jacobian series."""
+
+    def __init__(self, n: int, degree: int, limbs: int):
+        self.n, self.degree, self.limbs = int(n), int(degree), int(limbs)
+        self.handle = lib().mdps_solver_create(self.n, self.degree, self.limbs)
+        if not self.handle:
+            raise MdpsError(f"mdps_solver_create failed: {mdps_last_error()}")
+
+    def solve(self, jacobian, rhs, dx_out=None, stream=None):
+        import torch
+        if dx_out is None:
+            dx_out = torch.empty((self.n, 2, self.limbs, self.degree + 1), dtype=torch.float64,
+                                 device=rhs.device)
+        _check(lib().mdps_solve(self.handle, _dptr(jacobian), _dptr(rhs), _dptr(dx_out), _stream_handle(stream)),
+               "mdps_solve")
+        return dx_out
+
+    def status(self):
+        """(pivots [n] int32, singular bool) of the last solve (synchronises)."""
+        piv = np.zeros(self.n, dtype=np.int32)
+        sing = ctypes.c_int32(0)
+        _check(lib().mdps_solver_status(self.handle, _ptr_i32(piv), ctypes.byref(sing)), "mdps_solver_status")
+        return piv, bool(sing.value)
+
+    def stats(self) -> dict:
+        st = SolverInfo()
+        _check(lib().mdps_solver_stats(self.handle, ctypes.byref(st)), "mdps_solver_stats")
+        return st.as_dict()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().mdps_solver_destroy(self.handle)
             self.handle = None
 
     def __del__(self):

@@ -31,13 +31,43 @@ def deps():
         glob.glob(os.path.join(ROOT, "include", "*.h")) + [__file__]
 
 
+OBJDIR = os.path.join(HERE, "build_obj")
+
+
+def _headers():
+    return [p for p in deps() if p not in sources()]
+
+
 def build(force: bool = False, verbose: bool = False, extra=()) -> str:
+    """Compile every translation unit to an object in parallel (a unit is
+    recompiled when it or any header is newer than its object), then link."""
     if not force and os.path.exists(LIB):
         mt = os.path.getmtime(LIB)
         if all(os.path.getmtime(p) <= mt for p in deps()):
             return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJDIR, exist_ok=True)
+    hdr_mt = max(os.path.getmtime(p) for p in _headers())
+    flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+
+    def compile_one(src):
+        obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
+        if not force and not extra and os.path.exists(obj) and \
+                os.path.getmtime(obj) >= max(hdr_mt, os.path.getmtime(src)):
+            return obj
+        tmp = obj + f".tmp{os.getpid()}"
+        cmd = [NVCC, *flags, *extra, "-c", "-o", tmp, src]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        os.replace(tmp, obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, sources()))
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *NVCC_FLAGS, *extra, "-o", tmp, *sources()]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+           "-Xcompiler", "-fPIC", "-o", tmp, *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

@@ -24,6 +24,8 @@ static thread_local std::string g_err;
 
 static void set_err(const std::string &s) { g_err = s; }
 
+void mdps_internal_set_error(const std::string &s) { g_err = s; }  // solve.cu
+
 #define CUDA_TRY(call, code)                                                          \
     do {                                                                              \
         cudaError_t e_ = (call);                                                      \

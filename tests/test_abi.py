@@ -84,3 +84,16 @@ def test_product_path_has_no_oracle_or_fallback():
         if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
             src = open(f).read()
             assert "oracle" not in src.replace("CPU oracle (oracle/)", "").replace("oracle/)", ""), f
+
+
+@pytest.mark.parametrize("n,degree,limbs", [(0, 3, 2), (600, 3, 2), (4, -1, 2), (4, 300, 2), (4, 3, 7)])
+def test_solver_create_rejects_invalid_arguments(lib, n, degree, limbs):
+    with pytest.raises(mdps.MdpsError, match="mdps_solver_create"):
+        mdps.Solver(n, degree, limbs)
+
+
+def test_solver_null_handles_are_rejected(lib):
+    assert lib.mdps_solve(None, None, None, None, None) == mdps.MDPS_EINVAL
+    assert lib.mdps_solver_status(None, None, None) == mdps.MDPS_EINVAL
+    assert lib.mdps_solver_stats(None, None) == mdps.MDPS_EINVAL
+    lib.mdps_solver_destroy(None)  # no-op

@@ -1,0 +1,131 @@
+"""CUDA parity of the block lower-triangular Toeplitz solver (libmdps.h
+mdps_solve) against the CPU oracle's forward substitution.
+
+Inputs: mdinputs.random_toeplitz / toeplitz_config (seeded unit-circle series
+matrices, DESIGN.md input recipe).  Metric: the per-series error of
+oracle.series_err (exact differences), tolerance TOL[L] of the north star
+(reading R12).  The exactly solvable permutation case is compared
+bit for bit, the pivot sequence against the oracle's.
+"""
+import numpy as np
+import pytest
+
+import mdinputs
+import oracle
+from tests.gpu_util import NTHREADS, TOL
+
+pytestmark = pytest.mark.gpu
+LEVELS = (2, 3, 4, 5, 8, 10)
+
+
+@pytest.fixture(scope="module")
+def mdps():
+    import torch
+    import paper_2012_06607_b200 as m
+    assert torch.cuda.is_available()
+    m.lib()
+    return m
+
+
+def cuda(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_solve(mdps, t, jac=None):
+    import torch
+    jac = t.jac if jac is None else jac
+    with mdps.Solver(t.n, t.degree, t.limbs) as s:
+        dx = s.solve(cuda(jac), cuda(t.rhs))
+        torch.cuda.synchronize()
+        piv, sing = s.status()
+        return dx.cpu().numpy(), piv, sing
+
+
+@pytest.mark.parametrize("L", LEVELS)
+@pytest.mark.parametrize("n,degree", [(1, 0), (1, 6), (2, 3), (3, 0), (5, 4), (7, 9)])
+def test_small_random(mdps, n, degree, L):
+    t = mdinputs.random_toeplitz(200 + 10 * n + degree, n, degree, L)
+    dx, piv, sing = gpu_solve(mdps, t)
+    want, wpiv = oracle.toeplitz_solve(t.jac, t.rhs, nthreads=NTHREADS)
+    assert not sing
+    assert np.array_equal(piv, wpiv)
+    err = oracle.series_err(dx, want)
+    assert err.max() <= TOL[L], err.max()
+
+
+@pytest.mark.parametrize("L", (2, 5, 10))
+def test_permutation_case_bitexact(mdps, L):
+    """A_0 = P diag(+-2^e, +-i 2^e), A_i = 0: every operation is exact."""
+    n, D = 5, 4
+    rng = np.random.default_rng(3)
+    sigma = [2, 0, 4, 1, 3]
+    s = [(2.0 ** e, 0.0) if k % 2 == 0 else (0.0, -(2.0 ** e)) for k, e in enumerate([1, -3, 0, 5, -2])]
+    jac = np.zeros((n, n, 2, L, D))
+    for k in range(n):
+        jac[sigma[k], k, 0, 0, 0], jac[sigma[k], k, 1, 0, 0] = s[k]
+    rhs = np.zeros((n, 2, L, D))
+    rhs[:, :, 0, :] = rng.integers(-50, 50, size=(n, 2, D)).astype(np.float64)
+    t = mdinputs.ToeplitzInputs("perm", n, D - 1, L, jac, rhs)
+    dx, piv, sing = gpu_solve(mdps, t)
+    want, wpiv = oracle.toeplitz_solve(jac, rhs)
+    assert np.array_equal(piv, wpiv)
+    assert np.array_equal(dx, want)
+
+
+@pytest.mark.parametrize("name", ["dd", "qd"])
+def test_config_full(mdps, name):
+    t = mdinputs.toeplitz_config(name)
+    dx, piv, sing = gpu_solve(mdps, t)
+    want, wpiv = oracle.toeplitz_solve(t.jac, t.rhs, nthreads=NTHREADS)
+    assert np.array_equal(piv, wpiv)
+    err = oracle.series_err(dx, want)
+    assert err.max() <= TOL[t.limbs], err.max()
+
+
+@pytest.mark.parametrize("name,degree", [("od", 15), ("deca", 5)])
+def test_config_leading_coefficients(mdps, name, degree):
+    """Full n and full degree on the GPU; the oracle solves the system
+    truncated at `degree`, which fixes dx_0..dx_degree (truncation invariant,
+    tests/test_oracle_solve.py)."""
+    t = mdinputs.toeplitz_config(name)
+    dx, piv, sing = gpu_solve(mdps, t)
+    tt = t.truncate(degree)
+    want, wpiv = oracle.toeplitz_solve(tt.jac, tt.rhs, nthreads=NTHREADS)
+    assert np.array_equal(piv, wpiv)
+    err = oracle.series_err(np.ascontiguousarray(dx[..., :degree + 1]), want)
+    assert err.max() <= TOL[t.limbs], err.max()
+
+
+@pytest.mark.parametrize("name", ["od", "deca"])
+def test_config_residual_sampled_rows(mdps, name):
+    """Full size: for two sampled rows p, sum_q J_pq * dx_q - b_p formed by the
+    oracle at L+2 limbs is below TOL[L] times the largest product series."""
+    t = mdinputs.toeplitz_config(name)
+    dx, _, _ = gpu_solve(mdps, t)
+    L, Lh = t.limbs, t.limbs + 2
+    pad = lambda a: np.ascontiguousarray(np.pad(a, [(0, 0), (0, Lh - L), (0, 0)]))
+    for p in (0, t.n - 1):
+        acc = pad(-t.rhs[p])
+        scale = 0.0
+        for q in range(t.n):
+            prod = oracle.series_mul(pad(t.jac[p, q]), pad(dx[q]))
+            scale = max(scale, float(np.abs(prod[:, 0]).max()))
+            acc = oracle.series_add(acc, prod)
+        res = float(np.abs(acc[:, 0]).max())
+        assert res <= TOL[L] * scale, (p, res / scale)
+
+
+def test_deterministic(mdps):
+    t = mdinputs.toeplitz_config("qd")
+    a, _, _ = gpu_solve(mdps, t)
+    b, _, _ = gpu_solve(mdps, t)
+    assert np.array_equal(a, b)
+
+
+def test_singular_flag(mdps):
+    t = mdinputs.random_toeplitz(13, 3, 2, 2)
+    jac = t.jac.copy()
+    jac[:, 1, :, :, 0] = 0.0
+    _, _, sing = gpu_solve(mdps, t, jac)
+    assert sing
