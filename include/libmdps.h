@@ -152,7 +152,7 @@ int mdps_system_level_jobs(const mdps_system *sys, int64_t *jobs_per_level, int3
  * ------------------------------------------------------------------------- */
 typedef struct mdps_solver mdps_solver; /* opaque; owns its device workspace */
 
-/* n in [1, 512], degree in [0, 255], limbs in {2,3,4,5,8,10}.  Allocates the
+/* n in [1, 256], degree in [0, 255], limbs in {2,3,4,5,8,10}.  Allocates the
  * workspace (about 2x the Jacobian) on the current device.  NULL on error. */
 mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t limbs);
 
