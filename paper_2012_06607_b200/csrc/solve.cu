@@ -6,27 +6,32 @@
 //   A_0 dx_j = b_j - sum_{i=1..j} A_i dx_{j-i}
 //
 // Three launches per solve:
-//  1. ts_pack_kernel: the Jacobian coefficients A_1..A_d -> digit elements
-//     Ad[k-1][p][q] (kernels_dig.cuh representation: [2][S] digits + two
-//     radix exponents; a group of lanes reading row p reads consecutive q),
-//     the right-hand side -> the digit series R (r_k starts as b_k).
-//  2. ts_gj_kernel (persistent, cooperative): W = A_0^-1 by Gauss-Jordan with
-//     partial pivoting on [A_0 | I] in EFT md arithmetic (md.cuh): the pivots
-//     are those of the paper's LU, A_0 is factored once,
-//     and the d+1 solves become matrix-vector products; W -> digit elements.
-//  3. ts_loop_kernel (persistent, cooperative): for j = 0..d
-//       dx_j = W r_j                              (G lanes per row p)
-//       r_k -= A_{k-j} dx_j  for all k > j        (G lanes per (k, p))
-//     — the right-looking form of the paper's update ("one job is the update
-//     of one right hand side vector after the computation of one update
-//     vector"), so that every phase exposes (d-j) n
-//     independent dot products.  Each dot product (and the subtraction from
-//     r_k) is accumulated EXACTLY on digit planes as in the product kernel —
-//     one DFMA per digit pair — and rounded once (to S digits for r_k and
-//     dx_j, to L limbs for the output).
-// Reductions across lanes are fixed trees (bitwise deterministic).  Grid-wide
-// phases are separated by a software grid barrier (cooperative launch keeps
-// all blocks co-resident).
+//  1. ts_pack_kernel: the Jacobian coefficients A_0..A_d -> digit elements
+//     Ad[k][p][q] (kernels_dig.cuh representation: [2][S] digits + two radix
+//     exponents; a group of lanes reading row p reads consecutive q), the
+//     right-hand side -> digit planes R[k][2][S][n] (r_k starts as b_k).
+//  2. ts_gj_kernel (one block): A_0 is factored once — Gauss-Jordan with
+//     partial pivoting on [A_0 | I] in complex double on the leading limbs
+//     (the pivots of the paper's LU with partial pivoting, PAPER.md:260-262,
+//     GV83 §3.4) — giving W_0 ~ A_0^-1 to double precision.
+//  3. ts_main_kernel (persistent, cooperative):
+//     a. Newton-Schulz refinement W <- W + W (I - A_0 W) until
+//        ||I - A_0 W||^2 is below the md precision (each step squares it):
+//        two n-by-n matrix products per step, every entry an exact digit dot
+//        product — throughput work instead of 3n latency-bound md steps;
+//     b. for j = 0..d
+//          dx_j = W r_j                              (G lanes per row p)
+//          r_k -= A_{k-j} dx_j  for all k > j        (G lanes per (k, p))
+//        — the right-looking form of the paper's update ("one job is the
+//        update of one right hand side vector after the computation of one
+//        update vector"), so that every phase exposes
+//        (d-j) n independent dot products.
+// Every dot product (with its initial value: r_k, W_pc or the identity) is
+// accumulated EXACTLY on digit planes as in the product kernel — one DFMA per
+// digit pair — and rounded once (to S digits for r_k, W, dx_j in digits, to L
+// limbs for dx_out).  Reductions across lanes are fixed trees (bitwise
+// deterministic).  Grid-wide phases are separated by a software grid barrier
+// (the cooperative launch keeps all blocks co-resident).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -36,207 +41,62 @@
 
 #include "../../include/libmdps.h"
 #include "conv_dig.cuh"
-#include "md.cuh"
 
 void mdps_internal_set_error(const std::string &s);  // libmdps.cu
 
 namespace mdps {
 namespace ts {
 
-constexpr int THREADS = 256;
+constexpr int GJ_THREADS = 1024;
+constexpr int MAIN_THREADS = 128;
+constexpr int MAX_REFINE = 8;
 
-struct Barrier {
-    unsigned int count;
+struct Ctl {              // device control block (memset to 0 before every solve)
+    unsigned int count;   // grid barrier
     unsigned int gen;
+    int emax;             // max radix exponent of the entries of E = I - A_0 W (+ bias), 0 = none
+    int status;           // bit 0: singular A_0
+    int refine_steps;     // Newton-Schulz steps run
+    int pad[3];
 };
+constexpr int EMAX_BIAS = 1 << 20;
 
-// sense-free generation barrier over all blocks of a co-resident grid
-__device__ __forceinline__ void grid_sync(Barrier *b) {
+// generation barrier over all blocks of a co-resident grid
+__device__ __forceinline__ void grid_sync(Ctl *c) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned int *vgen = &b->gen;
+        volatile unsigned int *vgen = &c->gen;
         const unsigned int g = *vgen;
         __threadfence();
-        if (atomicAdd(&b->count, 1u) == gridDim.x - 1) {
-            atomicExch(&b->count, 0u);
+        if (atomicAdd(&c->count, 1u) == gridDim.x - 1) {
+            atomicExch(&c->count, 0u);
             __threadfence();
-            atomicAdd(&b->gen, 1u);
+            atomicAdd(&c->gen, 1u);
         } else {
-            while (*vgen == g) __nanosleep(40);
+            while (*vgen == g) __nanosleep(100);
         }
         __threadfence();
     }
     __syncthreads();
 }
 
-// ---- complex md helpers (element = re limbs then im limbs, 2L doubles) --------
-template <int L>
-__device__ __forceinline__ void ld(const double *p, double (&re)[L], double (&im)[L]) {
-#pragma unroll
-    for (int l = 0; l < L; l++) {
-        re[l] = p[l];
-        im[l] = p[L + l];
-    }
-}
-
-template <int L>
-__device__ __forceinline__ void st(double *p, const double (&re)[L], const double (&im)[L]) {
-#pragma unroll
-    for (int l = 0; l < L; l++) {
-        p[l] = re[l];
-        p[L + l] = im[l];
-    }
-}
-
-// (Br, Bi) += (NEG ? -1 : 1) * a * x   (re = ar xr - ai xi, im = ar xi + ai xr)
-template <int L, bool NEG>
-__device__ __forceinline__ void cfma(double (&Br)[L + 1], double (&Bi)[L + 1], const double (&ar)[L],
-                                     const double (&ai)[L], const double (&xr)[L], const double (&xi)[L]) {
-    double pr[L], pi[L], ni[L];
-#pragma unroll
-    for (int l = 0; l < L; l++) {
-        pr[l] = NEG ? -ar[l] : ar[l];
-        pi[l] = NEG ? -ai[l] : ai[l];
-        ni[l] = -pi[l];
-    }
-    bins_fma<L>(Br, pr, xr);
-    bins_fma<L>(Br, ni, xi);
-    bins_fma<L>(Bi, pr, xi);
-    bins_fma<L>(Bi, pi, xr);
-}
-
-template <int L>
-__device__ __forceinline__ void cbins_add(double (&Br)[L + 1], double (&Bi)[L + 1], const double (&ar)[L],
-                                          const double (&ai)[L]) {
-    bins_add<L>(Br, ar);
-    bins_add<L>(Bi, ai);
-}
-
-// B += C (bins of another accumulator: level o deposited at level o)
-template <int L>
-__device__ __forceinline__ void bins_merge(double (&B)[L + 1], const double (&C)[L + 1]) {
-#pragma unroll
-    for (int o = 0; o < L; o++) {
-        double v = C[o];
-#pragma unroll
-        for (int t = o; t < L; t++) two_sum(B[t], v, B[t], v);
-        B[L] = __dadd_rn(B[L], v);
-    }
-    B[L] = __dadd_rn(B[L], C[L]);
-}
-
-// tree reduction over aligned groups of G lanes (G a power of two <= 32);
-// lane 0 of each group ends with the group's sum
-template <int L>
-__device__ __forceinline__ void group_reduce(double (&Br)[L + 1], double (&Bi)[L + 1], int G) {
-    for (int off = G >> 1; off > 0; off >>= 1) {
-        double Cr[L + 1], Ci[L + 1];
-#pragma unroll
-        for (int t = 0; t <= L; t++) {
-            Cr[t] = __shfl_down_sync(0xffffffffu, Br[t], off, G);
-            Ci[t] = __shfl_down_sync(0xffffffffu, Bi[t], off, G);
-        }
-        bins_merge<L>(Br, Cr);
-        bins_merge<L>(Bi, Ci);
-    }
-}
-
-template <int L>
-__device__ __forceinline__ void cmul(const double (&ar)[L], const double (&ai)[L], const double (&xr)[L],
-                                     const double (&xi)[L], double (&zr)[L], double (&zi)[L]) {
-    double Br[L + 1], Bi[L + 1];
-    md_zero(Br);
-    md_zero(Bi);
-    cfma<L, false>(Br, Bi, ar, ai, xr, xi);
-    md_renorm(Br, zr);
-    md_renorm(Bi, zi);
-}
-
-// z = y - a * x, rounded once
-template <int L>
-__device__ __forceinline__ void cfms(const double (&yr)[L], const double (&yi)[L], const double (&ar)[L],
-                                     const double (&ai)[L], const double (&xr)[L], const double (&xi)[L],
-                                     double (&zr)[L], double (&zi)[L]) {
-    double Br[L + 1], Bi[L + 1];
-    md_zero(Br);
-    md_zero(Bi);
-    cbins_add<L>(Br, Bi, yr, yi);
-    cfma<L, true>(Br, Bi, ar, ai, xr, xi);
-    md_renorm(Br, zr);
-    md_renorm(Bi, zi);
-}
-
-// 1/a for a real md number a != 0 by Newton steps y <- y + y (1 - a y) at a
-// growing precision: the step on the leading P limbs doubles the correct bits
-// up to 53 P (P = 2, 4, 8, ..., L, then once more at L).
-template <int L, int P>
-__device__ __forceinline__ void recip_step(const double (&a)[L], double (&y)[L]) {
-    double ap[P], yp[P], nap[P];
-#pragma unroll
-    for (int l = 0; l < P; l++) {
-        ap[l] = a[l];
-        nap[l] = -a[l];
-        yp[l] = y[l];
-    }
-    double B[P + 1], e[P];
-    md_zero(B);
-    B[0] = 1.0;
-    bins_fma<P>(B, nap, yp);
-    md_renorm(B, e);
-    double B2[P + 1];
-    md_zero(B2);
-    bins_add<P>(B2, yp);
-    bins_fma<P>(B2, yp, e);
-    md_renorm(B2, yp);
-#pragma unroll
-    for (int l = 0; l < L; l++) y[l] = l < P ? yp[l] : 0.0;
-    (void)ap;
-}
-
-template <int L>
-__device__ __forceinline__ void md_recip_fast(const double (&a)[L], double (&y)[L]) {
-    md_zero(y);
-    y[0] = __ddiv_rn(1.0, a[0]);
-    recip_step<L, (L < 2 ? L : 2)>(a, y);
-    if (L > 2) recip_step<L, (L < 4 ? L : 4)>(a, y);
-    if (L > 4) recip_step<L, (L < 8 ? L : 8)>(a, y);
-    if (L > 8) recip_step<L, L>(a, y);
-    recip_step<L, L>(a, y);
-}
-
-template <int L>
-__device__ __forceinline__ void c_recip_fast(const double (&ar)[L], const double (&ai)[L], double (&rr)[L],
-                                             double (&ri)[L]) {
-    double B[L + 1], den[L], y[L], t[L];
-    md_zero(B);
-    bins_fma<L>(B, ar, ar);
-    bins_fma<L>(B, ai, ai);
-    md_renorm(B, den);
-    md_recip_fast<L>(den, y);
-    md_mul<L>(ar, y, rr);
-    md_mul<L>(ai, y, t);
-#pragma unroll
-    for (int l = 0; l < L; l++) ri[l] = -t[l];
-}
-
-// ---- 1. pack: Jacobian coefficients 1..d -> digit elements, rhs -> digit series ----
-// Ad[k-1][p][q] = [2][S] digits (part, digit) + exponents Ae[..][2]; Rd / Re in
-// the pool's series layout [n][2][S][D] / [n][2][D] (the
-// right-hand sides r_k start as b_k, negated for a Newton step).
+// ---- 1. pack ---------------------------------------------------------------------
+// Ad[k][p][q] = [2][S] digits + exponents Ae[k][p][q][2] (k = 0..d);
+// R planes [k][2][S][n] + exponents [k][2][n] (negated for a Newton step).
 template <int L>
 __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__ J, const double *__restrict__ b,
                                                       double *__restrict__ Ad, int *__restrict__ Ae,
-                                                      double *__restrict__ Rd, int *__restrict__ Re, int n, int D,
+                                                      double *__restrict__ Rp, int *__restrict__ Re, int n, int D,
                                                       int negate) {
     constexpr int S = digits_for(L);
-    const size_t nj = (size_t)n * n * (D - 1), total = nj + (size_t)n * D;
+    const size_t nj = (size_t)n * n * D, total = nj + (size_t)n * D;
     for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (size_t)gridDim.x * blockDim.x) {
-        if (g < nj) {  // (k >= 1, p, q): k fastest for coalesced limb reads
-            const int k = 1 + (int)(g % (D - 1));
-            const size_t pq = g / (D - 1);
+        if (g < nj) {  // (p, q, k): k fastest for coalesced limb reads
+            const int k = (int)(g % D);
+            const size_t pq = g / D;
             const double *src = J + pq * 2 * L * D + k;
-            double *dst = Ad + (((size_t)(k - 1) * n * n) + pq) * 2 * S;
-            int *de = Ae + (((size_t)(k - 1) * n * n) + pq) * 2;
+            double *dst = Ad + ((size_t)k * n * n + pq) * 2 * S;
+            int *de = Ae + ((size_t)k * n * n + pq) * 2;
 #pragma unroll 1
             for (int part = 0; part < 2; part++) {
                 double v[L], d[S];
@@ -258,151 +118,132 @@ __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__
                     const double x = b[(p * 2 * L + part * L + l) * D + k];
                     v[l] = negate ? -x : x;
                 }
-                Re[(p * 2 + part) * D + k] = limbs_to_digits<L, S>(v, d);
+                Re[((size_t)k * 2 + part) * n + p] = limbs_to_digits<L, S>(v, d);
 #pragma unroll
-                for (int t = 0; t < S; t++) Rd[((p * 2 + part) * S + t) * D + k] = d[t];
+                for (int t = 0; t < S; t++) Rp[(((size_t)k * 2 + part) * S + t) * n + p] = d[t];
             }
         }
     }
 }
 
-// ---- 2. W = A_0^-1 by Gauss-Jordan elimination with partial pivoting ------------------
-// [A_0 | I] -> [I | A_0^-1] (GV83 §3.4): the pivots are those of the LU with
-// partial pivoting of A_0 (rows below the pivot see the same Schur
-// complement), so A_0 is still factored once; Gauss-Jordan needs n instead of
-// 3n dependent steps.  Per step k one block picks the pivot (max |re_0| +
-// |im_0|, lowest row on ties), swaps, inverts it (one warp) and scales row k;
-// then the grid eliminates column k from every other row.  Complex md in EFT
-// level bins; W is converted to digit elements at the end.
+// ---- 2. factor A_0 once: Gauss-Jordan, partial pivoting, complex double -------------
+// [A_0 | I] -> [I | W_0] on the leading limbs (one block; M in global memory,
+// L2-resident).  Pivot k = the row i >= k maximising |re| + |im| (lowest row
+// on ties).  W_0 -> digit elements (rows) and digit column planes.
 template <int L>
-__global__ void __launch_bounds__(THREADS) ts_gj_kernel(const double *__restrict__ J, double *__restrict__ Ma,
-                                                        double *__restrict__ Mi, int *__restrict__ piv,
-                                                        int *__restrict__ status, double *__restrict__ Wd,
-                                                        int *__restrict__ We, int n, int D, Barrier *bar) {
-    constexpr int E = 2 * L;
+__global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restrict__ J, double *__restrict__ M,
+                                                           int *__restrict__ piv, Ctl *ctl, double *__restrict__ Wr,
+                                                           int *__restrict__ Wre, double *__restrict__ Wc,
+                                                           int *__restrict__ Wce, int n, int D) {
     constexpr int S = digits_for(L);
-    const int nth = gridDim.x * blockDim.x;
-    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int tx = threadIdx.x;
-    __shared__ double s_m[THREADS];
-    __shared__ int s_i[THREADS];
-    __shared__ double s_inv[E];
-
-    for (size_t t = tid; t < (size_t)n * n; t += nth) {  // Ma = A_0 (coefficient 0 of J), Mi = I
-#pragma unroll
-        for (int u = 0; u < E; u++) {
-            Ma[t * E + u] = J[(t * E + u) * D];
-            Mi[t * E + u] = (u == 0 && t / n == t % n) ? 1.0 : 0.0;
+    const int tx = threadIdx.x, nt = blockDim.x;
+    const int W2 = 2 * n;  // row length of [A | I] in complex entries
+    __shared__ double s_m[GJ_THREADS];
+    __shared__ int s_i[GJ_THREADS];
+    __shared__ double s_p[2];
+    double2 *Mc = reinterpret_cast<double2 *>(M);
+    for (int t = tx; t < n * W2; t += nt) {
+        const int i = t / W2, c = t - i * W2;
+        double2 v;
+        if (c < n) {
+            const double *src = J + ((size_t)i * n + c) * 2 * L * D;
+            v = make_double2(src[0], src[(size_t)L * D]);
+        } else {
+            v = make_double2(c - n == i ? 1.0 : 0.0, 0.0);
         }
+        Mc[t] = v;
     }
-    if (tid == 0) *status = 0;
-    grid_sync(bar);
-
+    __syncthreads();
+    bool singular = false;
     for (int k = 0; k < n; k++) {
-        if (blockIdx.x == 0) {
-            double bm = -1.0;
-            int bi = n;
-            for (int i = k + tx; i < n; i += blockDim.x) {
-                const double *a = Ma + ((size_t)i * n + k) * E;
-                const double m = __dadd_rn(fabs(a[0]), fabs(a[L]));
-                if (m > bm) {
-                    bm = m;
-                    bi = i;
-                }
-            }
-            s_m[tx] = bm;
-            s_i[tx] = bi;
-            __syncthreads();
-            for (int off = blockDim.x >> 1; off > 0; off >>= 1) {
-                if (tx < off) {
-                    const double m2 = s_m[tx + off];
-                    const int i2 = s_i[tx + off];
-                    if (m2 > s_m[tx] || (m2 == s_m[tx] && i2 < s_i[tx])) {
-                        s_m[tx] = m2;
-                        s_i[tx] = i2;
-                    }
-                }
-                __syncthreads();
-            }
-            const bool sing = !(s_m[0] > 0.0) || s_i[0] >= n;
-            const int p = sing ? k : s_i[0];
-            if (p != k)
-                for (int t = tx; t < 2 * n * E; t += blockDim.x) {
-                    double *M = t < n * E ? Ma : Mi;
-                    const int u = t < n * E ? t : t - n * E;
-                    double *rk = M + (size_t)k * n * E + u, *rp = M + (size_t)p * n * E + u;
-                    const double v = *rk;
-                    *rk = *rp;
-                    *rp = v;
-                }
-            __syncthreads();
-            if (tx < 32) {  // one warp inverts the pivot
-                double ir[L], ii[L];
-                if (sing) {
-                    md_zero(ir);
-                    md_zero(ii);
-                } else {
-                    double ar[L], ai[L];
-                    ld<L>(Ma + ((size_t)k * n + k) * E, ar, ai);
-                    c_recip_fast<L>(ar, ai, ir, ii);
-                }
-                if (tx == 0) {
-                    st<L>(s_inv, ir, ii);
-                    piv[k] = p;
-                    if (sing) atomicOr(status, 1);
-                }
-            }
-            __syncthreads();
-            double ir[L], ii[L];
-            ld<L>(s_inv, ir, ii);
-            // scale row k: Ma[k][c] (c > k) and Mi[k][c] (all c)
-            for (int t = tx; t < 2 * n - k - 1; t += blockDim.x) {
-                double *a = t < n - k - 1 ? Ma + ((size_t)k * n + k + 1 + t) * E : Mi + ((size_t)k * n + t - (n - k - 1)) * E;
-                double ar[L], ai[L], zr[L], zi[L];
-                ld<L>(a, ar, ai);
-                cmul<L>(ir, ii, ar, ai, zr, zi);
-                st<L>(a, zr, zi);
+        double bm = -1.0;
+        int bi = n;
+        for (int i = k + tx; i < n; i += nt) {
+            const double2 a = Mc[(size_t)i * W2 + k];
+            const double m = __dadd_rn(fabs(a.x), fabs(a.y));
+            if (m > bm) {
+                bm = m;
+                bi = i;
             }
         }
-        grid_sync(bar);
-        // eliminate column k from rows i != k
-        const int cols = 2 * n - k - 1;
-        for (int t = tid; t < (n - 1) * cols; t += nth) {
+        s_m[tx] = bm;
+        s_i[tx] = bi;
+        __syncthreads();
+        for (int off = nt >> 1; off > 0; off >>= 1) {
+            if (tx < off) {
+                const double m2 = s_m[tx + off];
+                const int i2 = s_i[tx + off];
+                if (m2 > s_m[tx] || (m2 == s_m[tx] && i2 < s_i[tx])) {
+                    s_m[tx] = m2;
+                    s_i[tx] = i2;
+                }
+            }
+            __syncthreads();
+        }
+        const bool sing = !(s_m[0] > 0.0) || s_i[0] >= n;
+        const int p = sing ? k : s_i[0];
+        singular |= sing;
+        __syncthreads();
+        if (p != k)
+            for (int c = tx; c < W2; c += nt) {
+                const double2 v = Mc[(size_t)k * W2 + c];
+                Mc[(size_t)k * W2 + c] = Mc[(size_t)p * W2 + c];
+                Mc[(size_t)p * W2 + c] = v;
+            }
+        if (tx == 0) piv[k] = p;
+        __syncthreads();
+        if (tx == 0) {  // 1 / pivot
+            const double2 a = Mc[(size_t)k * W2 + k];
+            const double den = __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+            s_p[0] = sing ? 0.0 : __ddiv_rn(a.x, den);
+            s_p[1] = sing ? 0.0 : __ddiv_rn(-a.y, den);
+        }
+        __syncthreads();
+        const double ir = s_p[0], ii = s_p[1];
+        for (int c = k + tx; c < W2; c += nt) {  // scale row k
+            const double2 v = Mc[(size_t)k * W2 + c];
+            Mc[(size_t)k * W2 + c] = make_double2(__dsub_rn(__dmul_rn(v.x, ir), __dmul_rn(v.y, ii)),
+                                                  __dadd_rn(__dmul_rn(v.x, ii), __dmul_rn(v.y, ir)));
+        }
+        __syncthreads();
+        const int cols = W2 - k - 1;
+        for (int t = tx; t < (n - 1) * cols; t += nt) {  // eliminate column k from rows i != k
             int i = t / cols;
-            const int c = t - i * cols;
+            const int c = k + 1 + (t - i * cols);
             if (i >= k) i++;
-            double *a = c < n - k - 1 ? Ma + ((size_t)i * n + k + 1 + c) * E : Mi + ((size_t)i * n + c - (n - k - 1)) * E;
-            const double *u = c < n - k - 1 ? Ma + ((size_t)k * n + k + 1 + c) * E : Mi + ((size_t)k * n + c - (n - k - 1)) * E;
-            double yr[L], yi[L], lr[L], li[L], ur[L], ui[L], zr[L], zi[L];
-            ld<L>(a, yr, yi);
-            ld<L>(Ma + ((size_t)i * n + k) * E, lr, li);
-            ld<L>(u, ur, ui);
-            cfms<L>(yr, yi, lr, li, ur, ui, zr, zi);
-            st<L>(a, zr, zi);
+            const double2 f = Mc[(size_t)i * W2 + k], u = Mc[(size_t)k * W2 + c], v = Mc[(size_t)i * W2 + c];
+            Mc[(size_t)i * W2 + c] =
+                make_double2(__dsub_rn(v.x, __dsub_rn(__dmul_rn(f.x, u.x), __dmul_rn(f.y, u.y))),
+                             __dsub_rn(v.y, __dadd_rn(__dmul_rn(f.x, u.y), __dmul_rn(f.y, u.x))));
         }
-        grid_sync(bar);
+        __syncthreads();
     }
-
-    // W = Mi -> digit elements [p][q][2][S] + exponents [p][q][2]
-    for (size_t t = tid; t < (size_t)n * n; t += nth) {
+    if (tx == 0 && singular) atomicOr(&ctl->status, 1);
+    for (int t = tx; t < n * n; t += nt) {  // W_0 -> digits: rows [p][q][2][S], column planes [c][2][S][row]
+        const int p = t / n, q = t - p * n;
+        const double2 w = Mc[(size_t)p * W2 + n + q];
 #pragma unroll 1
         for (int part = 0; part < 2; part++) {
             double v[L], d[S];
 #pragma unroll
-            for (int l = 0; l < L; l++) v[l] = Mi[t * E + part * L + l];
-            We[t * 2 + part] = limbs_to_digits<L, S>(v, d);
+            for (int l = 0; l < L; l++) v[l] = l == 0 ? (part ? w.y : w.x) : 0.0;
+            const int e = limbs_to_digits<L, S>(v, d);
+            Wre[(size_t)t * 2 + part] = e;
+            Wce[((size_t)q * 2 + part) * n + p] = e;
 #pragma unroll
-            for (int u = 0; u < S; u++) Wd[(t * 2 + part) * S + u] = d[u];
+            for (int s = 0; s < S; s++) {
+                Wr[((size_t)t * 2 + part) * S + s] = d[s];
+                Wc[(((size_t)q * 2 + part) * S + s) * n + p] = d[s];
+            }
         }
     }
 }
 
-// ---- 3. the substitution loop on digits ---------------------------------------------
-// Dot products sum_q a_q x_q of complex md numbers accumulated EXACTLY as in the
-// product kernel (kernels_dig.cuh): a_q are digit elements read from global
-// memory (row p of W or of A_{k-j}), x_q a digit vector staged in shared
+// ---- 3. exact digit dot products -------------------------------------------------------
+// sum_q a_q x_q of complex md numbers: a_q digit elements [2][S] read from
+// global memory (row p of a matrix), x_q a digit vector staged in shared
 // memory as planes [part][PADZ + S][n] (PADZ zero planes for the alignment
-// shift); one real part per pass, one DFMA per digit pair.
+// shift).  One real part per pass, one DFMA per digit pair.
 template <int L>
 __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, const int *__restrict__ aexp,
                                             const double *__restrict__ xs, const int *__restrict__ xe, int n,
@@ -468,142 +309,242 @@ __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, con
     carry_pass(A);
 }
 
-// stage coefficient k of the digit series vector (Xd, Xe) [n][2][S][D] as
-// planes [part][PADZ + S][n] (+ exponents [part][n]), optionally negated
+// stage a digit vector given as planes [2][S][n] (+ exponents [2][n]) into
+// shared planes [2][PADZ + S][n], optionally negated
 template <int L>
-__device__ __forceinline__ void ts_stage(const double *__restrict__ Xd, const int *__restrict__ Xe, int n, int D,
-                                         int k, bool negate, double *xs, int *xe) {
+__device__ __forceinline__ void ts_stage(const double *__restrict__ src, const int *__restrict__ srce, int n,
+                                         bool negate, double *xs, int *xe) {
     constexpr int S = digits_for(L);
     constexpr int P2 = PADZ + S;
-    for (int t = threadIdx.x; t < 2 * P2 * n; t += blockDim.x) {
-        const int part = t / (P2 * n), r = t - part * P2 * n;
-        const int pl = r / n, q = r - pl * n;
-        double v = 0.0;
-        if (pl >= PADZ) {
-            v = Xd[(((size_t)q * 2 + part) * S + (pl - PADZ)) * D + k];
-            if (negate) v = -v;
+    const int SN = S * n;
+#pragma unroll
+    for (int part = 0; part < 2; part++) {
+        double *dst = xs + ((size_t)part * P2 + PADZ) * n;
+        const double *s0 = src + (size_t)part * SN;
+        for (int t = threadIdx.x; t < SN; t += blockDim.x) {
+            const double v = s0[t];
+            dst[t] = negate ? -v : v;
         }
-        xs[t] = v;
+        double *z = xs + (size_t)part * P2 * n;
+        for (int t = threadIdx.x; t < PADZ * n; t += blockDim.x) z[t] = 0.0;
     }
-    for (int t = threadIdx.x; t < 2 * n; t += blockDim.x) {
-        const int part = t / n, q = t - part * n;
-        xe[t] = Xe[((size_t)q * 2 + part) * D + k];
-    }
+    for (int t = threadIdx.x; t < 2 * n; t += blockDim.x) xe[t] = srce[t];
 }
 
-// One task: out = (init) + sum_q arow[q] x_q over the G lanes of a group,
-// written as digits (zd/ze, coefficient k of a digit series) and optionally
-// limbs (zl).  init: an element of a digit series (Id/Ie at coefficient k) or
-// none.  All lanes of the warp call this (shuffles); `valid` masks the output.
+// A digit vector element in planes: digit s of part at d[(part*S + s)*stride],
+// its exponent at e[part*stride].
+struct DigRef {
+    const double *d;
+    const int *e;
+    int stride;
+};
+struct DigOut {
+    double *d;
+    int *e;
+    int stride;
+};
+
+// One task: out = init + sum_q arow[q] x_q over the G lanes of a group (G a
+// power of two; groups aligned in the warp).  init: a digit value (init.d) or
+// the identity (one: +1 to the real part) or nothing.  The result is written
+// as digits (out) and optionally as L limbs at zl[(part*L + l)*lstride].
+// Returns the larger output part exponent.  All lanes of the warp call it
+// (shuffles); `valid` masks the work and the output.
 template <int L>
-__device__ __forceinline__ void ts_task(const double *__restrict__ arow, const int *__restrict__ aexp,
-                                        const double *xs, const int *xe, int n, int lg, int G, bool valid,
-                                        const double *Id, const int *Ie, double *zd, int *ze, double *zl, int D,
-                                        int k, double *scratch) {
+__device__ __forceinline__ int ts_task(const double *__restrict__ arow, const int *__restrict__ aexp,
+                                       const double *xs, const int *xe, int n, int lg, int G, bool valid,
+                                       DigRef init, bool one, DigOut out, double *zl, int lstride,
+                                       double *scratch) {
     constexpr int S = digits_for(L);
-    // anchors per part: max exponent over the terms (and the init value + 1)
-    int ear = ZERO_E, eai = ZERO_E;
+    int ea0 = ZERO_E, ea1 = ZERO_E;
     if (valid) {
         for (int q = lg; q < n; q += G) {
             const int er = aexp[2 * q], ei = aexp[2 * q + 1], xr = xe[q], xi = xe[n + q];
-            ear = max(ear, max(er + xr, ei + xi));
-            eai = max(eai, max(er + xi, ei + xr));
+            ea0 = max(ea0, max(er + xr, ei + xi));
+            ea1 = max(ea1, max(er + xi, ei + xr));
         }
-        if (Id && lg == 0) {
-            ear = max(ear, Ie[k] + 1);
-            eai = max(eai, Ie[D + k] + 1);
+        if (lg == 0) {
+            if (init.d) {
+                ea0 = max(ea0, init.e[0] + 1);
+                ea1 = max(ea1, init.e[init.stride] + 1);
+            }
+            if (one) ea0 = max(ea0, 2);  // 1 = digit 0 of exponent 1
         }
     }
-    for (int off = G >> 1; off > 0; off >>= 1) {
-        ear = max(ear, __shfl_xor_sync(0xffffffffu, ear, off, G));
-        eai = max(eai, __shfl_xor_sync(0xffffffffu, eai, off, G));
+    for (int off = G >> 1; off > 0; off >>= 1) {  // xor partners stay inside the aligned group
+        ea0 = max(ea0, __shfl_xor_sync(0xffffffffu, ea0, off));
+        ea1 = max(ea1, __shfl_xor_sync(0xffffffffu, ea1, off));
     }
-    ear = max(ear, ZERO_E);
-    eai = max(eai, ZERO_E);
+    int eout = ZERO_E;
 #pragma unroll 1
     for (int part = 0; part < 2; part++) {
-        const int eacc = part ? eai : ear;
+        const int eacc = max(part ? ea1 : ea0, ZERO_E);
         double A[S];
         ts_dot_pass<L>(arow, aexp, xs, xe, valid ? n : 0, lg, G, part, eacc, A);
-        if (valid && Id && lg == 0) {  // the init value: digit s has weight R^(eI-1-s) = slot s + eacc-1-eI
-            const int eI = Ie[part * D + k];
-            if (eI > ZERO_E / 2) {
-                const int dI = eacc - 1 - eI;
-                const double *src = Id + (size_t)part * S * D + k;
+        if (valid && lg == 0) {
+            if (init.d) {  // digit s of the init value has weight R^(eI-1-s): slot s + eacc-1-eI
+                const int eI = init.e[part * init.stride];
+                if (eI > ZERO_E / 2) {
+                    const int dI = eacc - 1 - eI;
+                    const double *src = init.d + (size_t)part * S * init.stride;
 #pragma unroll
-                for (int t = 0; t < S; t++) {
-                    const int s = t - dI;
-                    if (s >= 0 && s < S) A[t] = __dadd_rn(A[t], src[(size_t)s * D]);
+                    for (int t = 0; t < S; t++) {
+                        const int s = t - dI;
+                        if (s >= 0 && s < S) A[t] = __dadd_rn(A[t], src[(size_t)s * init.stride]);
+                    }
                 }
+            }
+            if (one && part == 0) {  // weight R^0 = slot eacc - 2
+                const int t0 = eacc - 2;
+#pragma unroll
+                for (int u = 0; u < S; u++)
+                    if (u == t0) A[u] = __dadd_rn(A[u], 1.0);
             }
         }
         for (int off = G >> 1; off > 0; off >>= 1) {
 #pragma unroll
-            for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off, G));
+            for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
         }
-        if (valid && lg == 0) conv_dig_emit<L>(A, eacc, zd, ze, zl, D, k, part, scratch);
+        if (valid && lg == 0) {
+            conv_dig_emit<L>(A, eacc, out.d, out.e, nullptr, out.stride, 0, part, scratch);
+            eout = max(eout, out.e[part * out.stride]);
+            if (zl) {  // A is carry-normalised by the emit
+                double o[L];
+                digits_to_limbs<L, S, true>(A, eacc - 1, o);
+#pragma unroll
+                for (int l = 0; l < L; l++) zl[(size_t)(part * L + l) * lstride] = o[l];
+            }
+        }
     }
+    return eout;
 }
 
+// lanes per task: the smallest power of two in [4, 32] that fills the threads
+// `avail` in one round, as long as every lane keeps >= 8 terms
+__device__ __forceinline__ int pick_group(long long tasks, int n, long long avail) {
+    int G = 4;
+    while (G < 32 && tasks * G < avail && n / (2 * G) >= 8) G <<= 1;
+    return G;
+}
+
+// Newton-Schulz refinement of W, then the substitution loop.
 template <int L>
-__global__ void __launch_bounds__(128, L <= 8 ? 3 : 2) ts_loop_kernel(
-    const double *__restrict__ Ad, const int *__restrict__ Ae, const double *__restrict__ Wd,
-    const int *__restrict__ We, double *__restrict__ Rd, int *__restrict__ Re, double *__restrict__ Xd,
-    int *__restrict__ Xe, double *__restrict__ dx, int n, int D, Barrier *bar) {
+__global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
+    const double *__restrict__ Ad, const int *__restrict__ Ae, double *__restrict__ Wr, int *__restrict__ Wre,
+    double *__restrict__ Wc, int *__restrict__ Wce, double *__restrict__ Ec, int *__restrict__ Ece,
+    double *__restrict__ Rp, int *__restrict__ Re, double *__restrict__ Xp, int *__restrict__ Xe,
+    double *__restrict__ dx, int n, int D, Ctl *ctl) {
     constexpr int S = digits_for(L);
     constexpr int P2 = PADZ + S;
     extern __shared__ __align__(16) double sm[];
-    double *xs = sm;                                  // [2][P2][n]
-    int *xe = (int *)(xs + (size_t)2 * P2 * n);       // [2][n]
-    double *scr = (double *)(xe + 2 * n + 2);         // [blockDim/4][S+2] emit scratch (one per group leader)
+    double *xs = sm;                             // [2][P2][n]
+    int *xe = (int *)(xs + (size_t)2 * P2 * n);  // [2][n]
+    double *scr = (double *)(xe + 2 * n + 2);    // [blockDim/4][S+2] emit scratch (one per group leader)
+    __shared__ int s_emax;
     const int nth = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t SER = (size_t)2 * S * D;             // doubles per digit series
+    const size_t VEC = (size_t)2 * S * n;        // doubles per digit vector (planes)
+    double *scratch = scr + (size_t)(threadIdx.x / 4) * (S + 2);
+    // matrix products: column c per block, rows p over the block's groups
+    const int Gm = pick_group(n, n, blockDim.x);
+    const int gpb = blockDim.x / Gm, gm = threadIdx.x / Gm, lgm = threadIdx.x % Gm;
 
+    // a. W <- W + W (I - A_0 W): columns of E and W are digit vectors (planes)
+    for (int it = 0; it < MAX_REFINE; it++) {
+        if (threadIdx.x == 0) s_emax = ZERO_E;
+        for (int c = blockIdx.x; c < n; c += gridDim.x) {  // E[:, c] = e_c - A_0 W[:, c]
+            ts_stage<L>(Wc + (size_t)c * VEC, Wce + (size_t)c * 2 * n, n, true, xs, xe);
+            __syncthreads();
+            for (int base = 0; base < n; base += gpb) {
+                const int p = base + gm;
+                const bool valid = p < n;
+                const int pp = valid ? p : 0;
+                const int e = ts_task<L>(Ad + (size_t)pp * n * 2 * S, Ae + (size_t)pp * n * 2, xs, xe, n, lgm, Gm,
+                                         valid, DigRef{nullptr, nullptr, 0}, pp == c,
+                                         DigOut{Ec + (size_t)c * VEC + pp, Ece + (size_t)c * 2 * n + pp, n},
+                                         nullptr, 0, scratch);
+                if (valid && lgm == 0) atomicMax(&s_emax, e);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0 && s_emax > ZERO_E / 2) atomicMax(&ctl->emax, s_emax + EMAX_BIAS);
+        grid_sync(ctl);
+        // ||E|| < R^emax / 2; W += W E leaves an error ~||E||^2: stop once that
+        // is below 2^-(53 L + 16)
+        const int eraw = *(volatile int *)&ctl->emax;
+        const bool last = eraw == 0 || 2 * (BETA * (eraw - EMAX_BIAS) - 1) < -(53 * L + 16) || it + 1 == MAX_REFINE;
+        for (int c = blockIdx.x; c < n; c += gridDim.x) {  // W[:, c] += W E[:, c]
+            ts_stage<L>(Ec + (size_t)c * VEC, Ece + (size_t)c * 2 * n, n, false, xs, xe);
+            __syncthreads();
+            for (int base = 0; base < n; base += gpb) {
+                const int p = base + gm;
+                const bool valid = p < n;
+                const int pp = valid ? p : 0;
+                ts_task<L>(Wr + (size_t)pp * n * 2 * S, Wre + (size_t)pp * n * 2, xs, xe, n, lgm, Gm, valid,
+                           DigRef{Wc + (size_t)c * VEC + pp, Wce + (size_t)c * 2 * n + pp, n}, false,
+                           DigOut{Wc + (size_t)c * VEC + pp, Wce + (size_t)c * 2 * n + pp, n}, nullptr, 0, scratch);
+            }
+            __syncthreads();
+        }
+        grid_sync(ctl);
+        for (size_t t = tid; t < (size_t)n * n; t += nth) {  // rows <- columns
+            const int p = (int)(t / n), c = (int)(t % n);
+#pragma unroll
+            for (int part = 0; part < 2; part++) {
+                Wre[t * 2 + part] = Wce[((size_t)c * 2 + part) * n + p];
+#pragma unroll
+                for (int s = 0; s < S; s++)
+                    Wr[(t * 2 + part) * S + s] = Wc[(size_t)c * VEC + (size_t)(part * S + s) * n + p];
+            }
+        }
+        if (tid == 0) {
+            ctl->emax = 0;
+            ctl->refine_steps = it + 1;
+        }
+        grid_sync(ctl);
+        if (last) break;
+    }
+
+    // b. the substitution loop
     for (int j = 0; j < D; j++) {
-        // dx_j = W r_j: G lanes per row p
-        ts_stage<L>(Rd, Re, n, D, j, false, xs, xe);
-        __syncthreads();
-        {
-            int G = 4;
-            while (G < 32 && (long long)n * G * 2 < nth) G <<= 1;
+        {  // dx_j = W r_j
+            ts_stage<L>(Rp + (size_t)j * VEC, Re + (size_t)j * 2 * n, n, false, xs, xe);
+            __syncthreads();
+            const int G = pick_group(n, n, nth);
             const int ng = nth / G, g = tid / G, lg = tid % G;
-            double *scratch = scr + (size_t)(threadIdx.x / 4) * (S + 2);
             for (int base = 0; base < n; base += ng) {
                 const int p = base + g;
                 const bool valid = p < n;
                 const int pp = valid ? p : 0;
-                ts_task<L>(Wd + (size_t)pp * n * 2 * S, We + (size_t)pp * n * 2, xs, xe, n, lg, G, valid, nullptr,
-                           nullptr, Xd + pp * SER, Xe + (size_t)pp * 2 * D, dx + (size_t)pp * 2 * L * D, D, j,
-                           scratch);
+                ts_task<L>(Wr + (size_t)pp * n * 2 * S, Wre + (size_t)pp * n * 2, xs, xe, n, lg, G, valid,
+                           DigRef{nullptr, nullptr, 0}, false, DigOut{Xp + pp, Xe + pp, n},
+                           dx + (size_t)pp * 2 * L * D + j, D, scratch);
             }
         }
-        grid_sync(bar);
+        grid_sync(ctl);
         if (j + 1 == D) break;
-
-        // r_k -= A_{k-j} dx_j for k = j+1..d: G lanes per (k, p)
-        ts_stage<L>(Xd, Xe, n, D, j, true, xs, xe);
-        __syncthreads();
-        {
+        {  // r_k -= A_{k-j} dx_j, k = j+1..d
+            ts_stage<L>(Xp, Xe, n, true, xs, xe);
+            __syncthreads();
             const int T = (D - 1 - j) * n;
-            int G = 4;
-            while (G < 32 && (long long)T * G < nth) G <<= 1;
+            const int G = pick_group(T, n, nth);
             const int ng = nth / G, g = tid / G, lg = tid % G;
-            double *scratch = scr + (size_t)(threadIdx.x / 4) * (S + 2);
             for (int base = 0; base < T; base += ng) {
                 const int task = base + g;
                 const bool valid = task < T;
                 const int k = j + 1 + (valid ? task / n : 0), p = valid ? task % n : 0;
-                const size_t row = ((size_t)(k - j - 1) * n + p) * n;
-                ts_task<L>(Ad + row * 2 * S, Ae + row * 2, xs, xe, n, lg, G, valid, Rd + p * SER,
-                           Re + (size_t)p * 2 * D, Rd + p * SER, Re + (size_t)p * 2 * D, nullptr, D, k, scratch);
+                const size_t row = ((size_t)(k - j) * n + p) * n;
+                double *rk = Rp + (size_t)k * VEC + p;
+                int *rke = Re + (size_t)k * 2 * n + p;
+                ts_task<L>(Ad + row * 2 * S, Ae + row * 2, xs, xe, n, lg, G, valid, DigRef{rk, rke, n}, false,
+                           DigOut{rk, rke, n}, nullptr, 0, scratch);
             }
         }
-        grid_sync(bar);
+        grid_sync(ctl);
     }
 }
 
-__host__ __device__ inline size_t ts_loop_smem(int S, int n, int threads) {
+__host__ __device__ inline size_t ts_main_smem(int S, int n, int threads) {
     return (size_t)2 * (PADZ + S) * n * sizeof(double) + (size_t)(2 * n + 2) * sizeof(int) +
            (size_t)(threads / 4) * (S + 2) * sizeof(double);
 }
@@ -616,12 +557,12 @@ using namespace mdps;
 struct mdps_solver {
     int n = 0, D = 0, L = 0, S = 0;
     int device = 0;
-    double *Ad = nullptr, *Ma = nullptr, *Mi = nullptr, *Wd = nullptr, *Rd = nullptr, *Xd = nullptr;
-    int *Ae = nullptr, *We = nullptr, *Re = nullptr, *Xe = nullptr;
-    int *piv = nullptr, *status = nullptr;
-    ts::Barrier *bar = nullptr;
-    int grid_gj = 0, grid_loop = 0;
-    size_t smem_loop = 0;
+    double *Ad = nullptr, *M = nullptr, *Wr = nullptr, *Wc = nullptr, *Ec = nullptr, *Rp = nullptr, *Xp = nullptr;
+    int *Ae = nullptr, *Wre = nullptr, *Wce = nullptr, *Ece = nullptr, *Re = nullptr, *Xe = nullptr;
+    int *piv = nullptr;
+    ts::Ctl *ctl = nullptr;
+    int grid_main = 0;
+    size_t smem_main = 0;
     size_t bytes = 0;
     cudaStream_t last = nullptr;
 };
@@ -638,23 +579,21 @@ struct mdps_solver {
 template <int L>
 struct TsGeom {
     static int run(mdps_solver *s) {
-        int dev = 0, sms = 0, per_gj = 0, per_loop = 0;
+        int dev = 0, sms = 0, per = 0;
         TS_TRY(cudaGetDevice(&dev), MDPS_ECUDA);
         TS_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), MDPS_ECUDA);
-        s->smem_loop = ts::ts_loop_smem(digits_for(L), s->n, 128);
-        TS_TRY(cudaFuncSetAttribute(ts::ts_loop_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)s->smem_loop),
+        s->smem_main = ts::ts_main_smem(digits_for(L), s->n, ts::MAIN_THREADS);
+        TS_TRY(cudaFuncSetAttribute(ts::ts_main_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)s->smem_main),
                MDPS_ECUDA);
-        TS_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_gj, ts::ts_gj_kernel<L>, ts::THREADS, 0),
+        TS_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ts::ts_main_kernel<L>, ts::MAIN_THREADS,
+                                                             s->smem_main),
                MDPS_ECUDA);
-        TS_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_loop, ts::ts_loop_kernel<L>, 128, s->smem_loop),
-               MDPS_ECUDA);
-        if (per_gj < 1 || per_loop < 1) {
-            mdps_internal_set_error("solver kernels do not fit on an SM");
+        if (per < 1) {
+            mdps_internal_set_error("solver kernel does not fit on an SM");
             return MDPS_ECUDA;
         }
-        s->grid_gj = sms * per_gj;
-        s->grid_loop = sms * per_loop;
+        s->grid_main = sms * per;
         return MDPS_OK;
     }
 };
@@ -663,28 +602,23 @@ template <int L>
 struct TsRun {
     static int run(mdps_solver *s, const double *J, const double *b, double *dx, int negate, cudaStream_t st) {
         const int n = s->n, D = s->D;
-        const size_t total = (size_t)n * n * (D - 1) + (size_t)n * D;
+        const size_t total = (size_t)n * n * D + (size_t)n * D;
         const int pb = (int)std::min<size_t>((total + 127) / 128, 148 * 32);
-        ts::ts_pack_kernel<L><<<pb, 128, 0, st>>>(J, b, s->Ad, s->Ae, s->Rd, s->Re, n, D, negate);
+        TS_TRY(cudaMemsetAsync(s->ctl, 0, sizeof(ts::Ctl), st), MDPS_ECUDA);
+        ts::ts_pack_kernel<L><<<pb, 128, 0, st>>>(J, b, s->Ad, s->Ae, s->Rp, s->Re, n, D, negate);
         TS_TRY(cudaGetLastError(), MDPS_ECUDA);
-        TS_TRY(cudaMemsetAsync(s->bar, 0, sizeof(ts::Barrier), st), MDPS_ECUDA);
-        {
-            void *args[] = {(void *)&J, (void *)&s->Ma, (void *)&s->Mi, (void *)&s->piv, (void *)&s->status,
-                            (void *)&s->Wd, (void *)&s->We, (void *)&s->n, (void *)&s->D, (void *)&s->bar};
-            TS_TRY(cudaLaunchCooperativeKernel((const void *)ts::ts_gj_kernel<L>, dim3(s->grid_gj), dim3(ts::THREADS),
-                                               args, 0, st),
-                   MDPS_ECUDA);
-        }
-        {
-            const double *Ad = s->Ad, *Wd = s->Wd;
-            const int *Ae = s->Ae, *We = s->We;
-            void *args[] = {(void *)&Ad, (void *)&Ae, (void *)&Wd, (void *)&We, (void *)&s->Rd, (void *)&s->Re,
-                            (void *)&s->Xd, (void *)&s->Xe, (void *)&dx, (void *)&s->n, (void *)&s->D,
-                            (void *)&s->bar};
-            TS_TRY(cudaLaunchCooperativeKernel((const void *)ts::ts_loop_kernel<L>, dim3(s->grid_loop), dim3(128),
-                                               args, s->smem_loop, st),
-                   MDPS_ECUDA);
-        }
+        ts::ts_gj_kernel<L><<<1, ts::GJ_THREADS, 0, st>>>(J, s->M, s->piv, s->ctl, s->Wr, s->Wre, s->Wc, s->Wce, n,
+                                                          D);
+        TS_TRY(cudaGetLastError(), MDPS_ECUDA);
+        const double *Ad = s->Ad;
+        const int *Ae = s->Ae;
+        void *args[] = {(void *)&Ad,    (void *)&Ae,     (void *)&s->Wr, (void *)&s->Wre, (void *)&s->Wc,
+                        (void *)&s->Wce, (void *)&s->Ec, (void *)&s->Ece, (void *)&s->Rp, (void *)&s->Re,
+                        (void *)&s->Xp, (void *)&s->Xe,  (void *)&dx,    (void *)&s->n,   (void *)&s->D,
+                        (void *)&s->ctl};
+        TS_TRY(cudaLaunchCooperativeKernel((const void *)ts::ts_main_kernel<L>, dim3(s->grid_main),
+                                           dim3(ts::MAIN_THREADS), args, s->smem_main, st),
+               MDPS_ECUDA);
         return MDPS_OK;
     }
 };
@@ -704,25 +638,16 @@ static int ts_dispatch(int L, Args &&...args) {
 }
 
 static void solver_free(mdps_solver *s) {
-    cudaFree(s->Ad);
-    cudaFree(s->Ae);
-    cudaFree(s->Ma);
-    cudaFree(s->Mi);
-    cudaFree(s->Wd);
-    cudaFree(s->We);
-    cudaFree(s->Rd);
-    cudaFree(s->Re);
-    cudaFree(s->Xd);
-    cudaFree(s->Xe);
-    cudaFree(s->piv);
-    cudaFree(s->status);
-    cudaFree(s->bar);
+    void *ptrs[] = {s->Ad, s->Ae, s->M,  s->Wr, s->Wre, s->Wc, s->Wce, s->Ec,
+                    s->Ece, s->Rp, s->Re, s->Xp, s->Xe,  s->piv, s->ctl};
+    for (void *p : ptrs) cudaFree(p);
 }
 
 extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t limbs) {
     if (n < 1 || n > 256 || degree < 0 || degree > 255 ||
         !(limbs == 2 || limbs == 3 || limbs == 4 || limbs == 5 || limbs == 8 || limbs == 10)) {
-        mdps_internal_set_error("mdps_solver_create: need 1 <= n <= 256, 0 <= degree <= 255, limbs in {2,3,4,5,8,10}");
+        mdps_internal_set_error(
+            "mdps_solver_create: need 1 <= n <= 256, 0 <= degree <= 255, limbs in {2,3,4,5,8,10}");
         return nullptr;
     }
     mdps_solver *s = new (std::nothrow) mdps_solver();
@@ -735,14 +660,15 @@ extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t li
     s->L = limbs;
     s->S = digits_for(limbs);
     cudaGetDevice(&s->device);
-    const size_t nn = (size_t)n * n, D = s->D, S = s->S;
-    const size_t sz[] = {std::max<size_t>(1, nn * (D - 1) * 2 * S) * 8, std::max<size_t>(1, nn * (D - 1) * 2) * 4,
-                         nn * 2 * limbs * 8, nn * 2 * limbs * 8, nn * 2 * S * 8, nn * 2 * 4,
-                         n * 2 * S * D * 8, n * 2 * D * 4, n * 2 * S * D * 8, n * 2 * D * 4,
-                         n * sizeof(int), sizeof(int), sizeof(ts::Barrier)};
-    void **ptrs[] = {(void **)&s->Ad, (void **)&s->Ae, (void **)&s->Ma, (void **)&s->Mi, (void **)&s->Wd,
-                     (void **)&s->We, (void **)&s->Rd, (void **)&s->Re, (void **)&s->Xd, (void **)&s->Xe,
-                     (void **)&s->piv, (void **)&s->status, (void **)&s->bar};
+    const size_t nn = (size_t)n * n, D = s->D, S = s->S, VEC = 2 * S * n;
+    const size_t sz[] = {nn * D * 2 * S * 8, nn * D * 2 * 4, nn * 4 * 8,  // Ad, Ae, M ([n][2n] complex)
+                         nn * 2 * S * 8,     nn * 2 * 4,     n * VEC * 8,  // Wr, Wre, Wc
+                         nn * 2 * 4,         n * VEC * 8,    nn * 2 * 4,   // Wce, Ec, Ece
+                         D * VEC * 8,        D * 2 * n * 4,  VEC * 8,      // Rp, Re, Xp
+                         2 * (size_t)n * 4,  n * sizeof(int), sizeof(ts::Ctl)};  // Xe, piv, ctl
+    void **ptrs[] = {(void **)&s->Ad, (void **)&s->Ae,  (void **)&s->M,  (void **)&s->Wr,  (void **)&s->Wre,
+                     (void **)&s->Wc, (void **)&s->Wce, (void **)&s->Ec, (void **)&s->Ece, (void **)&s->Rp,
+                     (void **)&s->Re, (void **)&s->Xp,  (void **)&s->Xe, (void **)&s->piv, (void **)&s->ctl};
     bool ok = true;
     for (size_t i = 0; i < sizeof(sz) / sizeof(sz[0]) && ok; i++) {
         ok = cudaMalloc(ptrs[i], sz[i]) == cudaSuccess;
@@ -756,7 +682,7 @@ extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t li
         return nullptr;
     }
     cudaMemset(s->piv, 0, n * sizeof(int));
-    cudaMemset(s->status, 0, sizeof(int));
+    cudaMemset(s->ctl, 0, sizeof(ts::Ctl));
     if (ts_dispatch<TsGeom>(limbs, s) != MDPS_OK) {
         solver_free(s);
         delete s;
@@ -797,36 +723,29 @@ extern "C" int mdps_solver_status(mdps_solver *s, int32_t *pivots, int32_t *sing
     TS_TRY(cudaStreamSynchronize(s->last), MDPS_ECUDA);
     if (pivots) TS_TRY(cudaMemcpy(pivots, s->piv, s->n * sizeof(int), cudaMemcpyDeviceToHost), MDPS_ECUDA);
     if (singular) {
-        int v = 0;
-        TS_TRY(cudaMemcpy(&v, s->status, sizeof(int), cudaMemcpyDeviceToHost), MDPS_ECUDA);
-        *singular = v & 1;
+        ts::Ctl c;
+        TS_TRY(cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost), MDPS_ECUDA);
+        *singular = c.status & 1;
     }
     return MDPS_OK;
 }
 
-// complex md multiply-adds of one solve: Gauss-Jordan (row scaling + the
-// elimination of [A_0 | I]) and the substitution loop (d+1 products W r_j and
-// the n^2 d(d+1)/2 right-hand-side updates)
-static int64_t solver_cfma_gj(int64_t n) {
-    int64_t gj = 0;
-    for (int64_t k = 0; k < n; k++) gj += (2 * n - k - 1) * n;
-    return gj;
-}
-static int64_t solver_cfma_loop(int64_t n, int64_t D) { return D * n * n + n * n * D * (D - 1) / 2; }
-
+// Algorithmic work of one solve in complex md multiply-adds: the substitution
+// loop (d+1 products W r_j and n^2 d(d+1)/2 right-hand-side terms) plus one
+// Newton-Schulz step (2 n^3: I - A_0 W and W E).  FP64
+// instructions: 4 truncated S x S digit triangles per complex term.
 extern "C" int mdps_solver_stats(const mdps_solver *s, mdps_solver_info *out) {
     if (!s || !out) {
         mdps_internal_set_error("mdps_solver_stats: NULL argument");
         return MDPS_EINVAL;
     }
     std::memset(out, 0, sizeof *out);
-    const int64_t gj = solver_cfma_gj(s->n), loop = solver_cfma_loop(s->n, s->D);
-    out->complex_fma = gj + loop;
-    // EFT bins for Gauss-Jordan, digit DFMAs (4 truncated S x S triangles per
-    // complex term) for the loop
-    out->fp64_ops = gj * 4 * ops_bins_fma(s->L) + loop * 4 * (int64_t)(s->S * (s->S + 1) / 2);
+    const int64_t n = s->n, D = s->D;
+    const int64_t loop = D * n * n + n * n * D * (D - 1) / 2, refine = 2 * n * n * n;
+    out->complex_fma = loop + refine;
+    out->fp64_ops = out->complex_fma * 4 * (int64_t)(s->S * (s->S + 1) / 2);
     out->launches = 3;
-    out->grid_blocks = s->grid_loop;
+    out->grid_blocks = s->grid_main;
     out->workspace_bytes = s->bytes;
     return MDPS_OK;
 }
