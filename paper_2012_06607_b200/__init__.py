@@ -35,6 +35,7 @@ EXPORTED_SYMBOLS = (
     "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
     "mdps_fp64_peak", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
+    "mdps_solver_trace",
 )
 
 
@@ -116,6 +117,7 @@ def lib() -> ctypes.CDLL:
     L.mdps_solve.argtypes = [vp, vp, vp, vp, vp]
     L.mdps_solver_status.argtypes = [vp, P(i32), P(i32)]
     L.mdps_solver_stats.argtypes = [vp, P(SolverInfo)]
+    L.mdps_solver_trace.argtypes = [vp, P(i64), i32, P(i32)]
     L.mdps_solver_destroy.argtypes = [vp]
     L.mdps_solver_destroy.restype = None
     _lib = L
@@ -294,6 +296,16 @@ class Solver:
         sing = ctypes.c_int32(0)
         _check(lib().mdps_solver_status(self.handle, _ptr_i32(piv), ctypes.byref(sing)), "mdps_solver_status")
         return piv, bool(sing.value)
+
+    def trace(self):
+        """(barrier completion times in ns relative to the kernel start, refine steps)."""
+        buf = (ctypes.c_int64 * 1024)()
+        steps = ctypes.c_int32(0)
+        cnt = lib().mdps_solver_trace(self.handle, buf, 1024, ctypes.byref(steps))
+        if cnt < 0:
+            raise MdpsError(mdps_last_error())
+        t = list(buf[:cnt])
+        return [x - t[0] for x in t], steps.value
 
     def stats(self) -> dict:
         st = SolverInfo()

@@ -57,12 +57,23 @@ struct Ctl {              // device control block (memset to 0 before every solv
     int emax;             // max radix exponent of the entries of E = I - A_0 W (+ bias), 0 = none
     int status;           // bit 0: singular A_0
     int refine_steps;     // Newton-Schulz steps run
-    int pad[3];
+    int ntrace;           // entries of the phase trace written
+    int pad[2];
 };
+constexpr int TRACE_MAX = 1024;
+
+__device__ __forceinline__ long long global_ns() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 constexpr int EMAX_BIAS = 1 << 20;
 
-// generation barrier over all blocks of a co-resident grid
-__device__ __forceinline__ void grid_sync(Ctl *c) {
+__device__ __forceinline__ bool tid0() { return blockIdx.x == 0 && threadIdx.x == 0; }
+
+// generation barrier over all blocks of a co-resident grid; block 0 stamps
+// the completion time of every barrier into trace (diagnostics)
+__device__ __forceinline__ void grid_sync(Ctl *c, long long *trace) {
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned int *vgen = &c->gen;
@@ -76,13 +87,16 @@ __device__ __forceinline__ void grid_sync(Ctl *c) {
             while (*vgen == g) __nanosleep(100);
         }
         __threadfence();
+        if (blockIdx.x == 0 && c->ntrace < TRACE_MAX) trace[c->ntrace++] = global_ns();
     }
     __syncthreads();
 }
 
 // ---- 1. pack ---------------------------------------------------------------------
-// Ad[k][p][q] = [2][S] digits + exponents Ae[k][p][q][2] (k = 0..d);
-// R planes [k][2][S][n] + exponents [k][2][n] (negated for a Newton step).
+// Row p of A_k as a digit vector in planes: Ad[k][p][2][S][n] + exponents
+// Ae[k][p][2][n] (k = 0..d; q fastest, so that the lanes of a group reading
+// consecutive q load consecutive addresses); R planes [k][2][S][n] +
+// exponents [k][2][n] (negated for a Newton step).
 template <int L>
 __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__ J, const double *__restrict__ b,
                                                       double *__restrict__ Ad, int *__restrict__ Ae,
@@ -91,20 +105,21 @@ __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__
     constexpr int S = digits_for(L);
     const size_t nj = (size_t)n * n * D, total = nj + (size_t)n * D;
     for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (size_t)gridDim.x * blockDim.x) {
-        if (g < nj) {  // (p, q, k): k fastest for coalesced limb reads
-            const int k = (int)(g % D);
-            const size_t pq = g / D;
-            const double *src = J + pq * 2 * L * D + k;
-            double *dst = Ad + ((size_t)k * n * n + pq) * 2 * S;
-            int *de = Ae + ((size_t)k * n * n + pq) * 2;
+        if (g < nj) {  // (k, p, q): q fastest for coalesced digit-plane writes
+            const int q = (int)(g % n);
+            const size_t kp = g / n;
+            const int p = (int)(kp % n), k = (int)(kp / n);
+            const double *src = J + ((size_t)p * n + q) * 2 * L * D + k;
+            double *dst = Ad + kp * 2 * S * n + q;
+            int *de = Ae + kp * 2 * n + q;
 #pragma unroll 1
             for (int part = 0; part < 2; part++) {
                 double v[L], d[S];
 #pragma unroll
                 for (int l = 0; l < L; l++) v[l] = src[(size_t)(part * L + l) * D];
-                de[part] = limbs_to_digits<L, S>(v, d);
+                de[(size_t)part * n] = limbs_to_digits<L, S>(v, d);
 #pragma unroll
-                for (int t = 0; t < S; t++) dst[part * S + t] = d[t];
+                for (int t = 0; t < S; t++) dst[(size_t)(part * S + t) * n] = d[t];
             }
         } else {
             const size_t g2 = g - nj;
@@ -129,7 +144,7 @@ __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__
 // ---- 2. factor A_0 once: Gauss-Jordan, partial pivoting, complex double -------------
 // [A_0 | I] -> [I | W_0] on the leading limbs (one block; M in global memory,
 // L2-resident).  Pivot k = the row i >= k maximising |re| + |im| (lowest row
-// on ties).  W_0 -> digit elements (rows) and digit column planes.
+// on ties).  W_0 -> digit planes of its rows and of its columns.
 template <int L>
 __global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restrict__ J, double *__restrict__ M,
                                                            int *__restrict__ piv, Ctl *ctl, double *__restrict__ Wr,
@@ -228,11 +243,11 @@ __global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restr
 #pragma unroll
             for (int l = 0; l < L; l++) v[l] = l == 0 ? (part ? w.y : w.x) : 0.0;
             const int e = limbs_to_digits<L, S>(v, d);
-            Wre[(size_t)t * 2 + part] = e;
+            Wre[((size_t)p * 2 + part) * n + q] = e;
             Wce[((size_t)q * 2 + part) * n + p] = e;
 #pragma unroll
             for (int s = 0; s < S; s++) {
-                Wr[((size_t)t * 2 + part) * S + s] = d[s];
+                Wr[(((size_t)p * 2 + part) * S + s) * n + q] = d[s];
                 Wc[(((size_t)q * 2 + part) * S + s) * n + p] = d[s];
             }
         }
@@ -240,8 +255,8 @@ __global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restr
 }
 
 // ---- 3. exact digit dot products -------------------------------------------------------
-// sum_q a_q x_q of complex md numbers: a_q digit elements [2][S] read from
-// global memory (row p of a matrix), x_q a digit vector staged in shared
+// sum_q a_q x_q of complex md numbers: a (row p of a matrix) a digit vector
+// in planes [2][S][n] read from global memory, x a digit vector staged in shared
 // memory as planes [part][PADZ + S][n] (PADZ zero planes for the alignment
 // shift).  One real part per pass, one DFMA per digit pair.
 template <int L>
@@ -257,14 +272,14 @@ __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, con
     md_zero(A);
     int cnt = 0;
     for (int q = q0; q < n; q += G) {
-        const double *a = arow + (size_t)q * 2 * S;
+        const double *a = arow + q;
         double Ur[S], Ui[S];
 #pragma unroll
         for (int s = 0; s < S; s++) {
-            Ur[s] = a[s];
-            Ui[s] = __longlong_as_double(__double_as_longlong(a[S + s]) ^ sgn);
+            Ur[s] = a[(size_t)s * n];
+            Ui[s] = __longlong_as_double(__double_as_longlong(a[(size_t)(S + s) * n]) ^ sgn);
         }
-        const int er = aexp[2 * q], ei = aexp[2 * q + 1];
+        const int er = aexp[q], ei = aexp[n + q];
         const int x1 = xe[w1part * n + q], x2 = xe[w2part * n + q];
         int d1 = eacc - er - x1, d2 = eacc - ei - x2;
         if (er + x1 <= ZERO_E / 2) d1 = 0;  // zero product: any plane will do
@@ -321,8 +336,9 @@ __device__ __forceinline__ void ts_stage(const double *__restrict__ src, const i
     for (int part = 0; part < 2; part++) {
         double *dst = xs + ((size_t)part * P2 + PADZ) * n;
         const double *s0 = src + (size_t)part * SN;
+#pragma unroll 4
         for (int t = threadIdx.x; t < SN; t += blockDim.x) {
-            const double v = s0[t];
+            const double v = __ldcg(s0 + t);
             dst[t] = negate ? -v : v;
         }
         double *z = xs + (size_t)part * P2 * n;
@@ -359,7 +375,7 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
     int ea0 = ZERO_E, ea1 = ZERO_E;
     if (valid) {
         for (int q = lg; q < n; q += G) {
-            const int er = aexp[2 * q], ei = aexp[2 * q + 1], xr = xe[q], xi = xe[n + q];
+            const int er = aexp[q], ei = aexp[n + q], xr = xe[q], xi = xe[n + q];
             ea0 = max(ea0, max(er + xr, ei + xi));
             ea1 = max(ea1, max(er + xi, ei + xr));
         }
@@ -379,19 +395,22 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
 #pragma unroll 1
     for (int part = 0; part < 2; part++) {
         const int eacc = max(part ? ea1 : ea0, ZERO_E);
+        int eI = ZERO_E;
+        if (valid && lg == 0 && init.d) {  // fetch the init digits early (they land during the pass)
+            eI = init.e[part * init.stride];
+            const double *src = init.d + (size_t)part * S * init.stride;
+#pragma unroll
+            for (int t = 0; t < S; t++) scratch[t] = __ldcg(src + (size_t)t * init.stride);
+        }
         double A[S];
         ts_dot_pass<L>(arow, aexp, xs, xe, valid ? n : 0, lg, G, part, eacc, A);
         if (valid && lg == 0) {
-            if (init.d) {  // digit s of the init value has weight R^(eI-1-s): slot s + eacc-1-eI
-                const int eI = init.e[part * init.stride];
-                if (eI > ZERO_E / 2) {
-                    const int dI = eacc - 1 - eI;
-                    const double *src = init.d + (size_t)part * S * init.stride;
+            if (init.d && eI > ZERO_E / 2) {  // digit s of the init value has weight R^(eI-1-s): slot s + eacc-1-eI
+                const int dI = eacc - 1 - eI;
 #pragma unroll
-                    for (int t = 0; t < S; t++) {
-                        const int s = t - dI;
-                        if (s >= 0 && s < S) A[t] = __dadd_rn(A[t], src[(size_t)s * init.stride]);
-                    }
+                for (int t = 0; t < S; t++) {
+                    const int s = t - dI;
+                    if (s >= 0 && s < S) A[t] = __dadd_rn(A[t], scratch[s]);
                 }
             }
             if (one && part == 0) {  // weight R^0 = slot eacc - 2
@@ -419,11 +438,12 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
     return eout;
 }
 
-// lanes per task: the smallest power of two in [4, 32] that fills the threads
-// `avail` in one round, as long as every lane keeps >= 8 terms
+// lanes per task: the smallest power of two in [4, 32] that occupies half
+// the threads `avail` (the per-task latency is the critical path when tasks
+// are few), keeping >= 2 terms per lane
 __device__ __forceinline__ int pick_group(long long tasks, int n, long long avail) {
     int G = 4;
-    while (G < 32 && tasks * G < avail && n / (2 * G) >= 8) G <<= 1;
+    while (G < 32 && 2 * tasks * G < avail && n >= 4 * G) G <<= 1;
     return G;
 }
 
@@ -433,9 +453,10 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
     const double *__restrict__ Ad, const int *__restrict__ Ae, double *__restrict__ Wr, int *__restrict__ Wre,
     double *__restrict__ Wc, int *__restrict__ Wce, double *__restrict__ Ec, int *__restrict__ Ece,
     double *__restrict__ Rp, int *__restrict__ Re, double *__restrict__ Xp, int *__restrict__ Xe,
-    double *__restrict__ dx, int n, int D, Ctl *ctl) {
+    double *__restrict__ dx, int n, int D, Ctl *ctl, long long *trace) {
     constexpr int S = digits_for(L);
     constexpr int P2 = PADZ + S;
+    if (tid0()) trace[ctl->ntrace++] = global_ns();
     extern __shared__ __align__(16) double sm[];
     double *xs = sm;                             // [2][P2][n]
     int *xe = (int *)(xs + (size_t)2 * P2 * n);  // [2][n]
@@ -445,19 +466,26 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t VEC = (size_t)2 * S * n;        // doubles per digit vector (planes)
     double *scratch = scr + (size_t)(threadIdx.x / 4) * (S + 2);
-    // matrix products: column c per block, rows p over the block's groups
-    const int Gm = pick_group(n, n, blockDim.x);
+    // matrix products: blocks take (column c, chunk of rows); each block
+    // stages its column once
+    const int bpc = max(1, (int)gridDim.x / n);                // blocks per column
+    const int ncb = (int)gridDim.x / bpc;                      // columns in flight
+    const int rows_pb = (n + bpc - 1) / bpc;
+    const int Gm = pick_group(rows_pb, n, blockDim.x);
     const int gpb = blockDim.x / Gm, gm = threadIdx.x / Gm, lgm = threadIdx.x % Gm;
+    const int cslot = blockIdx.x / bpc, rchunk = blockIdx.x % bpc;
+    const int r0 = rchunk * rows_pb, r1 = min(n, r0 + rows_pb);
+    const bool mp_active = cslot < ncb;
 
     // a. W <- W + W (I - A_0 W): columns of E and W are digit vectors (planes)
     for (int it = 0; it < MAX_REFINE; it++) {
         if (threadIdx.x == 0) s_emax = ZERO_E;
-        for (int c = blockIdx.x; c < n; c += gridDim.x) {  // E[:, c] = e_c - A_0 W[:, c]
+        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // E[:, c] = e_c - A_0 W[:, c]
             ts_stage<L>(Wc + (size_t)c * VEC, Wce + (size_t)c * 2 * n, n, true, xs, xe);
             __syncthreads();
-            for (int base = 0; base < n; base += gpb) {
+            for (int base = r0; base < r1; base += gpb) {
                 const int p = base + gm;
-                const bool valid = p < n;
+                const bool valid = p < r1;
                 const int pp = valid ? p : 0;
                 const int e = ts_task<L>(Ad + (size_t)pp * n * 2 * S, Ae + (size_t)pp * n * 2, xs, xe, n, lgm, Gm,
                                          valid, DigRef{nullptr, nullptr, 0}, pp == c,
@@ -468,17 +496,17 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
             __syncthreads();
         }
         if (threadIdx.x == 0 && s_emax > ZERO_E / 2) atomicMax(&ctl->emax, s_emax + EMAX_BIAS);
-        grid_sync(ctl);
+        grid_sync(ctl, trace);
         // ||E|| < R^emax / 2; W += W E leaves an error ~||E||^2: stop once that
         // is below 2^-(53 L + 16)
         const int eraw = *(volatile int *)&ctl->emax;
         const bool last = eraw == 0 || 2 * (BETA * (eraw - EMAX_BIAS) - 1) < -(53 * L + 16) || it + 1 == MAX_REFINE;
-        for (int c = blockIdx.x; c < n; c += gridDim.x) {  // W[:, c] += W E[:, c]
+        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // W[:, c] += W E[:, c]
             ts_stage<L>(Ec + (size_t)c * VEC, Ece + (size_t)c * 2 * n, n, false, xs, xe);
             __syncthreads();
-            for (int base = 0; base < n; base += gpb) {
+            for (int base = r0; base < r1; base += gpb) {
                 const int p = base + gm;
-                const bool valid = p < n;
+                const bool valid = p < r1;
                 const int pp = valid ? p : 0;
                 ts_task<L>(Wr + (size_t)pp * n * 2 * S, Wre + (size_t)pp * n * 2, xs, xe, n, lgm, Gm, valid,
                            DigRef{Wc + (size_t)c * VEC + pp, Wce + (size_t)c * 2 * n + pp, n}, false,
@@ -486,22 +514,23 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
             }
             __syncthreads();
         }
-        grid_sync(ctl);
-        for (size_t t = tid; t < (size_t)n * n; t += nth) {  // rows <- columns
+        grid_sync(ctl, trace);
+        for (size_t t = tid; t < (size_t)n * n; t += nth) {  // row planes <- column planes
             const int p = (int)(t / n), c = (int)(t % n);
 #pragma unroll
             for (int part = 0; part < 2; part++) {
-                Wre[t * 2 + part] = Wce[((size_t)c * 2 + part) * n + p];
+                Wre[((size_t)p * 2 + part) * n + c] = Wce[((size_t)c * 2 + part) * n + p];
 #pragma unroll
                 for (int s = 0; s < S; s++)
-                    Wr[(t * 2 + part) * S + s] = Wc[(size_t)c * VEC + (size_t)(part * S + s) * n + p];
+                    Wr[(size_t)p * VEC + (size_t)(part * S + s) * n + c] =
+                        Wc[(size_t)c * VEC + (size_t)(part * S + s) * n + p];
             }
         }
         if (tid == 0) {
             ctl->emax = 0;
             ctl->refine_steps = it + 1;
         }
-        grid_sync(ctl);
+        grid_sync(ctl, trace);
         if (last) break;
     }
 
@@ -521,7 +550,7 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
                            dx + (size_t)pp * 2 * L * D + j, D, scratch);
             }
         }
-        grid_sync(ctl);
+        grid_sync(ctl, trace);
         if (j + 1 == D) break;
         {  // r_k -= A_{k-j} dx_j, k = j+1..d
             ts_stage<L>(Xp, Xe, n, true, xs, xe);
@@ -540,7 +569,7 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
                            DigOut{rk, rke, n}, nullptr, 0, scratch);
             }
         }
-        grid_sync(ctl);
+        grid_sync(ctl, trace);
     }
 }
 
@@ -561,6 +590,7 @@ struct mdps_solver {
     int *Ae = nullptr, *Wre = nullptr, *Wce = nullptr, *Ece = nullptr, *Re = nullptr, *Xe = nullptr;
     int *piv = nullptr;
     ts::Ctl *ctl = nullptr;
+    long long *trace = nullptr;
     int grid_main = 0;
     size_t smem_main = 0;
     size_t bytes = 0;
@@ -615,7 +645,7 @@ struct TsRun {
         void *args[] = {(void *)&Ad,    (void *)&Ae,     (void *)&s->Wr, (void *)&s->Wre, (void *)&s->Wc,
                         (void *)&s->Wce, (void *)&s->Ec, (void *)&s->Ece, (void *)&s->Rp, (void *)&s->Re,
                         (void *)&s->Xp, (void *)&s->Xe,  (void *)&dx,    (void *)&s->n,   (void *)&s->D,
-                        (void *)&s->ctl};
+                        (void *)&s->ctl, (void *)&s->trace};
         TS_TRY(cudaLaunchCooperativeKernel((const void *)ts::ts_main_kernel<L>, dim3(s->grid_main),
                                            dim3(ts::MAIN_THREADS), args, s->smem_main, st),
                MDPS_ECUDA);
@@ -639,7 +669,7 @@ static int ts_dispatch(int L, Args &&...args) {
 
 static void solver_free(mdps_solver *s) {
     void *ptrs[] = {s->Ad, s->Ae, s->M,  s->Wr, s->Wre, s->Wc, s->Wce, s->Ec,
-                    s->Ece, s->Rp, s->Re, s->Xp, s->Xe,  s->piv, s->ctl};
+                    s->Ece, s->Rp, s->Re, s->Xp, s->Xe,  s->piv, s->ctl, s->trace};
     for (void *p : ptrs) cudaFree(p);
 }
 
@@ -665,10 +695,12 @@ extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t li
                          nn * 2 * S * 8,     nn * 2 * 4,     n * VEC * 8,  // Wr, Wre, Wc
                          nn * 2 * 4,         n * VEC * 8,    nn * 2 * 4,   // Wce, Ec, Ece
                          D * VEC * 8,        D * 2 * n * 4,  VEC * 8,      // Rp, Re, Xp
-                         2 * (size_t)n * 4,  n * sizeof(int), sizeof(ts::Ctl)};  // Xe, piv, ctl
+                         2 * (size_t)n * 4,  n * sizeof(int), sizeof(ts::Ctl),  // Xe, piv, ctl
+                         ts::TRACE_MAX * sizeof(long long)};
     void **ptrs[] = {(void **)&s->Ad, (void **)&s->Ae,  (void **)&s->M,  (void **)&s->Wr,  (void **)&s->Wre,
                      (void **)&s->Wc, (void **)&s->Wce, (void **)&s->Ec, (void **)&s->Ece, (void **)&s->Rp,
-                     (void **)&s->Re, (void **)&s->Xp,  (void **)&s->Xe, (void **)&s->piv, (void **)&s->ctl};
+                     (void **)&s->Re, (void **)&s->Xp,  (void **)&s->Xe, (void **)&s->piv, (void **)&s->ctl,
+                     (void **)&s->trace};
     bool ok = true;
     for (size_t i = 0; i < sizeof(sz) / sizeof(sz[0]) && ok; i++) {
         ok = cudaMalloc(ptrs[i], sz[i]) == cudaSuccess;
@@ -755,4 +787,18 @@ extern "C" void mdps_solver_destroy(mdps_solver *s) {
     cudaDeviceSynchronize();
     solver_free(s);
     delete s;
+}
+
+extern "C" int mdps_solver_trace(mdps_solver *s, int64_t *ns, int32_t max, int32_t *refine_steps) {
+    if (!s || !ns) {
+        mdps_internal_set_error("mdps_solver_trace: NULL argument");
+        return MDPS_EINVAL;
+    }
+    TS_TRY(cudaStreamSynchronize(s->last), MDPS_ECUDA);
+    ts::Ctl c;
+    TS_TRY(cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost), MDPS_ECUDA);
+    const int cnt = std::min(c.ntrace, (int)max);
+    if (cnt > 0) TS_TRY(cudaMemcpy(ns, s->trace, cnt * sizeof(long long), cudaMemcpyDeviceToHost), MDPS_ECUDA);
+    if (refine_steps) *refine_steps = c.refine_steps;
+    return cnt;
 }

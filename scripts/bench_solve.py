@@ -40,7 +40,31 @@ def measure(name, steps=5, warmup=2):
     return out
 
 
+
+
+def trace(name):
+    t = mdinputs.toeplitz_config(name)
+    s = mdps.Solver(t.n, t.degree, t.limbs)
+    J, b = torch.from_numpy(t.jac).cuda(), torch.from_numpy(t.rhs).cuda()
+    s.solve(J, b)
+    s.solve(J, b)
+    raw = (__import__("ctypes").c_int64 * 1024)()
+    st = __import__("ctypes").c_int32(0)
+    mdps.lib().mdps_solver_trace(s.handle, raw, 1024, __import__("ctypes").byref(st))
+    dbg = list(raw[899:912])
+    print("DBG", [round((x - dbg[0]) / 1e3, 2) for x in dbg])
+    tr, steps = s.trace()
+    tr = [x for x in tr[:200] if x >= 0][:2 * t.D + 3 * 8 + 2]
+    d = [round((tr[i + 1] - tr[i]) / 1e3, 1) for i in range(len(tr) - 1)]
+    print(json.dumps({"config": name, "refine_steps": steps, "total_us": tr[-1] / 1e3,
+                      "refine_us": d[:3 * steps], "loop_phase_us": d[3 * steps:3 * steps + 40]}), flush=True)
+
+
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["dd", "qd", "od", "deca"]
+    args = sys.argv[1:]
+    do_trace = "--trace" in args
+    names = [a for a in args if not a.startswith("--")] or ["dd", "qd", "od", "deca"]
     for nm in names:
         print(json.dumps(measure(nm)), flush=True)
+        if do_trace:
+            trace(nm)
