@@ -182,6 +182,25 @@ int mdps_solver_stats(const mdps_solver *solver, mdps_solver_info *out);
 
 void mdps_solver_destroy(mdps_solver *solver);
 
+/* One step of Newton's method on power series: f and its
+ * Jacobian at x(t) (mdps_eval_diff), then J(t) dx(t) = -f(t) (the solver),
+ * then x <- x + dx (md addition per coefficient).  `sys` and `solver` must
+ * have the same n, degree and limbs.  DEVICE pointers: x [n][2][limbs][D]
+ * in/out; dx_out (NULL: solver scratch) receives dx; update_norm (NULL: not
+ * written) receives ||dx|| = max over components and coefficients of the
+ * complex modulus of dx's leading limbs (reading R14).  The solver
+ * owns the f and J workspace (allocated at the first step).  Asynchronous. */
+int mdps_newton_step(mdps_system *sys, mdps_solver *solver, double *x, double *dx_out, double *update_norm,
+                     mdps_stream_t stream);
+
+/* Newton's method: steps from x until ||dx|| <= tol or max_iters steps (the
+ * paper's stopping rule, §6: tolerance 1.0E-32 on ||dx||, at most
+ * 8, 8, 12, 16 steps for degrees 8, 16, 24, 32).  Synchronises `stream` after
+ * every step to read the norm.  Returns the number of steps taken (>= 1) or
+ * < 0 on error; *last_norm (optional) = ||dx|| of the last step. */
+int mdps_newton(mdps_system *sys, mdps_solver *solver, double *x, int32_t max_iters, double tol,
+                double *last_norm, mdps_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,6 +10,7 @@ builds it and marshals numpy arrays.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 import os
 import subprocess
 from typing import Optional, Sequence, Tuple
@@ -239,3 +240,19 @@ def toeplitz_solve(jac, rhs, nthreads: Optional[int] = None, limbs: Optional[int
         raise SingularError("A_0 is singular (zero pivot column)")
     _check(rc, "toeplitz_solve")
     return dx, piv
+
+
+# ---- Newton's method on power series ----------------------------------------------
+def newton(si, steps: int, nthreads: Optional[int] = None):
+    """`steps` Newton steps from si.x: at x_k, f and J by the
+    plain definition (eval_diff), dx from J(t) dx(t) = -f(t) by forward
+    substitution (toeplitz_solve), x_{k+1} = x_k + dx (series_add).
+    Returns (x, update norms max_{q,k} |dx_{q,k}| of the leading limbs)."""
+    x = _f64(si.x).copy()
+    norms = []
+    for _ in range(steps):
+        vals, jac, _ = eval_diff(dataclasses.replace(si, x=x), nthreads)
+        dx, _ = toeplitz_solve(jac, -vals, nthreads)
+        x = series_add(x, dx)
+        norms.append(float(np.max(np.hypot(dx[:, 0, 0, :], dx[:, 1, 0, :]))))
+    return x, norms

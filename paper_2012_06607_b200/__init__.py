@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
     "mdps_fp64_peak", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
-    "mdps_solver_trace",
+    "mdps_solver_trace", "mdps_newton_step", "mdps_newton",
 )
 
 
@@ -118,6 +118,8 @@ def lib() -> ctypes.CDLL:
     L.mdps_solver_status.argtypes = [vp, P(i32), P(i32)]
     L.mdps_solver_stats.argtypes = [vp, P(SolverInfo)]
     L.mdps_solver_trace.argtypes = [vp, P(i64), i32, P(i32)]
+    L.mdps_newton_step.argtypes = [vp, vp, vp, vp, vp, vp]
+    L.mdps_newton.argtypes = [vp, vp, vp, i32, ctypes.c_double, P(ctypes.c_double), vp]
     L.mdps_solver_destroy.argtypes = [vp]
     L.mdps_solver_destroy.restype = None
     _lib = L
@@ -289,6 +291,22 @@ class Solver:
         _check(lib().mdps_solve(self.handle, _dptr(jacobian), _dptr(rhs), _dptr(dx_out), _stream_handle(stream)),
                "mdps_solve")
         return dx_out
+
+    def newton_step(self, system: "System", x, dx_out=None, norm_out=None, stream=None):
+        """x <- x + dx with J dx = -f at x (asynchronous; device tensors)."""
+        _check(lib().mdps_newton_step(system.handle, self.handle, _dptr(x),
+                                      _dptr(dx_out) if dx_out is not None else None,
+                                      _dptr(norm_out) if norm_out is not None else None, _stream_handle(stream)),
+               "mdps_newton_step")
+
+    def newton(self, system: "System", x, max_iters: int, tol: float, stream=None):
+        """Newton's method in place on x; returns (steps, last update norm)."""
+        norm = ctypes.c_double(0.0)
+        rc = lib().mdps_newton(system.handle, self.handle, _dptr(x), int(max_iters), float(tol), ctypes.byref(norm),
+                               _stream_handle(stream))
+        if rc < 0:
+            raise MdpsError(f"mdps_newton failed (rc={rc}): {mdps_last_error()}")
+        return rc, norm.value
 
     def status(self):
         """(pivots [n] int32, singular bool) of the last solve (synchronises)."""

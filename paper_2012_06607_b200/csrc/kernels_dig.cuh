@@ -101,16 +101,18 @@ __device__ __forceinline__ void carry_normalize(double (&A)[N]) {
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return a >= 0 ? (a + b - 1) / b : -((-a) / b); }
 
-// one real md number (L limbs, any overlap) -> S balanced digits + exponent
+// 2^k as a double for k in [-1022, 1023]
+__device__ __forceinline__ double pow2i(int k) { return __longlong_as_double((long long)(1023 + k) << 52); }
+
+// one real md number (L limbs, any overlap) -> S balanced digits + exponent.
+// The limbs are first scaled EXACTLY by 2^(-BETA (e-1)) (two power-of-two
+// factors, each in range), so the digit grid is fixed — R^0 .. R^-(S-1) —
+// whatever the magnitude: no weight under- or overflows for tiny values.
 template <int L, int S>
 __device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d)[S]) {
-    double v[L];
     double m = 0.0;
 #pragma unroll
-    for (int p = 0; p < L; p++) {
-        v[p] = v0[p];
-        m = __dadd_ru(m, fabs(v0[p]));
-    }
+    for (int p = 0; p < L; p++) m = __dadd_ru(m, fabs(v0[p]));
     if (!(m > 0.0)) {  // zero (or NaN: also mapped to the zero encoding's exponent)
 #pragma unroll
         for (int j = 0; j < S; j++) d[j] = (m == 0.0) ? 0.0 : m;
@@ -118,10 +120,14 @@ __device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d
     }
     const int emin = ilogb(m) + 1;          // |v| <= m < 2^emin
     const int e = ceil_div(emin + 1, BETA);  // |v| < R^e / 2: a balanced top digit
+    const int sh = -BETA * (e - 1), s1 = sh / 2, s2 = sh - s1;
+    const double f1 = pow2i(s1), f2 = pow2i(s2);
+    double v[L];
+#pragma unroll
+    for (int p = 0; p < L; p++) v[p] = __dmul_rn(__dmul_rn(v0[p], f1), f2);  // |v| < R / 2
 #pragma unroll
     for (int j = 0; j < S; j++) {
-        const double G = radix_pow(e - 1 - j);
-        const double C = __dmul_rn(MAGIC, G);
+        const double C = MAGIC * pow2i(-BETA * j);  // rounds to multiples of R^-j
         double acc = 0.0;
 #pragma unroll
         for (int p = 0; p < L; p++) {
@@ -129,7 +135,7 @@ __device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d
             v[p] = __dsub_rn(v[p], q);
             acc = __dadd_rn(acc, q);
         }
-        d[j] = __dmul_rn(acc, radix_pow(1 + j - e));
+        d[j] = __dmul_rn(acc, pow2i(BETA * j));
     }
     carry_normalize(d);
     return e;

@@ -538,6 +538,15 @@ static int64_t conv_ops_per_product(int algo, int L, int D) {
     return terms * 2 * S * (S + 1);  // one DFMA per digit pair, 2 real products per part
 }
 
+// shape of a system for solve.cu (the Newton step checks it against the solver)
+int mdps_internal_system_shape(const mdps_system *s, int *n, int *D, int *L) {
+    if (!s) return MDPS_EINVAL;
+    *n = s->n;
+    *D = s->D;
+    *L = s->L;
+    return MDPS_OK;
+}
+
 extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     if (!s || !out) {
         set_err("NULL argument");

@@ -43,6 +43,7 @@
 #include "conv_dig.cuh"
 
 void mdps_internal_set_error(const std::string &s);  // libmdps.cu
+int mdps_internal_system_shape(const mdps_system *s, int *n, int *D, int *L);
 
 namespace mdps {
 namespace ts {
@@ -578,6 +579,46 @@ __host__ __device__ inline size_t ts_main_smem(int S, int n, int threads) {
            (size_t)(threads / 4) * (S + 2) * sizeof(double);
 }
 
+// ---- Newton update: x <- x + dx and ||dx|| ------------------------------------------
+// One thread per (component, coefficient); md addition in EFT level bins;
+// the update norm max_{q,k} |dx_{q,k}| (complex modulus of the leading
+// limbs) is reduced per block and combined with an atomic max on the bit
+// pattern (non-negative doubles order like their 64-bit patterns).
+template <int L>
+__global__ void __launch_bounds__(128) ts_update_kernel(double *__restrict__ x, const double *__restrict__ dx, int n,
+                                                        int D, unsigned long long *__restrict__ norm_bits) {
+    __shared__ double s_max[4];
+    double m = 0.0;
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g < n * D) {
+        const int q = g / D, k = g - q * D;
+        double v[2];
+#pragma unroll
+        for (int part = 0; part < 2; part++) {
+            double a[L], b[L], c[L];
+            double *xp = x + ((size_t)q * 2 + part) * L * D + k;
+            const double *dp = dx + ((size_t)q * 2 + part) * L * D + k;
+#pragma unroll
+            for (int l = 0; l < L; l++) {
+                a[l] = xp[(size_t)l * D];
+                b[l] = dp[(size_t)l * D];
+            }
+            v[part] = b[0];
+            md_add<L>(a, b, c);
+#pragma unroll
+            for (int l = 0; l < L; l++) xp[(size_t)l * D] = c[l];
+        }
+        m = hypot(v[0], v[1]);
+    }
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = fmax(m, s_max[w]);
+        if (m > 0.0) atomicMax(norm_bits, (unsigned long long)__double_as_longlong(m));
+    }
+}
+
 }  // namespace ts
 }  // namespace mdps
 
@@ -591,6 +632,8 @@ struct mdps_solver {
     int *piv = nullptr;
     ts::Ctl *ctl = nullptr;
     long long *trace = nullptr;
+    double *nv = nullptr, *nj = nullptr, *ndx = nullptr;  // Newton workspace (lazy): f, J, dx
+    unsigned long long *nnorm = nullptr;
     int grid_main = 0;
     size_t smem_main = 0;
     size_t bytes = 0;
@@ -668,6 +711,10 @@ static int ts_dispatch(int L, Args &&...args) {
 }
 
 static void solver_free(mdps_solver *s) {
+    cudaFree(s->nv);
+    cudaFree(s->nj);
+    cudaFree(s->ndx);
+    cudaFree(s->nnorm);
     void *ptrs[] = {s->Ad, s->Ae, s->M,  s->Wr, s->Wre, s->Wc, s->Wce, s->Ec,
                     s->Ece, s->Rp, s->Re, s->Xp, s->Xe,  s->piv, s->ctl, s->trace};
     for (void *p : ptrs) cudaFree(p);
@@ -801,4 +848,76 @@ extern "C" int mdps_solver_trace(mdps_solver *s, int64_t *ns, int32_t max, int32
     if (cnt > 0) TS_TRY(cudaMemcpy(ns, s->trace, cnt * sizeof(long long), cudaMemcpyDeviceToHost), MDPS_ECUDA);
     if (refine_steps) *refine_steps = c.refine_steps;
     return cnt;
+}
+
+// ---- Newton's method on power series (§6 stopping rule) ----------
+template <int L>
+struct TsUpdate {
+    static int run(double *x, const double *dx, int n, int D, unsigned long long *norm, cudaStream_t st) {
+        const int blocks = (n * D + 127) / 128;
+        ts::ts_update_kernel<L><<<blocks, 128, 0, st>>>(x, dx, n, D, norm);
+        TS_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+extern "C" int mdps_newton_step(mdps_system *sys, mdps_solver *s, double *x, double *dx_out, double *update_norm,
+                                mdps_stream_t stream) {
+    if (!sys || !s || !x) {
+        mdps_internal_set_error("mdps_newton_step: NULL argument");
+        return MDPS_EINVAL;
+    }
+    int sn = 0, sD = 0, sL = 0;
+    mdps_internal_system_shape(sys, &sn, &sD, &sL);
+    if (sn != s->n || sD != s->D || sL != s->L) {
+        mdps_internal_set_error("mdps_newton_step: system and solver differ in n, degree or limbs");
+        return MDPS_EINVAL;
+    }
+    const size_t ser = (size_t)2 * s->L * s->D;
+    if (!s->nv) {
+        if (cudaMalloc(&s->nv, (size_t)s->n * ser * 8) != cudaSuccess ||
+            cudaMalloc(&s->nj, (size_t)s->n * s->n * ser * 8) != cudaSuccess ||
+            cudaMalloc(&s->ndx, (size_t)s->n * ser * 8) != cudaSuccess ||
+            cudaMalloc(&s->nnorm, sizeof(unsigned long long)) != cudaSuccess) {
+            cudaGetLastError();
+            mdps_internal_set_error("mdps_newton_step: device allocation failed");
+            return MDPS_ENOMEM;
+        }
+        s->bytes += (size_t)(2 * s->n + s->n * s->n) * ser * 8 + 8;
+    }
+    cudaStream_t cs = (cudaStream_t)stream;
+    int rc = mdps_eval_diff(sys, x, s->nv, s->nj, stream);
+    if (rc != MDPS_OK) return rc;
+    double *dx = dx_out ? dx_out : s->ndx;
+    rc = mdps_solve_internal(s, s->nj, s->nv, dx, /*negate=*/1, cs);  // J dx = -f
+    if (rc != MDPS_OK) return rc;
+    TS_TRY(cudaMemsetAsync(s->nnorm, 0, sizeof(unsigned long long), cs), MDPS_ECUDA);
+    rc = ts_dispatch<TsUpdate>(s->L, x, (const double *)dx, s->n, s->D, s->nnorm, cs);
+    if (rc != MDPS_OK) return rc;
+    if (update_norm) TS_TRY(cudaMemcpyAsync(update_norm, s->nnorm, sizeof(double), cudaMemcpyDeviceToDevice, cs),
+                            MDPS_ECUDA);
+    return MDPS_OK;
+}
+
+extern "C" int mdps_newton(mdps_system *sys, mdps_solver *s, double *x, int32_t max_iters, double tol,
+                           double *last_norm, mdps_stream_t stream) {
+    if (max_iters < 1 || !(tol >= 0.0)) {
+        mdps_internal_set_error("mdps_newton: need max_iters >= 1 and tol >= 0");
+        return MDPS_EINVAL;
+    }
+    double norm = 0.0;
+    int it = 0;
+    while (it < max_iters) {
+        const int rc = mdps_newton_step(sys, s, x, nullptr, nullptr, stream);
+        if (rc != MDPS_OK) return rc;
+        it++;
+        unsigned long long bits = 0;
+        TS_TRY(cudaMemcpyAsync(&bits, s->nnorm, sizeof bits, cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+               MDPS_ECUDA);
+        TS_TRY(cudaStreamSynchronize((cudaStream_t)stream), MDPS_ECUDA);
+        std::memcpy(&norm, &bits, sizeof norm);
+        if (norm <= tol) break;
+    }
+    if (last_norm) *last_norm = norm;
+    return it;
 }

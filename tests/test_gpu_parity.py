@@ -72,6 +72,22 @@ def test_digits_roundtrip(mdps, L):
     assert err.max() <= 4 * 2.0 ** (-53 * L)
 
 
+@pytest.mark.parametrize("L", LEVELS)
+@pytest.mark.parametrize("scale_exp", [-500, -160 * 3, -300, 300, 900])
+def test_digits_roundtrip_extreme_magnitudes(mdps, L, scale_exp):
+    """Tiny and huge md numbers (late Newton updates reach 2^-530 at L = 10):
+    the digit split scales exactly, so no digit weight under/overflows; the
+    round trip keeps every limb that is a normal double."""
+    si = mdinputs.random_system(8, 4, 2, (1, 2), (1,), 9, L)
+    x = si.x * 2.0 ** scale_exp            # exact power-of-two scaling
+    y = mdps.test_digits_roundtrip(cuda(x)).cpu().numpy()
+    assert np.isfinite(y).all()
+    err = float(np.max(np.abs(y[:, :, 0] - x[:, :, 0]) / np.maximum(np.abs(x[:, :, 0]), 1e-300)))
+    assert err <= 2.0 ** -52
+    if scale_exp - 53 * L - 30 > -1074:   # the md precision floor is above the subnormals
+        assert (oracle.series_err(y * 2.0 ** -scale_exp, si.x) <= 4 * 2.0 ** (-53 * L)).all()
+
+
 @pytest.mark.parametrize("algo", ALGOS)
 @pytest.mark.parametrize("L", LEVELS)
 def test_series_product_grid(mdps, algo, L):
