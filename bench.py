@@ -157,6 +157,56 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+def bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal, dist, args):
+    """mdps_solve on the eval's own (J, -f) and mdps_newton_step from x."""
+    steps = max(3, min(args.steps, 5))
+
+    def timed(fn, prep=None):
+        for _ in range(2):
+            if prep:
+                prep()
+            fn()
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(steps):
+            if prep:
+                prep()
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        t = sum(ms) / len(ms)
+        if dist:
+            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    with mdps.Solver(si.n, si.degree, si.limbs) as sol:
+        sys_.eval_diff(x, vals, jac)
+        rhs = -vals
+        dx = torch.empty_like(vals)
+        t_solve = timed(lambda: sol.solve(jac, rhs, dx))
+        info = sol.stats()
+        xw = torch.empty_like(x)
+        t_newton = timed(lambda: sol.newton_step(sys_, xw), prep=lambda: xw.copy_(x))
+        _, refine = sol.trace()
+    achieved = info["fp64_ops"] / (t_solve * 1e-3)
+    return {
+        "toeplitz_solve": {
+            "ms": t_solve, "complex_md_fma": info["complex_fma"], "fp64_instr": info["fp64_ops"],
+            "refine_steps": refine,
+            "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_nominal / 1e12,
+                         "unit": "T FP64 instr/s", "frac": achieved / peak_nominal},
+            "input": "the eval's own Jacobian and -f (one Newton step's linear system)"},
+        "newton_step": {"ms": t_newton, "of_which_eval_ms": None,
+                        "api": "mdps_newton_step (eval/diff + solve + update)"},
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -167,6 +217,7 @@ def main():
     ap.add_argument("--algo", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-next", action="store_true", help="skip the solver / Newton-step measurements")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "mdps" else args.warmup
 
@@ -293,6 +344,14 @@ def main():
         if not (torch.equal(hv, vals.cpu()) and torch.equal(hj, jac.cpu())):
             raise RuntimeError("e2e outputs differ from the device-path outputs")
 
+    # the next rows of the hot path: the block Toeplitz solve of
+    # this system's own Jacobian and f (J dx = -f), and whole Newton steps
+    # (eval/diff + solve + update), device-timed like the eval
+    nxt = None
+    if not args.no_next:
+        nxt = bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal, dist, args)
+        nxt["newton_step"]["of_which_eval_ms"] = ms / args.steps
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(si)
@@ -320,6 +379,7 @@ def main():
             "kernel_ms_per_step": {"conv": tim["conv_ms"] / args.steps, "accum": tim["accum_ms"] / args.steps,
                                    "convert": tim["convert_ms"] / args.steps},
             "clocks": clocks,
+            "next_rows": nxt,
         }
         print(json.dumps(line), flush=True)
     sys_.close()
