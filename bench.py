@@ -157,6 +157,22 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+def max_over_ranks(value: float, dist=None, device="cpu") -> float:
+    """The max of a per-rank time over all ranks (identity without a process group)."""
+    if not dist:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_rate(units_per_step: float, world: int, steps: int, ms: float) -> float:
+    """Units per second of the whole job: every rank processes units_per_step
+    per step (replicas, weak scaling); ms = the max over ranks."""
+    return units_per_step * world * steps / (ms * 1e-3)
+
+
 def bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal, dist, args):
     """mdps_solve on the eval's own (J, -f) and mdps_newton_step from x."""
     steps = max(3, min(args.steps, 5))
@@ -178,12 +194,7 @@ def bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal,
             e1.record(stream)
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
-        t = sum(ms) / len(ms)
-        if dist:
-            tt = torch.tensor([t], dtype=torch.float64, device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t = float(tt.item())
-        return t
+        return max_over_ranks(sum(ms) / len(ms), dist, "cuda")
 
     with mdps.Solver(si.n, si.degree, si.limbs) as sol:
         sys_.eval_diff(x, vals, jac)
@@ -278,14 +289,10 @@ def main():
     clocks = sampler.stop()
     sys_.set_timing(False)
     tim = sys_.timing(reset=True)
-    ms = sum(a.elapsed_time(b) for a, b in ev)
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), dist, "cuda")
     products_per_step = st["products"]
-    value = products_per_step * world * args.steps / (ms * 1e-3)
-    fp64_per_s = st["fp64_ops_total"] * world * args.steps / (ms * 1e-3)
+    value = whole_job_rate(products_per_step, world, args.steps, ms)
+    fp64_per_s = whole_job_rate(st["fp64_ops_total"], world, args.steps, ms)
 
     # dominant kernel: the product jobs (all levels), live CUDA-event durations
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
@@ -332,12 +339,8 @@ def main():
                 raise RuntimeError(mdps.mdps_last_error())
         e1.record(stream)
         torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if dist:
-            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
-        e2e = {"value": products_per_step * world * e2e_steps / (ems * 1e-3), "unit": "products/s",
+        ems = max_over_ranks(e0.elapsed_time(e1), dist, "cuda")
+        e2e = {"value": whole_job_rate(products_per_step, world, e2e_steps, ems), "unit": "products/s",
                "h2d_bytes_per_step": int(hx.numel() * 8), "d2h_bytes_per_step": int((hv.numel() + hj.numel()) * 8),
                "steps": e2e_steps, "ms_per_step": ems / e2e_steps, "api": "mdps_eval_diff_host (pinned host buffers)"}
         # the host-buffer outputs must equal the device path's outputs
