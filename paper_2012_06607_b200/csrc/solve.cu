@@ -439,12 +439,14 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
     return eout;
 }
 
-// lanes per task: the smallest power of two in [4, 32] that occupies half
-// the threads `avail` (the per-task latency is the critical path when tasks
-// are few), keeping >= 2 terms per lane
+// lanes per task: as many as keep >= 4 terms per lane (G <= 32): the lanes of
+// a group read consecutive q of one row, so wide groups make every digit-plane
+// load one contiguous run (the loads, not the DFMAs, bound narrow groups)
 __device__ __forceinline__ int pick_group(long long tasks, int n, long long avail) {
+    (void)tasks;
+    (void)avail;
     int G = 4;
-    while (G < 32 && 2 * tasks * G < avail && n >= 4 * G) G <<= 1;
+    while (G < 32 && n >= 8 * G) G <<= 1;
     return G;
 }
 
