@@ -218,6 +218,7 @@ struct mdps_system {
     // CUDA graph cache
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
+    cudaStream_t cap_stream = nullptr;  // capture stream of the graph
     const void *g_in = nullptr, *g_vals = nullptr, *g_jac = nullptr;
     cudaStream_t g_stream = nullptr;
     // measurement: event pairs per launch group (kind 0 conv, 1 accum, 2 convert)
@@ -258,6 +259,7 @@ static void free_system(mdps_system *s) {
     drop_marks(s);
     if (s->gexec) cudaGraphExecDestroy(s->gexec);
     if (s->graph) cudaGraphDestroy(s->graph);
+    if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
     cudaFree(s->pool);
     cudaFree(s->epool);
     cudaFree(s->jobs);
@@ -488,13 +490,17 @@ extern "C" int mdps_eval_diff(mdps_system *s, const double *in, double *vals, do
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (!s->use_graph || s->timing) return enqueue(s, in, vals, jac, st);
-    if (!s->gexec || s->g_in != in || s->g_vals != vals || s->g_jac != jac || s->g_stream != st) {
+    if (!s->gexec || s->g_in != in || s->g_vals != vals || s->g_jac != jac) {
         if (s->gexec) { cudaGraphExecDestroy(s->gexec); s->gexec = nullptr; }
         if (s->graph) { cudaGraphDestroy(s->graph); s->graph = nullptr; }
-        CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), MDPS_ECUDA);
-        const int rc = enqueue(s, in, vals, jac, st);
+        // capture on the system's own stream (the caller's may be the legacy
+        // default stream, which cannot be captured); the graph then launches
+        // on the caller's stream
+        if (!s->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking), MDPS_ECUDA);
+        CUDA_TRY(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeThreadLocal), MDPS_ECUDA);
+        const int rc = enqueue(s, in, vals, jac, s->cap_stream);
         cudaGraph_t g = nullptr;
-        const cudaError_t ce = cudaStreamEndCapture(st, &g);
+        const cudaError_t ce = cudaStreamEndCapture(s->cap_stream, &g);
         if (rc != MDPS_OK) { if (g) cudaGraphDestroy(g); return rc; }
         if (ce != cudaSuccess) { set_err(std::string("graph capture: ") + cudaGetErrorString(ce)); return MDPS_ECUDA; }
         s->graph = g;
