@@ -206,13 +206,32 @@ def bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal,
         t_newton = timed(lambda: sol.newton_step(sys_, xw), prep=lambda: xw.copy_(x))
         _, refine = sol.trace()
     achieved = info["fp64_ops"] / (t_solve * 1e-3)
+    # the oracle's forward substitution on a bounded sample of the same solve:
+    # the first coefficients (dx_0..dx_dc depend only on A_0..A_dc, b_0..b_dc)
+    cpu = None
+    if not args.no_cpu_baseline and (not dist or dist.get_rank() == 0):
+        import oracle
+        J, b = jac.cpu().numpy(), rhs.cpu().numpy()
+        dc = {2: 15, 3: 12, 4: 10, 5: 8, 8: 5, 10: 3}[si.limbs]
+        dc = min(dc, si.degree)
+        cores = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        oracle.toeplitz_solve(np.ascontiguousarray(J[..., :dc + 1]), np.ascontiguousarray(b[..., :dc + 1]),
+                              nthreads=cores)
+        dt = time.perf_counter() - t0
+        n, D = si.n, dc + 1
+        cfma = D * n * n + n * n * D * (D - 1) // 2 + n ** 3
+        cpu = {"value": cfma / dt, "unit": "complex md multiply-adds/s", "cores": min(cores, n), "kind": "oracle",
+               "sample": f"the same solve truncated at degree {dc} (n={n}), {dt:.1f} s"}
     return {
         "toeplitz_solve": {
             "ms": t_solve, "complex_md_fma": info["complex_fma"], "fp64_instr": info["fp64_ops"],
             "refine_steps": refine,
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": peak_nominal / 1e12,
                          "unit": "T FP64 instr/s", "frac": achieved / peak_nominal},
-            "input": "the eval's own Jacobian and -f (one Newton step's linear system)"},
+            "input": "the eval's own Jacobian and -f (one Newton step's linear system)",
+            "value": info["complex_fma"] / (t_solve * 1e-3), "unit": "complex md multiply-adds/s",
+            "cpu_baseline": cpu},
         "newton_step": {"ms": t_newton, "of_which_eval_ms": None,
                         "api": "mdps_newton_step (eval/diff + solve + update)"},
     }

@@ -49,7 +49,9 @@ namespace mdps {
 namespace ts {
 
 constexpr int GJ_THREADS = 1024;
-constexpr int MAIN_THREADS = 128;
+// persistent solver kernel: 128-thread blocks, 3 per SM (L <= 8); 256-thread
+// blocks, 1 per SM at L = 10 (255 registers, two staged vectors of 61 KB)
+__host__ __device__ constexpr int main_threads(int L) { return L == 10 ? 256 : 128; }
 constexpr int MAX_REFINE = 8;
 
 struct Ctl {              // device control block (memset to 0 before every solve)
@@ -263,14 +265,15 @@ __global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restr
 template <int L>
 __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, const int *__restrict__ aexp,
                                             const double *__restrict__ xs, const int *__restrict__ xe, int n,
-                                            int q0, int G, int part, int eacc, double (&A)[digits_for(L)]) {
+                                            int q0, int G, int part, int eacc, double (&A)[digits_for(L)],
+                                            bool zero = true) {
     constexpr int S = digits_for(L);
     constexpr int NORM = norm_every(S);
     constexpr int P2 = PADZ + S;
     // part 0 (re): ar xr - ai xi ; part 1 (im): ar xi + ai xr
     const int w1part = part, w2part = 1 - part;
     const long long sgn = part == 0 ? (long long)0x8000000000000000ULL : 0LL;
-    md_zero(A);
+    if (zero) md_zero(A);
     int cnt = 0;
     for (int q = q0; q < n; q += G) {
         const double *a = arow + q;
@@ -367,11 +370,20 @@ struct DigOut {
 // as digits (out) and optionally as L limbs at zl[(part*L + l)*lstride].
 // Returns the larger output part exponent.  All lanes of the warp call it
 // (shuffles); `valid` masks the work and the output.
+// A dot-product segment: row `a` (digit planes [2][S][n], exponents [2][n])
+// times the staged vector (xs, xe).
+struct Seg {
+    const double *a;
+    const int *ae;
+    const double *xs;
+    const int *xe;
+};
+
 template <int L>
 __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const int *__restrict__ aexp,
                                        const double *xs, const int *xe, int n, int lg, int G, bool valid,
                                        DigRef init, bool one, DigOut out, double *zl, int lstride,
-                                       double *scratch) {
+                                       double *scratch, Seg seg2 = Seg{nullptr, nullptr, nullptr, nullptr}) {
     constexpr int S = digits_for(L);
     int ea0 = ZERO_E, ea1 = ZERO_E;
     if (valid) {
@@ -380,6 +392,12 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
             ea0 = max(ea0, max(er + xr, ei + xi));
             ea1 = max(ea1, max(er + xi, ei + xr));
         }
+        if (seg2.a)
+            for (int q = lg; q < n; q += G) {
+                const int er = seg2.ae[q], ei = seg2.ae[n + q], xr = seg2.xe[q], xi = seg2.xe[n + q];
+                ea0 = max(ea0, max(er + xr, ei + xi));
+                ea1 = max(ea1, max(er + xi, ei + xr));
+            }
         if (lg == 0) {
             if (init.d) {
                 ea0 = max(ea0, init.e[0] + 1);
@@ -405,6 +423,7 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
         }
         double A[S];
         ts_dot_pass<L>(arow, aexp, xs, xe, valid ? n : 0, lg, G, part, eacc, A);
+        if (seg2.a) ts_dot_pass<L>(seg2.a, seg2.ae, seg2.xs, seg2.xe, valid ? n : 0, lg, G, part, eacc, A, false);
         if (valid && lg == 0) {
             if (init.d && eI > ZERO_E / 2) {  // digit s of the init value has weight R^(eI-1-s): slot s + eacc-1-eI
                 const int dI = eacc - 1 - eI;
@@ -452,18 +471,21 @@ __device__ __forceinline__ int pick_group(long long tasks, int n, long long avai
 
 // Newton-Schulz refinement of W, then the substitution loop.
 template <int L>
-__global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
+__global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kernel(
     const double *__restrict__ Ad, const int *__restrict__ Ae, double *__restrict__ Wr, int *__restrict__ Wre,
     double *__restrict__ Wc, int *__restrict__ Wce, double *__restrict__ Ec, int *__restrict__ Ece,
-    double *__restrict__ Rp, int *__restrict__ Re, double *__restrict__ Xp, int *__restrict__ Xe,
-    double *__restrict__ dx, int n, int D, Ctl *ctl, long long *trace) {
+    double *__restrict__ Mr, int *__restrict__ Mre, double *__restrict__ Rp, int *__restrict__ Re,
+    double *__restrict__ Xp, int *__restrict__ Xe, double *__restrict__ dx, int n, int D, Ctl *ctl,
+    long long *trace) {
     constexpr int S = digits_for(L);
     constexpr int P2 = PADZ + S;
     if (tid0()) trace[ctl->ntrace++] = global_ns();
     extern __shared__ __align__(16) double sm[];
-    double *xs = sm;                             // [2][P2][n]
-    int *xe = (int *)(xs + (size_t)2 * P2 * n);  // [2][n]
-    double *scr = (double *)(xe + 2 * n + 2);    // [blockDim/4][S+2] emit scratch (one per group leader)
+    double *xs = sm;                              // [2][P2][n]  staged vector 0
+    double *xs1 = sm + (size_t)2 * P2 * n;        // [2][P2][n]  staged vector 1
+    int *xe = (int *)(xs1 + (size_t)2 * P2 * n);  // [2][n]
+    int *xe1 = xe + 2 * n;                        // [2][n]
+    double *scr = (double *)(xe1 + 2 * n + 2);    // [blockDim/4][S+2] emit scratch (one per group leader)
     __shared__ int s_emax;
     const int nth = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -537,39 +559,101 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
         if (last) break;
     }
 
-    // b. the substitution loop
-    for (int j = 0; j < D; j++) {
-        {  // dx_j = W r_j
-            ts_stage<L>(Rp + (size_t)j * VEC, Re + (size_t)j * 2 * n, n, false, xs, xe);
+    // b. M = -W A_1 W (row planes in Mr): with it two coefficients per step,
+    //      dx_j     = W r_j
+    //      dx_{j+1} = W r'_{j+1} + M r_j,   r'_{j+1} = r_{j+1} before A_1 dx_j
+    //    (r_{j+1} = r'_{j+1} - A_1 dx_j and dx_j = W r_j): half the dependent steps.
+    if (D >= 2) {
+        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // P[:, c] = A_1 W[:, c]  (into Ec)
+            ts_stage<L>(Wc + (size_t)c * VEC, Wce + (size_t)c * 2 * n, n, false, xs, xe);
             __syncthreads();
-            const int G = pick_group(n, n, nth);
-            const int ng = nth / G, g = tid / G, lg = tid % G;
-            for (int base = 0; base < n; base += ng) {
-                const int p = base + g;
-                const bool valid = p < n;
+            for (int base = r0; base < r1; base += gpb) {
+                const int p = base + gm;
+                const bool valid = p < r1;
                 const int pp = valid ? p : 0;
-                ts_task<L>(Wr + (size_t)pp * n * 2 * S, Wre + (size_t)pp * n * 2, xs, xe, n, lg, G, valid,
-                           DigRef{nullptr, nullptr, 0}, false, DigOut{Xp + pp, Xe + pp, n},
-                           dx + (size_t)pp * 2 * L * D + j, D, scratch);
+                const size_t row = ((size_t)n + pp) * n;  // row p of A_1
+                ts_task<L>(Ad + row * 2 * S, Ae + row * 2, xs, xe, n, lgm, Gm, valid, DigRef{nullptr, nullptr, 0},
+                           false, DigOut{Ec + (size_t)c * VEC + pp, Ece + (size_t)c * 2 * n + pp, n}, nullptr, 0,
+                           scratch);
+            }
+            __syncthreads();
+        }
+        grid_sync(ctl, trace);
+        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // M[:, c] = -W P[:, c]  (columns into Wc)
+            ts_stage<L>(Ec + (size_t)c * VEC, Ece + (size_t)c * 2 * n, n, true, xs, xe);
+            __syncthreads();
+            for (int base = r0; base < r1; base += gpb) {
+                const int p = base + gm;
+                const bool valid = p < r1;
+                const int pp = valid ? p : 0;
+                ts_task<L>(Wr + (size_t)pp * n * 2 * S, Wre + (size_t)pp * n * 2, xs, xe, n, lgm, Gm, valid,
+                           DigRef{nullptr, nullptr, 0}, false,
+                           DigOut{Wc + (size_t)c * VEC + pp, Wce + (size_t)c * 2 * n + pp, n}, nullptr, 0, scratch);
+            }
+            __syncthreads();
+        }
+        grid_sync(ctl, trace);
+        for (size_t t = tid; t < (size_t)n * n; t += nth) {  // Mr (row planes) <- columns
+            const int p = (int)(t / n), c = (int)(t % n);
+#pragma unroll
+            for (int part = 0; part < 2; part++) {
+                Mre[((size_t)p * 2 + part) * n + c] = Wce[((size_t)c * 2 + part) * n + p];
+#pragma unroll
+                for (int s = 0; s < S; s++)
+                    Mr[(size_t)p * VEC + (size_t)(part * S + s) * n + c] =
+                        Wc[(size_t)c * VEC + (size_t)(part * S + s) * n + p];
             }
         }
         grid_sync(ctl, trace);
-        if (j + 1 == D) break;
-        {  // r_k -= A_{k-j} dx_j, k = j+1..d
-            ts_stage<L>(Xp, Xe, n, true, xs, xe);
+    }
+
+    // c. the substitution loop, two coefficients per step
+    double *Xp1 = Xp + VEC;
+    int *Xe1 = Xe + 2 * n;
+    for (int j = 0; j < D; j += 2) {
+        const bool pair = j + 1 < D;
+        {  // dx_j = W r_j ; dx_{j+1} = W r'_{j+1} + M r_j
+            ts_stage<L>(Rp + (size_t)j * VEC, Re + (size_t)j * 2 * n, n, false, xs, xe);
+            if (pair) ts_stage<L>(Rp + (size_t)(j + 1) * VEC, Re + (size_t)(j + 1) * 2 * n, n, false, xs1, xe1);
             __syncthreads();
-            const int T = (D - 1 - j) * n;
-            const int G = pick_group(T, n, nth);
+            const int T = pair ? 2 * n : n;
+            const int G = pick_group(T, pair ? 2 * n : n, nth);
             const int ng = nth / G, g = tid / G, lg = tid % G;
             for (int base = 0; base < T; base += ng) {
                 const int task = base + g;
                 const bool valid = task < T;
-                const int k = j + 1 + (valid ? task / n : 0), p = valid ? task % n : 0;
-                const size_t row = ((size_t)(k - j) * n + p) * n;
+                const int second = valid && task >= n;
+                const int pp = valid ? task - (second ? n : 0) : 0;
+                const double *wr = Wr + (size_t)pp * n * 2 * S;
+                const int *wre = Wre + (size_t)pp * n * 2;
+                if (!second)
+                    ts_task<L>(wr, wre, xs, xe, n, lg, G, valid, DigRef{nullptr, nullptr, 0}, false,
+                               DigOut{Xp + pp, Xe + pp, n}, dx + (size_t)pp * 2 * L * D + j, D, scratch);
+                else
+                    ts_task<L>(wr, wre, xs1, xe1, n, lg, G, valid, DigRef{nullptr, nullptr, 0}, false,
+                               DigOut{Xp1 + pp, Xe1 + pp, n}, dx + (size_t)pp * 2 * L * D + j + 1, D, scratch,
+                               Seg{Mr + (size_t)pp * n * 2 * S, Mre + (size_t)pp * n * 2, xs, xe});
+            }
+        }
+        grid_sync(ctl, trace);
+        if (j + 2 >= D) break;
+        {  // r_k -= A_{k-j} dx_j + A_{k-j-1} dx_{j+1}, k = j+2..d
+            ts_stage<L>(Xp, Xe, n, true, xs, xe);
+            ts_stage<L>(Xp1, Xe1, n, true, xs1, xe1);
+            __syncthreads();
+            const int T = (D - 2 - j) * n;
+            const int G = pick_group(T, 2 * n, nth);
+            const int ng = nth / G, g = tid / G, lg = tid % G;
+            for (int base = 0; base < T; base += ng) {
+                const int task = base + g;
+                const bool valid = task < T;
+                const int k = j + 2 + (valid ? task / n : 0), p = valid ? task % n : 0;
+                const size_t row0 = ((size_t)(k - j) * n + p) * n, row1 = ((size_t)(k - j - 1) * n + p) * n;
                 double *rk = Rp + (size_t)k * VEC + p;
                 int *rke = Re + (size_t)k * 2 * n + p;
-                ts_task<L>(Ad + row * 2 * S, Ae + row * 2, xs, xe, n, lg, G, valid, DigRef{rk, rke, n}, false,
-                           DigOut{rk, rke, n}, nullptr, 0, scratch);
+                ts_task<L>(Ad + row0 * 2 * S, Ae + row0 * 2, xs, xe, n, lg, G, valid, DigRef{rk, rke, n}, false,
+                           DigOut{rk, rke, n}, nullptr, 0, scratch,
+                           Seg{Ad + row1 * 2 * S, Ae + row1 * 2, xs1, xe1});
             }
         }
         grid_sync(ctl, trace);
@@ -577,7 +661,7 @@ __global__ void __launch_bounds__(MAIN_THREADS, L <= 8 ? 3 : 2) ts_main_kernel(
 }
 
 __host__ __device__ inline size_t ts_main_smem(int S, int n, int threads) {
-    return (size_t)2 * (PADZ + S) * n * sizeof(double) + (size_t)(2 * n + 2) * sizeof(int) +
+    return (size_t)4 * (PADZ + S) * n * sizeof(double) + (size_t)(4 * n + 2) * sizeof(int) +
            (size_t)(threads / 4) * (S + 2) * sizeof(double);
 }
 
@@ -631,6 +715,8 @@ struct mdps_solver {
     int device = 0;
     double *Ad = nullptr, *M = nullptr, *Wr = nullptr, *Wc = nullptr, *Ec = nullptr, *Rp = nullptr, *Xp = nullptr;
     int *Ae = nullptr, *Wre = nullptr, *Wce = nullptr, *Ece = nullptr, *Re = nullptr, *Xe = nullptr;
+    double *Mr = nullptr;  // -W A_1 W, row planes
+    int *Mre = nullptr;
     int *piv = nullptr;
     ts::Ctl *ctl = nullptr;
     long long *trace = nullptr;
@@ -657,11 +743,16 @@ struct TsGeom {
         int dev = 0, sms = 0, per = 0;
         TS_TRY(cudaGetDevice(&dev), MDPS_ECUDA);
         TS_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), MDPS_ECUDA);
-        s->smem_main = ts::ts_main_smem(digits_for(L), s->n, ts::MAIN_THREADS);
+        s->smem_main = ts::ts_main_smem(digits_for(L), s->n, ts::main_threads(L));
+        if (s->smem_main > 227 * 1024) {
+            mdps_internal_set_error("mdps_solver_create: n too large for this limb count (two staged digit vectors "
+                                    "exceed 227 KB of shared memory)");
+            return MDPS_EINVAL;
+        }
         TS_TRY(cudaFuncSetAttribute(ts::ts_main_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)s->smem_main),
                MDPS_ECUDA);
-        TS_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ts::ts_main_kernel<L>, ts::MAIN_THREADS,
+        TS_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, ts::ts_main_kernel<L>, ts::main_threads(L),
                                                              s->smem_main),
                MDPS_ECUDA);
         if (per < 1) {
@@ -687,12 +778,12 @@ struct TsRun {
         TS_TRY(cudaGetLastError(), MDPS_ECUDA);
         const double *Ad = s->Ad;
         const int *Ae = s->Ae;
-        void *args[] = {(void *)&Ad,    (void *)&Ae,     (void *)&s->Wr, (void *)&s->Wre, (void *)&s->Wc,
-                        (void *)&s->Wce, (void *)&s->Ec, (void *)&s->Ece, (void *)&s->Rp, (void *)&s->Re,
-                        (void *)&s->Xp, (void *)&s->Xe,  (void *)&dx,    (void *)&s->n,   (void *)&s->D,
-                        (void *)&s->ctl, (void *)&s->trace};
+        void *args[] = {(void *)&Ad,     (void *)&Ae,     (void *)&s->Wr,  (void *)&s->Wre, (void *)&s->Wc,
+                        (void *)&s->Wce, (void *)&s->Ec,  (void *)&s->Ece, (void *)&s->Mr,  (void *)&s->Mre,
+                        (void *)&s->Rp,  (void *)&s->Re,  (void *)&s->Xp,  (void *)&s->Xe,  (void *)&dx,
+                        (void *)&s->n,   (void *)&s->D,   (void *)&s->ctl, (void *)&s->trace};
         TS_TRY(cudaLaunchCooperativeKernel((const void *)ts::ts_main_kernel<L>, dim3(s->grid_main),
-                                           dim3(ts::MAIN_THREADS), args, s->smem_main, st),
+                                           dim3(ts::main_threads(L)), args, s->smem_main, st),
                MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -718,7 +809,7 @@ static void solver_free(mdps_solver *s) {
     cudaFree(s->ndx);
     cudaFree(s->nnorm);
     void *ptrs[] = {s->Ad, s->Ae, s->M,  s->Wr, s->Wre, s->Wc, s->Wce, s->Ec,
-                    s->Ece, s->Rp, s->Re, s->Xp, s->Xe,  s->piv, s->ctl, s->trace};
+                    s->Ece, s->Rp, s->Re, s->Xp, s->Xe,  s->piv, s->ctl, s->trace, s->Mr, s->Mre};
     for (void *p : ptrs) cudaFree(p);
 }
 
@@ -743,13 +834,13 @@ extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t li
     const size_t sz[] = {nn * D * 2 * S * 8, nn * D * 2 * 4, nn * 4 * 8,  // Ad, Ae, M ([n][2n] complex)
                          nn * 2 * S * 8,     nn * 2 * 4,     n * VEC * 8,  // Wr, Wre, Wc
                          nn * 2 * 4,         n * VEC * 8,    nn * 2 * 4,   // Wce, Ec, Ece
-                         D * VEC * 8,        D * 2 * n * 4,  VEC * 8,      // Rp, Re, Xp
-                         2 * (size_t)n * 4,  n * sizeof(int), sizeof(ts::Ctl),  // Xe, piv, ctl
-                         ts::TRACE_MAX * sizeof(long long)};
+                         D * VEC * 8,        D * 2 * n * 4,  2 * VEC * 8,  // Rp, Re, Xp (two vectors)
+                         4 * (size_t)n * 4,  n * sizeof(int), sizeof(ts::Ctl),  // Xe, piv, ctl
+                         ts::TRACE_MAX * sizeof(long long), nn * 2 * S * 8, nn * 2 * 4};  // trace, Mr, Mre
     void **ptrs[] = {(void **)&s->Ad, (void **)&s->Ae,  (void **)&s->M,  (void **)&s->Wr,  (void **)&s->Wre,
                      (void **)&s->Wc, (void **)&s->Wce, (void **)&s->Ec, (void **)&s->Ece, (void **)&s->Rp,
                      (void **)&s->Re, (void **)&s->Xp,  (void **)&s->Xe, (void **)&s->piv, (void **)&s->ctl,
-                     (void **)&s->trace};
+                     (void **)&s->trace, (void **)&s->Mr, (void **)&s->Mre};
     bool ok = true;
     for (size_t i = 0; i < sizeof(sz) / sizeof(sz[0]) && ok; i++) {
         ok = cudaMalloc(ptrs[i], sz[i]) == cudaSuccess;
