@@ -248,6 +248,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-next", action="store_true", help="skip the solver / Newton-step measurements")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "rows"],
+                    help="N > 1: independent replicas (weak scaling, default) or one system's rows sharded (strong)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "mdps" else args.warmup
 
@@ -273,13 +275,23 @@ def main():
     mdps.lib()
 
     si = workload(args.config)
+    sharded = args.shard == "rows" and world > 1
+    if sharded:  # strong scaling: this rank evaluates its share of the rows
+        import dataclasses
+        from paper_2012_06607_b200 import shard
+        costs = shard.row_products(si.poly_ptr, si.mono_ptr, si.exps)
+        rows = shard.partition_rows(costs, world)[rank]
+        pp, mp_, vv, ee, cc = shard.subsystem(si.poly_ptr, si.mono_ptr, si.vars, si.exps, si.coeffs, rows)
+        si = dataclasses.replace(si, poly_ptr=pp, mono_ptr=mp_, vars=vv, exps=ee, coeffs=cc)
+        full_products = sum(costs)
+    n_rows = len(si.poly_ptr) - 1
     peaks = load_peaks()
     sys_ = mdps.System.from_inputs(si, algo=args.algo)
     st = sys_.stats()
     stream = torch.cuda.current_stream()
     x = torch.from_numpy(si.x).cuda()
-    vals = torch.empty((si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
-    jac = torch.empty((si.n, si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
+    vals = torch.empty((n_rows, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
+    jac = torch.empty((n_rows, si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
 
     fp64_peak_measured = mdps.fp64_peak(20000)
@@ -311,6 +323,8 @@ def main():
     ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), dist, "cuda")
     products_per_step = st["products"]
     value = whole_job_rate(products_per_step, world, args.steps, ms)
+    if sharded:  # the whole system's products once per step, over the slowest rank's time
+        value = whole_job_rate(full_products, 1, args.steps, ms)
     fp64_per_s = whole_job_rate(st["fp64_ops_total"], world, args.steps, ms)
 
     # dominant kernel: the product jobs (all levels), live CUDA-event durations
@@ -359,7 +373,8 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         ems = max_over_ranks(e0.elapsed_time(e1), dist, "cuda")
-        e2e = {"value": whole_job_rate(products_per_step, world, e2e_steps, ems), "unit": "products/s",
+        e2e = {"value": whole_job_rate(full_products, 1, e2e_steps, ems) if sharded else
+               whole_job_rate(products_per_step, world, e2e_steps, ems), "unit": "products/s",
                "h2d_bytes_per_step": int(hx.numel() * 8), "d2h_bytes_per_step": int((hv.numel() + hj.numel()) * 8),
                "steps": e2e_steps, "ms_per_step": ems / e2e_steps, "api": "mdps_eval_diff_host (pinned host buffers)"}
         # the host-buffer outputs must equal the device path's outputs
@@ -370,7 +385,7 @@ def main():
     # this system's own Jacobian and f (J dx = -f), and whole Newton steps
     # (eval/diff + solve + update), device-timed like the eval
     nxt = None
-    if not args.no_next:
+    if not args.no_next and not sharded:
         nxt = bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal, dist, args)
         nxt["newton_step"]["of_which_eval_ms"] = ms / args.steps
 
@@ -383,12 +398,13 @@ def main():
             "metric": "series products/s (mdps_eval_diff)",
             "value": value, "unit": "products/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT.get(args.config, args.config), "name": args.config,
                        "n": si.n, "monomials": si.M, "degree": si.degree, "limbs": si.limbs,
                        "algo": {1: "eft", 2: "digits"}[st["algo"]], "digits": st["digits"],
                        "products_per_step": products_per_step, "levels": st["levels"],
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"rows sharded over {world} GPUs" if sharded else f"replicas x{world}")
+                       if world > 1 else "single GPU",
                        "l2": "256 MiB buffer written between timed steps (L2 flushed)",
                        "seed": mdinputs.CONFIGS[si.name].seed if si.name in mdinputs.CONFIGS else None,
                        "input_sha256": si.sha256()[:16]},

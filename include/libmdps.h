@@ -15,7 +15,9 @@
  * z_k = sum_{i<=k} x_i y_{k-i} (§3); the Jacobian is
  * computed by algorithmic differentiation at about 3x the cost of the
  * evaluation: forward, backward and cross products per
- * monomial.  In v1, N must equal n (square systems).
+ * monomial.  N may differ from n (PAPER.md:258 allows N >= n; N < n is a
+ * subset of the rows, e.g. one GPU's share of a system sharded by rows,
+ * DESIGN.md §10).
  *
  * Series layout (all series arguments): float64, [part][limb][coefficient]
  * per series — part 0 = real, 1 = imaginary; limb 0 most significant
@@ -51,7 +53,7 @@ typedef struct mdps_system mdps_system; /* opaque; owns device memory */
  * within a monomial, in any order.  An empty monomial is a constant term.
  * Duplicate monomials within a polynomial are allowed (they are summed). */
 typedef struct {
-    int32_t n_polys;          /* must equal n in v1 */
+    int32_t n_polys;          /* N >= 1 polynomials (rows); N = n for a square system */
     const int32_t *poly_ptr;  /* [n_polys+1], non-decreasing, poly_ptr[0] = 0 */
     const int32_t *mono_ptr;  /* [M+1], non-decreasing, mono_ptr[0] = 0, M = poly_ptr[n_polys] */
     const int32_t *vars;      /* [nnz], nnz = mono_ptr[M] */
@@ -73,7 +75,7 @@ typedef struct {
  * coefficient of each monomial.  n >= 1, 0 <= degree <= 255,
  * limbs in {2,3,4,5,8,10}.  All host arrays are deep-copied; the caller may
  * free them on return.  Returns NULL on error (mdps_last_error() says why):
- * invalid sizes, NULL pointers, n_polys != n, non-monotone CSR, a variable
+ * invalid sizes, NULL pointers, n_polys < 1, non-monotone CSR, a variable
  * out of range or repeated within a monomial, an exponent < 1, or a failed
  * allocation.  Variables are sorted per monomial internally.  Requires a
  * current CUDA device (the device of the caller's current context). */
@@ -88,8 +90,8 @@ mdps_system *mdps_system_create_ex(const mdps_supports *supports, const int32_t 
 
 /* Evaluate and differentiate (the hot path).  DEVICE pointers:
  *   series_in    [n][2][limbs][D]      read only
- *   values_out   [n][2][limbs][D]      fully overwritten
- *   jacobian_out [n][n][2][limbs][D]   fully overwritten; row i = polynomial,
+ *   values_out   [N][2][limbs][D]      fully overwritten (N = supports->n_polys)
+ *   jacobian_out [N][n][2][limbs][D]   fully overwritten; row i = polynomial,
  *                                      column j = variable; entries with no
  *                                      monomial of f_i containing x_j are 0.
  * Asynchronous: enqueues kernels on `stream` (NULL = legacy default stream)

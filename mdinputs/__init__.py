@@ -271,6 +271,32 @@ def subsystem(si: SystemInputs, rows: Sequence[int], name: Optional[str] = None)
                         np.ascontiguousarray(si.coeffs[monos]), si.x)
 
 
+def rect_system(seed: int, N: int, n: int, monos: int, m_range: Tuple[int, int], exps: Tuple[int, ...],
+                degree: int, limbs: int, lower: str = "random") -> SystemInputs:
+    """N polynomials in n variables (N != n allowed), same recipe as the configs."""
+    rng = SplitMix64(seed, "structure")
+    pp, mp, vv, ee = [0], [0], [], []
+    lo, hi = m_range
+    for _ in range(N):
+        for _ in range(monos):
+            m = min(n, lo + rng.below(hi - lo + 1))
+            pool = list(range(n))
+            for j in range(m):
+                r = j + rng.below(n - j)
+                pool[j], pool[r] = pool[r], pool[j]
+            for v in sorted(pool[:m]):
+                vv.append(v)
+                ee.append(exps[rng.below(len(exps))])
+            mp.append(len(vv))
+        pp.append(len(mp) - 1)
+    D = degree + 1
+    M = len(mp) - 1
+    coeffs = unit_circle_series(SplitMix64(seed, "c"), M, D, limbs, lower)
+    x = unit_circle_series(SplitMix64(seed, "x"), n, D, limbs, lower)
+    return SystemInputs(f"rect{seed}_{N}x{n}", n, degree, limbs, np.asarray(pp, np.int32), np.asarray(mp, np.int32),
+                        np.asarray(vv, np.int32), np.asarray(ee, np.int32), coeffs, x)
+
+
 def random_system(seed: int, n: int, monos: int, m_range: Tuple[int, int], exps: Tuple[int, ...],
                   degree: int, limbs: int, lower: str = "random") -> SystemInputs:
     """A small seeded random system in the same recipe (tests)."""

@@ -208,6 +208,7 @@ class System:
     def __init__(self, poly_ptr, mono_ptr, vars_, exponents, coefficients, n, degree, limbs,
                  algo: int = MDPS_ALGO_AUTO, use_graph: bool = False):
         self.n, self.degree, self.limbs = int(n), int(degree), int(limbs)
+        self.n_polys = int(len(poly_ptr) - 1)
         self.handle = mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n,
                                          degree, limbs, algo, use_graph)
 
@@ -224,16 +225,17 @@ class System:
     def eval_diff(self, series_in, values_out=None, jacobian_out=None, stream=None):
         import torch
         if values_out is None:
-            values_out = torch.empty((self.n,) + self.series_shape, dtype=torch.float64, device=series_in.device)
+            values_out = torch.empty((self.n_polys,) + self.series_shape, dtype=torch.float64,
+                                     device=series_in.device)
         if jacobian_out is None:
-            jacobian_out = torch.empty((self.n, self.n) + self.series_shape, dtype=torch.float64,
+            jacobian_out = torch.empty((self.n_polys, self.n) + self.series_shape, dtype=torch.float64,
                                        device=series_in.device)
         mdps_eval_diff(self.handle, series_in, values_out, jacobian_out, stream)
         return values_out, jacobian_out
 
     def eval_diff_host(self, series_in: np.ndarray, stream=None):
-        vals = np.empty((self.n,) + self.series_shape)
-        jac = np.empty((self.n, self.n) + self.series_shape)
+        vals = np.empty((self.n_polys,) + self.series_shape)
+        jac = np.empty((self.n_polys, self.n) + self.series_shape)
         mdps_eval_diff_host(self.handle, np.ascontiguousarray(series_in, dtype=np.float64), vals, jac, stream)
         return vals, jac
 

@@ -199,7 +199,7 @@ struct ToDigits {
 
 // ---------------------------------------------------------------------------
 struct mdps_system {
-    int n = 0, D = 0, L = 0, M = 0, algo = MDPS_ALGO_DIGITS, S = 0;
+    int n = 0, N = 0, D = 0, L = 0, M = 0, algo = MDPS_ALGO_DIGITS, S = 0;  // n variables, N polynomials
     int use_graph = 0;
     int64_t nslots = 0, products = 0, add_terms = 0;
     std::vector<int64_t> level_off, level_cnt;  // in jobs
@@ -313,6 +313,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     mdps_system *s = new (std::nothrow) mdps_system();
     if (!s) { set_err("host allocation failed"); return nullptr; }
     s->n = n;
+    s->N = S.N;
     s->D = D;
     s->L = limbs;
     s->M = S.M;
@@ -322,7 +323,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->nslots = S.nslots;
     s->products = S.products;
     s->add_terms = (int64_t)S.ent_slot.size();
-    s->ntasks = n + n * n;
+    s->ntasks = S.N + S.N * n;
 
     std::vector<int32_t> alljobs;  // (in1, in2, out, code) per job, level by level
     for (auto &lv : S.levels4) {
@@ -417,7 +418,7 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
         }
         TimedGroup tg(s, st, 1);
         return dispatch_L<AccumEft>(L, (const double *)s->pool, (const int *)s->task_ptr,
-                                    (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, n, D, vals, jac, st);
+                                    (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, s->N, D, vals, jac, st);
     }
     {
         TimedGroup tg(s, st, 2);
@@ -438,7 +439,7 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
     // exactly the series they sum)
     TimedGroup tg(s, st, 1);
     return dispatch_L<AccumEft>(L, (const double *)s->lpool, (const int *)s->task_ptr, (const int *)s->ent_lslot,
-                                (const int *)s->ent_w, s->ntasks, n, D, vals, jac, st);
+                                (const int *)s->ent_w, s->ntasks, s->N, D, vals, jac, st);
 }
 
 extern "C" int mdps_system_set_timing(mdps_system *s, int32_t enable) {
@@ -483,8 +484,8 @@ extern "C" int mdps_eval_diff(mdps_system *s, const double *in, double *vals, do
         return MDPS_EINVAL;
     }
     const size_t ser = (size_t)2 * s->L * s->D * 8;
-    const size_t nin = ser * s->n, njac = ser * s->n * s->n;
-    if (overlaps(in, nin, vals, nin) || overlaps(in, nin, jac, njac) || overlaps(vals, nin, jac, njac)) {
+    const size_t nin = ser * s->n, nval = ser * s->N, njac = ser * s->N * s->n;
+    if (overlaps(in, nin, vals, nval) || overlaps(in, nin, jac, njac) || overlaps(vals, nval, jac, njac)) {
         set_err("outputs alias each other or the input");
         return MDPS_EINVAL;
     }
@@ -522,16 +523,16 @@ extern "C" int mdps_eval_diff_host(mdps_system *s, const double *in_h, double *v
     }
     const size_t ser = (size_t)2 * s->L * s->D;
     if (!s->dev_in) {
-        if (!dalloc(s, &s->dev_in, ser * s->n) || !dalloc(s, &s->dev_vals, ser * s->n) ||
-            !dalloc(s, &s->dev_jac, ser * s->n * s->n))
+        if (!dalloc(s, &s->dev_in, ser * s->n) || !dalloc(s, &s->dev_vals, ser * s->N) ||
+            !dalloc(s, &s->dev_jac, ser * s->N * s->n))
             return MDPS_ENOMEM;
     }
     cudaStream_t st = (cudaStream_t)stream;
     CUDA_TRY(cudaMemcpyAsync(s->dev_in, in_h, ser * s->n * 8, cudaMemcpyHostToDevice, st), MDPS_ECUDA);
     int rc = mdps_eval_diff(s, s->dev_in, s->dev_vals, s->dev_jac, stream);
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(vals_h, s->dev_vals, ser * s->n * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
-    CUDA_TRY(cudaMemcpyAsync(jac_h, s->dev_jac, ser * s->n * s->n * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
+    CUDA_TRY(cudaMemcpyAsync(vals_h, s->dev_vals, ser * s->N * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
+    CUDA_TRY(cudaMemcpyAsync(jac_h, s->dev_jac, ser * s->N * s->n * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
     CUDA_TRY(cudaStreamSynchronize(st), MDPS_ECUDA);
     return MDPS_OK;
 }
@@ -547,7 +548,7 @@ static int64_t conv_ops_per_product(int algo, int L, int D) {
 // shape of a system for solve.cu (the Newton step checks it against the solver)
 int mdps_internal_system_shape(const mdps_system *s, int *n, int *D, int *L) {
     if (!s) return MDPS_EINVAL;
-    *n = s->n;
+    *n = s->N == s->n ? s->n : -1;  // the Newton step needs a square system
     *D = s->D;
     *L = s->L;
     return MDPS_OK;
@@ -569,7 +570,7 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
         add_ops = s->add_terms * s->D * 2 * (digits_for(s->L) + 1);
     out->fp64_ops_total = out->fp64_ops_conv + add_ops;
     const int64_t ser = (int64_t)2 * s->L * s->D * 8;
-    out->compulsory_bytes = ser * ((int64_t)s->n + s->M + s->n + (int64_t)s->n * s->n);
+    out->compulsory_bytes = ser * ((int64_t)s->n + s->M + s->N + (int64_t)s->N * s->n);
     out->levels = (int32_t)s->level_cnt.size();
     out->algo = s->algo;
     out->digits = s->S;

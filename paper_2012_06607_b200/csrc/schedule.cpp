@@ -35,7 +35,7 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
                     const int32_t *vars, const int32_t *exps, int32_t n, Schedule &S,
                     std::string &err) {
     if (n < 1) { err = "n must be >= 1"; return false; }
-    if (n_polys != n) { err = "n_polys must equal n (square systems only in v1)"; return false; }
+    if (n_polys < 1) { err = "n_polys must be >= 1"; return false; }
     if (!poly_ptr || !mono_ptr) { err = "NULL poly_ptr or mono_ptr"; return false; }
     if (poly_ptr[0] != 0) { err = "poly_ptr[0] must be 0"; return false; }
     for (int i = 0; i < n_polys; i++)
@@ -46,18 +46,19 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
         if (mono_ptr[r + 1] < mono_ptr[r]) { err = "mono_ptr is not non-decreasing"; return false; }
     const int32_t nnz = mono_ptr[M];
     if (nnz > 0 && (!vars || !exps)) { err = "NULL vars or exponents"; return false; }
-    if ((int64_t)n + (int64_t)n * n + 1 > INT32_MAX) { err = "n too large"; return false; }
+    if ((int64_t)n_polys + (int64_t)n_polys * n + 1 > INT32_MAX) { err = "n too large"; return false; }
 
     S.n = n;
+    S.N = n_polys;
     S.M = M;
     S.levels.clear();
     S.products = 0;
     Builder B(S);
     B.level.assign((size_t)n + M, 0);
-    const int64_t ntasks = (int64_t)n + (int64_t)n * n;
+    const int64_t ntasks = (int64_t)n_polys + (int64_t)n_polys * n;
     std::vector<std::vector<std::pair<int32_t, int32_t>>> lists((size_t)ntasks);
     auto jac = [&](int i, int j) -> std::vector<std::pair<int32_t, int32_t>> & {
-        return lists[(size_t)n + (size_t)i * n + j];
+        return lists[(size_t)n_polys + (size_t)i * n + j];
     };
 
     std::vector<std::pair<int32_t, int32_t>> mono;

@@ -12,7 +12,9 @@
 // level is 1 + the max level of its inputs (x and c are level 0); each level
 // is one launch (the GPU analogue of the paper's stage synchronisation,
 // PAPER.md:420-424).  The addition jobs are a CSR list per
-// output series: n values then n*n Jacobian entries (row-major).
+// output series: N values then N*n Jacobian entries (row-major); N = n for a
+// square system, any N >= 1 otherwise (a row subset, an over/under-determined
+// system).
 #pragma once
 #include <cstdint>
 #include <string>
@@ -21,10 +23,10 @@
 namespace mdps {
 
 struct Schedule {
-    int n = 0, D = 0, L = 0, M = 0;
+    int n = 0, N = 0, D = 0, L = 0, M = 0;  // n variables, N polynomials
     int64_t nslots = 0;                         // n + M + jobs
     std::vector<std::vector<int32_t>> levels;   // per level: (in1, in2, out) triples
-    std::vector<int32_t> task_ptr;              // [n + n*n + 1]
+    std::vector<int32_t> task_ptr;              // [N + N*n + 1]
     std::vector<int32_t> ent_slot, ent_w;       // addition terms
     int64_t products = 0;
     int32_t max_weight = 1;

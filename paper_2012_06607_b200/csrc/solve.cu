@@ -963,7 +963,8 @@ extern "C" int mdps_newton_step(mdps_system *sys, mdps_solver *s, double *x, dou
     int sn = 0, sD = 0, sL = 0;
     mdps_internal_system_shape(sys, &sn, &sD, &sL);
     if (sn != s->n || sD != s->D || sL != s->L) {
-        mdps_internal_set_error("mdps_newton_step: system and solver differ in n, degree or limbs");
+        mdps_internal_set_error("mdps_newton_step: system and solver differ in n, degree or limbs (or the system "
+                                "is not square)");
         return MDPS_EINVAL;
     }
     const size_t ser = (size_t)2 * s->L * s->D;

@@ -57,7 +57,7 @@ def _create(**kw):
     (dict(n=0), "n must be"),
     (dict(limbs=7), "limbs"),
     (dict(degree=-1), "degree"),
-    (dict(poly_ptr=[0, 1]), "n_polys"),
+    (dict(poly_ptr=[0]), "n_polys"),
     (dict(poly_ptr=[0, 1, 0]), "non-decreasing"),
     (dict(mono_ptr=[0, 3], vars_=[0, 1, 1], exponents=[1, 1, 1]), "repeated"),
     (dict(vars_=[0, 2]), "out of range"),
