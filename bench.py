@@ -110,12 +110,13 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_baseline(si, budget_entries: int = 8):
+def cpu_baseline(si, budget_entries: int = 0):
     """The oracle as it stands on a bounded sample of the same workload:
     f_0 and the first nonzero Jacobian entries of row 0, one worker per entry
     (the paper's job queue), naive per-monomial products."""
     import oracle
-    entries = mdinputs.first_entries(si, budget_entries)
+    # one output per host core (at least 8): ~5-15 s of oracle work at od
+    entries = mdinputs.first_entries(si, budget_entries or max(8, os.cpu_count() or 1))
     cores = min(os.cpu_count() or 1, len(entries))
     t0 = time.perf_counter()
     _, prods = oracle.eval_entries(si, entries, nthreads=cores)
