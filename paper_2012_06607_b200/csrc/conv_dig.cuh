@@ -18,9 +18,10 @@
 //  * Partials: the k1 partial is parked in shared memory when a lane crosses
 //    the fold (lanes cross at different iterations); the k2 partials are
 //    added with warp shuffles.  All additions are exact (integer digits).
-//  * Shared memory per job: x planes [S][2][D], y planes [PADZ+S][2][D]
-//    (part-interleaved so the zero planes are shared), exponents [2][2][D];
-//    per thread a parking slot of S doubles.
+//  * Shared memory per job: x planes [2][S][D] (the pool's own layout, one
+//    TMA bulk copy), y planes [2][PADZ+S][D] (PADZ zero planes in front of
+//    each part, one bulk copy per part), exponents [2][2][D]; per thread a
+//    parking slot of S doubles.
 #pragma once
 #include "kernels_dig.cuh"
 
@@ -76,7 +77,7 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     constexpr int S = digits_for(L);
     constexpr int NORM = norm_every(S);
     const int D = DT > 0 ? DT : Drt;
-    const int D2 = 2 * D;
+    constexpr int P2 = PADZ + S;
     // part 0 (re): Ur*Wr - Ui*Wi ;  part 1 (im): Ur*Wi + Ui*Wr.  One code
     // copy serves both passes (instruction-cache footprint): the part only
     // selects the y planes and the sign applied to Ui (a sign-bit flip).
@@ -104,8 +105,8 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
         const double *ux = sx + i;
 #pragma unroll
         for (int s = 0; s < S; s++) {
-            Ur[s] = ux[(2 * s) * D];
-            Ui[s] = __longlong_as_double(__double_as_longlong(ux[(2 * s + 1) * D]) ^ sgn);
+            Ur[s] = ux[s * D];
+            Ui[s] = __longlong_as_double(__double_as_longlong(ux[(S + s) * D]) ^ sgn);
         }
         const int exr = ex[i], exi = ex[D + i];
         const int ey1 = ey[w1part * D + kk], ey2 = ey[w2part * D + kk];
@@ -114,16 +115,16 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
         if (exi + ey2 <= ZERO_E / 2) d2 = 0;
         const bool fast = d1 <= PADZ && d2 <= PADZ;
         if (__all_sync(__activemask(), fast)) {
-            const double *W1 = sy + (PADZ - d1) * D2 + w1part * D + kk;
-            const double *W2 = sy + (PADZ - d2) * D2 + w2part * D + kk;
+            const double *W1 = sy + (w1part * P2 + PADZ - d1) * D + kk;
+            const double *W2 = sy + (w2part * P2 + PADZ - d2) * D + kk;
             // software pipelined: row l+1's two digits load while row l's FMAs run
             double w1 = W1[0], w2 = W2[0];
 #pragma unroll
             for (int l = 0; l < S; l++) {
                 double w1n = 0.0, w2n = 0.0;
                 if (l + 1 < S) {
-                    w1n = W1[(l + 1) * D2];
-                    w2n = W2[(l + 1) * D2];
+                    w1n = W1[(l + 1) * D];
+                    w2n = W2[(l + 1) * D];
                 }
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
@@ -134,12 +135,12 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
                 w2 = w2n;
             }
         } else {
-            const double *W1 = sy + w1part * D + kk;
-            const double *W2 = sy + w2part * D + kk;
+            const double *W1 = sy + w1part * P2 * D + kk;
+            const double *W2 = sy + w2part * P2 * D + kk;
 #pragma unroll
             for (int l = 0; l < S; l++) {
-                const double w1 = (l >= d1) ? W1[(PADZ + l - d1) * D2] : 0.0;
-                const double w2 = (l >= d2) ? W2[(PADZ + l - d2) * D2] : 0.0;
+                const double w1 = (l >= d1) ? W1[(PADZ + l - d1) * D] : 0.0;
+                const double w2 = (l >= d2) ? W2[(PADZ + l - d2) * D] : 0.0;
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
@@ -238,29 +239,31 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
     int *sexp = (int *)(spark + (size_t)blockDim.x * PSTR);   // [P][2 series][2][D]
 
     const int job0 = blockIdx.x * P;
-    // stage: x planes -> [s][part][D], y planes -> [PADZ + s][part][D], zero
-    // planes.  Even D: every plane row is a 16-byte aligned contiguous run in
-    // both places, so warp 0 issues one TMA bulk copy (cp.async.bulk) per row
-    // against an mbarrier while the other warps write the zero planes and
-    // exponents.  Odd D: one warp per row, scalar loads.
+    // stage: x planes -> [part][s][D] (the pool layout), y planes ->
+    // [part][PADZ + s][D], zero planes.  Even D: three 16-byte aligned
+    // contiguous runs per job (x whole, y per part), so one thread issues
+    // three TMA bulk copies (cp.async.bulk) per job against an mbarrier while
+    // the other warps write the zero planes and exponents.  Odd D: one warp
+    // per plane row, scalar loads.
     uint64_t *bar = reinterpret_cast<uint64_t *>(sexp + (size_t)P * 4 * D);
     const bool use_tma = (D & 1) == 0;
     if (use_tma) {
         if (threadIdx.x == 0) mbar_init(bar, 1);
         __syncthreads();
         if (threadIdx.x < 32) {
-            const int nrows = P * 4 * S;
-            if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(nrows * D * 8));
+            if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(P * 4 * S * D * 8));
             __syncwarp();
-            for (int row = threadIdx.x; row < nrows; row += 32) {
-                const int jl = row / (4 * S), rem = row - jl * 4 * S;
-                const int which = rem / (2 * S), ps = rem - which * 2 * S;
-                const int part = ps / S, s = ps - part * S;
+            for (int c = threadIdx.x; c < 3 * P; c += 32) {  // (job, copy): x | y re | y im
+                const int jl = c / 3, which = c - jl * 3;
                 const int job = min(job0 + jl, njobs - 1);
-                const double *g = dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D) + (size_t)ps * D;
-                double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
-                                                                       : (s * 2 + part) * D);
-                bulk_g2s(dst, g, (unsigned)(D * 8), bar);
+                double *base = sdig + (size_t)jl * (SX + SY);
+                if (which == 0)
+                    bulk_g2s(base, dpool + (size_t)jobs[4 * job] * dig_slot_stride(S, D), (unsigned)(2 * S * D * 8),
+                             bar);
+                else
+                    bulk_g2s(base + SX + ((which - 1) * (PADZ + S) + PADZ) * D,
+                             dpool + (size_t)jobs[4 * job + 1] * dig_slot_stride(S, D) + (size_t)(which - 1) * S * D,
+                             (unsigned)(S * D * 8), bar);
             }
         }
     } else {
@@ -273,8 +276,8 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
             const int part = ps / S, s = ps - part * S;
             const int job = min(job0 + jl, njobs - 1);
             const double *g = dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D) + (size_t)ps * D;
-            double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + ((PADZ + s) * 2 + part) * D
-                                                                   : (s * 2 + part) * D);
+            double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + (part * (PADZ + S) + PADZ + s) * D
+                                                                   : (size_t)ps * D);
             if ((D & 1) == 0) {
                 for (int k = 2 * lane; k < D; k += 64)
                     *reinterpret_cast<double2 *>(dst + k) = __ldg(reinterpret_cast<const double2 *>(g + k));
@@ -283,9 +286,10 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
             }
         }
     }
-    for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {  // zero planes of both parts
         const int jl = idx / (2 * PADZ * D), r = idx - jl * 2 * PADZ * D;
-        sdig[(size_t)jl * (SX + SY) + SX + r] = 0.0;
+        const int part = r / (PADZ * D), rr = r - part * PADZ * D;
+        sdig[(size_t)jl * (SX + SY) + SX + part * (PADZ + S) * D + rr] = 0.0;
     }
     for (int idx = threadIdx.x; idx < P * 2 * 2 * D; idx += blockDim.x) {
         const int jl = idx / (4 * D), r = idx - jl * 4 * D;
