@@ -353,6 +353,16 @@ def random_toeplitz(seed: int, n: int, degree: int, limbs: int, lower: str = "ra
                           np.ascontiguousarray(jac), rhs)
 
 
+def random_toeplitz_rect(seed: int, N: int, n: int, degree: int, limbs: int, lower: str = "random",
+                         name: Optional[str] = None) -> ToeplitzInputs:
+    """N >= n equations (least squares): jac [N][n][2][L][D], rhs [N][2][L][D]."""
+    D = degree + 1
+    jac = unit_circle_series(SplitMix64(seed, "jac"), N * n, D, limbs, lower).reshape(N, n, 2, limbs, D)
+    rhs = unit_circle_series(SplitMix64(seed, "rhs"), N, D, limbs, lower)
+    return ToeplitzInputs(name or f"toeplitz{seed}_{N}x{n}_d{degree}_L{limbs}", n, degree, limbs,
+                          np.ascontiguousarray(jac), rhs)
+
+
 def toeplitz_config(name: str) -> ToeplitzInputs:
     """The solve that follows config `name`'s eval/diff: its n, degree, limbs,
     lower-limb rule and seed (sweep: its largest cell)."""

@@ -55,6 +55,7 @@ def lib() -> ctypes.CDLL:
                                        i32, P(i32), P(i32), P(d), i32, P(ll)]
         L.mdo_series_err.argtypes = [P(d), P(d), i32, i32, i32, P(d)]
         L.mdo_toeplitz_solve.argtypes = [i32, i32, i32, P(d), P(d), P(d), P(i32), i32]
+        L.mdo_toeplitz_normal.argtypes = [i32, i32, i32, i32, P(d), P(d), i32, P(d), P(d)]
         _lib = L
     return _lib
 
@@ -240,6 +241,28 @@ def toeplitz_solve(jac, rhs, nthreads: Optional[int] = None, limbs: Optional[int
         raise SingularError("A_0 is singular (zero pivot column)")
     _check(rc, "toeplitz_solve")
     return dx, piv
+
+
+def toeplitz_lstsq(jac, rhs, nthreads: Optional[int] = None):
+    """Least-squares forward substitution for N >= n equations:
+    dx_j = argmin |A_0 dx_j - r_j|, r_j = b_j - sum_{i>=1} A_i dx_{j-i}, i.e. the
+    square forward substitution of the normal equations A_0^H A(t) dx = A_0^H b
+    (formed exactly, rounded to L+3 limbs, solved at L+3 limbs, dx rounded to L).
+    jac [N][n][2][L][D], rhs [N][2][L][D] -> dx [n][2][L][D]."""
+    jac, rhs = _f64(jac), _f64(rhs)
+    N, n, two, L, D = jac.shape
+    assert two == 2 and rhs.shape == (N, 2, L, D) and N >= n
+    Lo = L + 3
+    jt = np.zeros((n, n, 2, Lo, D))
+    bt = np.zeros((n, 2, Lo, D))
+    _check(lib().mdo_toeplitz_normal(N, n, D, L, _dp(jac), _dp(rhs), Lo, _dp(jt), _dp(bt)), "toeplitz_normal")
+    dxo, _ = toeplitz_solve(jt, bt, nthreads)
+    dx = np.zeros((n, 2, L, D))
+    for q in range(n):
+        for part in range(2):
+            for k in range(D):
+                dx[q, part, :, k] = md_round(dxo[q, part, :, k], L)
+    return dx
 
 
 # ---- Newton's method on power series ----------------------------------------------

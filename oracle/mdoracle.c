@@ -883,3 +883,53 @@ int mdo_toeplitz_solve(int n, int D, int L, const double *J, const double *b, do
     if (rc) return rc;
     return g_err ? -1 : 0;
 }
+
+/* ---------------------------------------------------------------------------
+ * Least squares for N > n equations ("For N > n, the linear
+ * systems are solved in the least squares sense").  With full column rank,
+ * the least-squares solution of A_0 dx_j = r_j is the plain definition
+ * dx_j = (A_0^H A_0)^-1 A_0^H r_j, and r_j = b_j - sum_{i>=1} A_i dx_{j-i}
+ * turns the whole forward substitution into the square one for
+ *     At_i = A_0^H A_i (n x n),  bt_j = A_0^H b_j,
+ * At_0 = A_0^H A_0 (reading R18).  This routine forms every entry of
+ * At and bt EXACTLY and rounds it to Lo limbs (Lo = L + 3 keeps the squared
+ * condition number of the normal equations out of the result); the caller
+ * solves the square system at Lo limbs and rounds to L.
+ * J: [N][n][2][L][D], b: [N][2][L][D]; Jt: [n][n][2][Lo][D], bt: [n][2][Lo][D].
+ * ------------------------------------------------------------------------- */
+int mdo_toeplitz_normal(int N, int n, int D, int L, const double *J, const double *b, int Lo, double *Jt,
+                        double *bt) {
+    if (N < 1 || n < 1 || D < 1 || L < 1 || Lo < 1 || Lo > MDO_MAXL) return -3;
+    g_err = 0;
+    sa_t *s = (sa_t *)malloc(2 * sizeof(sa_t));
+    if (!s) return -5;
+    sa_init(&s[0]);
+    sa_init(&s[1]);
+    /* conj(a) * c: re = ar cr + ai ci, im = ar ci - ai cr */
+    for (int p = 0; p < n; p++)
+        for (int col = 0; col <= n; col++)  /* col == n: the right-hand side */
+            for (int k = 0; k < D; k++) {
+                for (int r = 0; r < N; r++)
+                    for (int u = 0; u < L; u++)
+                        for (int v = 0; v < L; v++) {
+                            double ar = J[EIDX(r, p, 0, u, 0, n, L, D)], ai = J[EIDX(r, p, 1, u, 0, n, L, D)];
+                            double cr, ci;
+                            if (col < n) {
+                                cr = J[EIDX(r, col, 0, v, k, n, L, D)];
+                                ci = J[EIDX(r, col, 1, v, k, n, L, D)];
+                            } else {
+                                cr = b[SIDX(0, v, k, L, D) + (size_t)r * 2 * L * D];
+                                ci = b[SIDX(1, v, k, L, D) + (size_t)r * 2 * L * D];
+                            }
+                            sa_add_prod(&s[0], ar, cr, 1);
+                            sa_add_prod(&s[0], ai, ci, 1);
+                            sa_add_prod(&s[1], ar, ci, 1);
+                            sa_add_prod(&s[1], ai, cr, -1);
+                        }
+                double *out = col < n ? Jt + EIDX(p, col, 0, 0, k, n, Lo, D) : bt + SIDX(0, 0, k, Lo, D) + (size_t)p * 2 * Lo * D;
+                sa_round_limbs(&s[0], Lo, out, D);
+                sa_round_limbs(&s[1], Lo, out + (size_t)Lo * D, D);
+            }
+    free(s);
+    return g_err ? -1 : 0;
+}
