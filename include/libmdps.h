@@ -155,10 +155,20 @@ int mdps_system_level_jobs(const mdps_system *sys, int64_t *jobs_per_level, int3
 typedef struct mdps_solver mdps_solver; /* opaque; owns its device workspace */
 
 /* n in [1, 256], degree in [0, 255], limbs in {2,3,4,5,8,10}.  Allocates the
- * workspace (about 2x the Jacobian) on the current device.  NULL on error. */
+ * workspace (about 2x the Jacobian) on the current device.  NULL on error
+ * (also when the shared-memory footprint of the solver kernel for this n and
+ * limb count exceeds 227 KB: n > ~230 at 10 limbs). */
 mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t limbs);
 
-/* dx(t) with A(t) dx(t) = rhs(t) mod t^D.  DEVICE pointers: jacobian and rhs
+/* A solver for N >= n equations in n unknowns (least squares):
+ * each dx_j minimises |A_0 dx_j - r_j| with r_j = b_j - sum_{i>=1} A_i dx_{j-i};
+ * the GPU applies A_0^+ (refined to md precision from the normal equations'
+ * double-precision solution).  Then jacobian is [N][n][...], rhs [N][...] and
+ * dx_out [n][...] in mdps_solve; pivots (mdps_solver_status) are those of
+ * A_0^H A_0.  N = n is mdps_solver_create.  Requires full column rank. */
+mdps_solver *mdps_solver_create_ls(int32_t N, int32_t n, int32_t degree, int32_t limbs);
+
+/* dx(t) with A(t) dx(t) = rhs(t) mod t^D (least squares for N > n).  DEVICE pointers: jacobian and rhs
  * read only, dx_out fully overwritten; dx_out must not alias the inputs.
  * Asynchronous on `stream`; one solve may be in flight per solver.  Returns
  * MDPS_OK, MDPS_EINVAL or MDPS_ECUDA.  A singular A_0 (a zero pivot column)

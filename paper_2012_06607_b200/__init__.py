@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
     "mdps_fp64_peak", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
-    "mdps_solver_trace", "mdps_newton_step", "mdps_newton",
+    "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls",
 )
 
 
@@ -114,6 +114,8 @@ def lib() -> ctypes.CDLL:
     L.mdps_system_timing.argtypes = [vp, P(Timing), i32]
     L.mdps_solver_create.restype = vp
     L.mdps_solver_create.argtypes = [i32, i32, i32]
+    L.mdps_solver_create_ls.restype = vp
+    L.mdps_solver_create_ls.argtypes = [i32, i32, i32, i32]
     L.mdps_solve.argtypes = [vp, vp, vp, vp, vp]
     L.mdps_solver_status.argtypes = [vp, P(i32), P(i32)]
     L.mdps_solver_stats.argtypes = [vp, P(SolverInfo)]
@@ -279,9 +281,10 @@ class Solver:
     """RAII wrapper of the block lower-triangular Toeplitz solver (libmdps.h):
     dx(t) with A(t) dx(t) = b(t) mod t^D, A(t) the n-by-n Jacobian series."""
 
-    def __init__(self, n: int, degree: int, limbs: int):
+    def __init__(self, n: int, degree: int, limbs: int, n_eqs: Optional[int] = None):
         self.n, self.degree, self.limbs = int(n), int(degree), int(limbs)
-        self.handle = lib().mdps_solver_create(self.n, self.degree, self.limbs)
+        self.n_eqs = int(n_eqs) if n_eqs is not None else self.n
+        self.handle = lib().mdps_solver_create_ls(self.n_eqs, self.n, self.degree, self.limbs)
         if not self.handle:
             raise MdpsError(f"mdps_solver_create failed: {mdps_last_error()}")
 

@@ -546,9 +546,10 @@ static int64_t conv_ops_per_product(int algo, int L, int D) {
 }
 
 // shape of a system for solve.cu (the Newton step checks it against the solver)
-int mdps_internal_system_shape(const mdps_system *s, int *n, int *D, int *L) {
+int mdps_internal_system_shape(const mdps_system *s, int *N, int *n, int *D, int *L) {
     if (!s) return MDPS_EINVAL;
-    *n = s->N == s->n ? s->n : -1;  // the Newton step needs a square system
+    *N = s->N;
+    *n = s->n;
     *D = s->D;
     *L = s->L;
     return MDPS_OK;

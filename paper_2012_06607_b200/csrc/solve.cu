@@ -43,7 +43,7 @@
 #include "conv_dig.cuh"
 
 void mdps_internal_set_error(const std::string &s);  // libmdps.cu
-int mdps_internal_system_shape(const mdps_system *s, int *n, int *D, int *L);
+int mdps_internal_system_shape(const mdps_system *s, int *N, int *n, int *D, int *L);
 
 namespace mdps {
 namespace ts {
@@ -96,22 +96,25 @@ __device__ __forceinline__ void grid_sync(Ctl *c, long long *trace) {
 }
 
 // ---- 1. pack ---------------------------------------------------------------------
-// Row p of A_k as a digit vector in planes: Ad[k][p][2][S][n] + exponents
-// Ae[k][p][2][n] (k = 0..d; q fastest, so that the lanes of a group reading
-// consecutive q load consecutive addresses); R planes [k][2][S][n] +
-// exponents [k][2][n] (negated for a Newton step).
+// A(t) has N rows (equations) and n columns (unknowns), N >= n.  Row p of A_k
+// as a digit vector in planes: Ad[k][p][2][S][n] + exponents Ae[k][p][2][n]
+// (q fastest, so that the lanes of a group reading consecutive q load
+// consecutive addresses); A_0's columns as planes Ac[c][2][S][N] (for the
+// refinement); R planes [k][2][S][N] + exponents [k][2][N] (r_k starts as b_k,
+// negated for a Newton step).
 template <int L>
 __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__ J, const double *__restrict__ b,
                                                       double *__restrict__ Ad, int *__restrict__ Ae,
-                                                      double *__restrict__ Rp, int *__restrict__ Re, int n, int D,
-                                                      int negate) {
+                                                      double *__restrict__ Ac, int *__restrict__ Ace,
+                                                      double *__restrict__ Rp, int *__restrict__ Re, int N, int n,
+                                                      int D, int negate) {
     constexpr int S = digits_for(L);
-    const size_t nj = (size_t)n * n * D, total = nj + (size_t)n * D;
+    const size_t nj = (size_t)N * n * D, total = nj + (size_t)N * D;
     for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (size_t)gridDim.x * blockDim.x) {
         if (g < nj) {  // (k, p, q): q fastest for coalesced digit-plane writes
             const int q = (int)(g % n);
             const size_t kp = g / n;
-            const int p = (int)(kp % n), k = (int)(kp / n);
+            const int p = (int)(kp % N), k = (int)(kp / N);
             const double *src = J + ((size_t)p * n + q) * 2 * L * D + k;
             double *dst = Ad + kp * 2 * S * n + q;
             int *de = Ae + kp * 2 * n + q;
@@ -120,9 +123,14 @@ __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__
                 double v[L], d[S];
 #pragma unroll
                 for (int l = 0; l < L; l++) v[l] = src[(size_t)(part * L + l) * D];
-                de[(size_t)part * n] = limbs_to_digits<L, S>(v, d);
+                const int e = limbs_to_digits<L, S>(v, d);
+                de[(size_t)part * n] = e;
+                if (k == 0) Ace[((size_t)q * 2 + part) * N + p] = e;
 #pragma unroll
-                for (int t = 0; t < S; t++) dst[(size_t)(part * S + t) * n] = d[t];
+                for (int t = 0; t < S; t++) {
+                    dst[(size_t)(part * S + t) * n] = d[t];
+                    if (k == 0) Ac[(((size_t)q * 2 + part) * S + t) * N + p] = d[t];
+                }
             }
         } else {
             const size_t g2 = g - nj;
@@ -136,38 +144,52 @@ __global__ void __launch_bounds__(128) ts_pack_kernel(const double *__restrict__
                     const double x = b[(p * 2 * L + part * L + l) * D + k];
                     v[l] = negate ? -x : x;
                 }
-                Re[((size_t)k * 2 + part) * n + p] = limbs_to_digits<L, S>(v, d);
+                Re[((size_t)k * 2 + part) * N + p] = limbs_to_digits<L, S>(v, d);
 #pragma unroll
-                for (int t = 0; t < S; t++) Rp[(((size_t)k * 2 + part) * S + t) * n + p] = d[t];
+                for (int t = 0; t < S; t++) Rp[(((size_t)k * 2 + part) * S + t) * N + p] = d[t];
             }
         }
     }
 }
 
 // ---- 2. factor A_0 once: Gauss-Jordan, partial pivoting, complex double -------------
-// [A_0 | I] -> [I | W_0] on the leading limbs (one block; M in global memory,
-// L2-resident).  Pivot k = the row i >= k maximising |re| + |im| (lowest row
-// on ties).  W_0 -> digit planes of its rows and of its columns.
+// Square (N = n): [A_0 | I] -> [I | W_0], W_0 ~ A_0^-1.  Least squares (N > n,
+// PAPER.md:258-262): [G | I] -> [I | V_0], V_0 ~ G^-1, G = A_0^H A_0 (the
+// refinement then makes V = G^-1 exact to md precision and forms A_0^+ =
+// V A_0^H).  Leading limbs, one block, M in global memory (L2-resident).
+// Pivot k = the row i >= k maximising |re| + |im| (lowest row on ties).  The
+// n x n result -> digit planes of its rows [p][2][S][n] and columns [c][2][S][n].
 template <int L>
 __global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restrict__ J, double *__restrict__ M,
                                                            int *__restrict__ piv, Ctl *ctl, double *__restrict__ Wr,
                                                            int *__restrict__ Wre, double *__restrict__ Wc,
-                                                           int *__restrict__ Wce, int n, int D) {
+                                                           int *__restrict__ Wce, int N, int n, int D) {
     constexpr int S = digits_for(L);
     const int tx = threadIdx.x, nt = blockDim.x;
-    const int W2 = 2 * n;  // row length of [A | I] in complex entries
+    const int W2 = 2 * n;  // row length of [left | I] in complex entries
     __shared__ double s_m[GJ_THREADS];
     __shared__ int s_i[GJ_THREADS];
     __shared__ double s_p[2];
     double2 *Mc = reinterpret_cast<double2 *>(M);
+    auto a0 = [&](int r, int c) {  // leading limbs of A_0[r][c]
+        const double *src = J + ((size_t)r * n + c) * 2 * L * D;
+        return make_double2(src[0], src[(size_t)L * D]);
+    };
     for (int t = tx; t < n * W2; t += nt) {
         const int i = t / W2, c = t - i * W2;
         double2 v;
-        if (c < n) {
-            const double *src = J + ((size_t)i * n + c) * 2 * L * D;
-            v = make_double2(src[0], src[(size_t)L * D]);
-        } else {
+        if (c >= n) {
             v = make_double2(c - n == i ? 1.0 : 0.0, 0.0);
+        } else if (N == n) {
+            v = a0(i, c);
+        } else {  // G[i][c] = sum_r conj(A_0[r][i]) A_0[r][c]
+            double re = 0.0, im = 0.0;
+            for (int r = 0; r < N; r++) {
+                const double2 x = a0(r, i), y = a0(r, c);
+                re = __fma_rn(x.x, y.x, __fma_rn(x.y, y.y, re));
+                im = __fma_rn(x.x, y.y, __fma_rn(-x.y, y.x, im));
+            }
+            v = make_double2(re, im);
         }
         Mc[t] = v;
     }
@@ -237,7 +259,7 @@ __global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restr
         __syncthreads();
     }
     if (tx == 0 && singular) atomicOr(&ctl->status, 1);
-    for (int t = tx; t < n * n; t += nt) {  // W_0 -> digits: rows [p][q][2][S], column planes [c][2][S][row]
+    for (int t = tx; t < n * n; t += nt) {  // W_0 (or V_0) -> digits
         const int p = t / n, q = t - p * n;
         const double2 w = Mc[(size_t)p * W2 + n + q];
 #pragma unroll 1
@@ -331,8 +353,9 @@ __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, con
 // stage a digit vector given as planes [2][S][n] (+ exponents [2][n]) into
 // shared planes [2][PADZ + S][n], optionally negated
 template <int L>
+// mode: 0 as is, 1 negated, 2 conjugated (imaginary part negated)
 __device__ __forceinline__ void ts_stage(const double *__restrict__ src, const int *__restrict__ srce, int n,
-                                         bool negate, double *xs, int *xe) {
+                                         int mode, double *xs, int *xe) {
     constexpr int S = digits_for(L);
     constexpr int P2 = PADZ + S;
     const int SN = S * n;
@@ -340,10 +363,11 @@ __device__ __forceinline__ void ts_stage(const double *__restrict__ src, const i
     for (int part = 0; part < 2; part++) {
         double *dst = xs + ((size_t)part * P2 + PADZ) * n;
         const double *s0 = src + (size_t)part * SN;
+        const bool neg = mode == 1 || (mode == 2 && part == 1);
 #pragma unroll 4
         for (int t = threadIdx.x; t < SN; t += blockDim.x) {
             const double v = __ldcg(s0 + t);
-            dst[t] = negate ? -v : v;
+            dst[t] = neg ? -v : v;
         }
         double *z = xs + (size_t)part * P2 * n;
         for (int t = threadIdx.x; t < PADZ * n; t += blockDim.x) z[t] = 0.0;
@@ -469,86 +493,141 @@ __device__ __forceinline__ int pick_group(long long tasks, int n, long long avai
     return G;
 }
 
-// Newton-Schulz refinement of W, then the substitution loop.
+// Matrix-product phases: task (column c, row p) with the column staged once
+// per block; blocks are split into `bpc` blocks per column, each taking a
+// chunk of the rows.
+struct ColSplit {
+    int c0, cstep, r0, r1;
+};
+__device__ __forceinline__ ColSplit col_split(int ncols, int nrows) {
+    const int bpc = max(1, (int)gridDim.x / ncols), ncb = (int)gridDim.x / bpc;
+    const int cslot = blockIdx.x / bpc, rchunk = blockIdx.x % bpc, rpb = (nrows + bpc - 1) / bpc;
+    ColSplit cs;
+    cs.c0 = cslot < ncb ? cslot : ncols;
+    cs.cstep = ncb;
+    cs.r0 = rchunk * rpb;
+    cs.r1 = min(nrows, cs.r0 + rpb);
+    return cs;
+}
+
+// Newton-Schulz refinement of W ~ A_0^+, the two-coefficient operator M, then
+// the substitution loop.  A(t): N x n (N >= n); W, M: n x N.
 template <int L>
 __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kernel(
-    const double *__restrict__ Ad, const int *__restrict__ Ae, double *__restrict__ Wr, int *__restrict__ Wre,
-    double *__restrict__ Wc, int *__restrict__ Wce, double *__restrict__ Ec, int *__restrict__ Ece,
-    double *__restrict__ Mr, int *__restrict__ Mre, double *__restrict__ Rp, int *__restrict__ Re,
-    double *__restrict__ Xp, int *__restrict__ Xe, double *__restrict__ dx, int n, int D, Ctl *ctl,
-    long long *trace) {
+    const double *__restrict__ Ad, const int *__restrict__ Ae, const double *__restrict__ Ac,
+    const int *__restrict__ Ace, double *__restrict__ Wr, int *__restrict__ Wre, double *Wc, int *Wce,
+    double *Wc2, int *Wce2, double *__restrict__ Er, int *__restrict__ Ere, double *__restrict__ Pc,
+    int *__restrict__ Pce, double *__restrict__ Mr, int *__restrict__ Mre, double *__restrict__ Rp,
+    int *__restrict__ Re, double *__restrict__ Xp, int *__restrict__ Xe, double *__restrict__ dx,
+    double *__restrict__ Gc, int *__restrict__ Gce, int N, int n, int D, Ctl *ctl, long long *trace) {
     constexpr int S = digits_for(L);
     constexpr int P2 = PADZ + S;
     if (tid0()) trace[ctl->ntrace++] = global_ns();
     extern __shared__ __align__(16) double sm[];
-    double *xs = sm;                              // [2][P2][n]  staged vector 0
-    double *xs1 = sm + (size_t)2 * P2 * n;        // [2][P2][n]  staged vector 1
-    int *xe = (int *)(xs1 + (size_t)2 * P2 * n);  // [2][n]
-    int *xe1 = xe + 2 * n;                        // [2][n]
-    double *scr = (double *)(xe1 + 2 * n + 2);    // [blockDim/4][S+2] emit scratch (one per group leader)
+    double *xs = sm;                              // [2][P2][N]  staged vector 0
+    double *xs1 = sm + (size_t)2 * P2 * N;        // [2][P2][N]  staged vector 1
+    int *xe = (int *)(xs1 + (size_t)2 * P2 * N);  // [2][N]
+    int *xe1 = xe + 2 * N;                        // [2][N]
+    double *scr = (double *)(xe1 + 2 * N + 2);    // [blockDim/4][S+2] emit scratch (one per group leader)
     __shared__ int s_emax;
     const int nth = gridDim.x * blockDim.x;
     const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t VEC = (size_t)2 * S * n;        // doubles per digit vector (planes)
+    const size_t VN = (size_t)2 * S * n, VM = (size_t)2 * S * N;  // doubles per digit vector of length n / N
     double *scratch = scr + (size_t)(threadIdx.x / 4) * (S + 2);
-    // matrix products: blocks take (column c, chunk of rows); each block
-    // stages its column once
-    const int bpc = max(1, (int)gridDim.x / n);                // blocks per column
-    const int ncb = (int)gridDim.x / bpc;                      // columns in flight
-    const int rows_pb = (n + bpc - 1) / bpc;
-    const int Gm = pick_group(rows_pb, n, blockDim.x);
-    const int gpb = blockDim.x / Gm, gm = threadIdx.x / Gm, lgm = threadIdx.x % Gm;
-    const int cslot = blockIdx.x / bpc, rchunk = blockIdx.x % bpc;
-    const int r0 = rchunk * rows_pb, r1 = min(n, r0 + rows_pb);
-    const bool mp_active = cslot < ncb;
+    const DigRef none{nullptr, nullptr, 0};
 
-    // a. W <- W + W (I - A_0 W): columns of E and W are digit vectors (planes)
-    for (int it = 0; it < MAX_REFINE; it++) {
-        if (threadIdx.x == 0) s_emax = ZERO_E;
-        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // E[:, c] = e_c - A_0 W[:, c]
-            ts_stage<L>(Wc + (size_t)c * VEC, Wce + (size_t)c * 2 * n, n, true, xs, xe);
+    // a0. least squares (N > n): G = A_0^H A_0 (n x n, exact dot products): the
+    //     task for staged conj(A_0[:, c]) and row p computes sum_r A_0[r][p]
+    //     conj(A_0[r][c]) = G[c][p] (G is Hermitian), written to column p.
+    const bool lsq = N > n;
+    if (lsq) {
+        const ColSplit cs = col_split(n, n);
+        const int G = pick_group(cs.r1 - cs.r0, N, blockDim.x);
+        const int gpb = blockDim.x / G, g = threadIdx.x / G, lg = threadIdx.x % G;
+        for (int c = cs.c0; c < n; c += cs.cstep) {
+            ts_stage<L>(Ac + (size_t)c * VM, Ace + (size_t)c * 2 * N, N, 2, xs, xe);
             __syncthreads();
-            for (int base = r0; base < r1; base += gpb) {
-                const int p = base + gm;
-                const bool valid = p < r1;
+            for (int base = cs.r0; base < cs.r1; base += gpb) {
+                const int p = base + g;
+                const bool valid = p < cs.r1;
                 const int pp = valid ? p : 0;
-                const int e = ts_task<L>(Ad + (size_t)pp * n * 2 * S, Ae + (size_t)pp * n * 2, xs, xe, n, lgm, Gm,
-                                         valid, DigRef{nullptr, nullptr, 0}, pp == c,
-                                         DigOut{Ec + (size_t)c * VEC + pp, Ece + (size_t)c * 2 * n + pp, n},
-                                         nullptr, 0, scratch);
-                if (valid && lgm == 0) atomicMax(&s_emax, e);
+                ts_task<L>(Ac + (size_t)pp * VM, Ace + (size_t)pp * 2 * N, xs, xe, N, lg, G, valid, none, false,
+                           DigOut{Gc + (size_t)pp * VN + c, Gce + (size_t)pp * 2 * n + c, n}, nullptr, 0, scratch);
             }
             __syncthreads();
+        }
+        grid_sync(ctl, trace);
+    }
+    // a. W <- W + (I - W A) W, the left Newton-Schulz step: W -> A_0^-1 (N = n)
+    //    or V -> G^-1 (N > n, A = G); E = I - W A (n x n, row planes), W' = W + E W.
+    const int RL = lsq ? n : N;                    // length of W's rows / A's columns here
+    const double *RA = lsq ? Gc : Ac;
+    const int *RAe = lsq ? Gce : Ace;
+    const size_t VR = (size_t)2 * S * RL;
+    for (int it = 0; it < MAX_REFINE; it++) {
+        if (threadIdx.x == 0) s_emax = ZERO_E;
+        {
+            const ColSplit cs = col_split(n, n);
+            const int G = pick_group(cs.r1 - cs.r0, RL, blockDim.x);
+            const int gpb = blockDim.x / G, g = threadIdx.x / G, lg = threadIdx.x % G;
+            for (int c = cs.c0; c < n; c += cs.cstep) {  // E[:, c] = e_c - W A[:, c]
+                ts_stage<L>(RA + (size_t)c * VR, RAe + (size_t)c * 2 * RL, RL, 1, xs, xe);
+                __syncthreads();
+                for (int base = cs.r0; base < cs.r1; base += gpb) {
+                    const int p = base + g;
+                    const bool valid = p < cs.r1;
+                    const int pp = valid ? p : 0;
+                    const int e = ts_task<L>(Wr + (size_t)pp * VR, Wre + (size_t)pp * 2 * RL, xs, xe, RL, lg, G, valid,
+                                             none, pp == c, DigOut{Er + (size_t)pp * VN + c, Ere + (size_t)pp * 2 * n + c, n},
+                                             nullptr, 0, scratch);
+                    if (valid && lg == 0) atomicMax(&s_emax, e);
+                }
+                __syncthreads();
+            }
         }
         if (threadIdx.x == 0 && s_emax > ZERO_E / 2) atomicMax(&ctl->emax, s_emax + EMAX_BIAS);
         grid_sync(ctl, trace);
-        // ||E|| < R^emax / 2; W += W E leaves an error ~||E||^2: stop once that
+        // ||E|| < R^emax / 2; the step leaves an error ~||E||^2: stop once that
         // is below 2^-(53 L + 16)
         const int eraw = *(volatile int *)&ctl->emax;
         const bool last = eraw == 0 || 2 * (BETA * (eraw - EMAX_BIAS) - 1) < -(53 * L + 16) || it + 1 == MAX_REFINE;
-        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // W[:, c] += W E[:, c]
-            ts_stage<L>(Ec + (size_t)c * VEC, Ece + (size_t)c * 2 * n, n, false, xs, xe);
-            __syncthreads();
-            for (int base = r0; base < r1; base += gpb) {
-                const int p = base + gm;
-                const bool valid = p < r1;
-                const int pp = valid ? p : 0;
-                ts_task<L>(Wr + (size_t)pp * n * 2 * S, Wre + (size_t)pp * n * 2, xs, xe, n, lgm, Gm, valid,
-                           DigRef{Wc + (size_t)c * VEC + pp, Wce + (size_t)c * 2 * n + pp, n}, false,
-                           DigOut{Wc + (size_t)c * VEC + pp, Wce + (size_t)c * 2 * n + pp, n}, nullptr, 0, scratch);
+        {
+            const ColSplit cs = col_split(RL, n);
+            const int G = pick_group(cs.r1 - cs.r0, n, blockDim.x);
+            const int gpb = blockDim.x / G, g = threadIdx.x / G, lg = threadIdx.x % G;
+            for (int c = cs.c0; c < RL; c += cs.cstep) {  // W'[:, c] = W[:, c] + E W[:, c]
+                ts_stage<L>(Wc + (size_t)c * VN, Wce + (size_t)c * 2 * n, n, 0, xs, xe);
+                __syncthreads();
+                for (int base = cs.r0; base < cs.r1; base += gpb) {
+                    const int p = base + g;
+                    const bool valid = p < cs.r1;
+                    const int pp = valid ? p : 0;
+                    ts_task<L>(Er + (size_t)pp * VN, Ere + (size_t)pp * 2 * n, xs, xe, n, lg, G, valid,
+                               DigRef{Wc + (size_t)c * VN + pp, Wce + (size_t)c * 2 * n + pp, n}, false,
+                               DigOut{Wc2 + (size_t)c * VN + pp, Wce2 + (size_t)c * 2 * n + pp, n}, nullptr, 0,
+                               scratch);
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
         grid_sync(ctl, trace);
-        for (size_t t = tid; t < (size_t)n * n; t += nth) {  // row planes <- column planes
-            const int p = (int)(t / n), c = (int)(t % n);
+        {  // W' becomes W (column planes); row planes from it
+            double *t = Wc;
+            Wc = Wc2;
+            Wc2 = t;
+            int *te = Wce;
+            Wce = Wce2;
+            Wce2 = te;
+        }
+        for (size_t t = tid; t < (size_t)n * RL; t += nth) {
+            const int pr = (int)(t / RL), c = (int)(t % RL);
 #pragma unroll
             for (int part = 0; part < 2; part++) {
-                Wre[((size_t)p * 2 + part) * n + c] = Wce[((size_t)c * 2 + part) * n + p];
+                Wre[((size_t)pr * 2 + part) * RL + c] = Wce[((size_t)c * 2 + part) * n + pr];
 #pragma unroll
-                for (int s = 0; s < S; s++)
-                    Wr[(size_t)p * VEC + (size_t)(part * S + s) * n + c] =
-                        Wc[(size_t)c * VEC + (size_t)(part * S + s) * n + p];
+                for (int sd = 0; sd < S; sd++)
+                    Wr[(size_t)pr * VR + (size_t)(part * S + sd) * RL + c] =
+                        Wc[(size_t)c * VN + (size_t)(part * S + sd) * n + pr];
             }
         }
         if (tid == 0) {
@@ -558,102 +637,152 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
         grid_sync(ctl, trace);
         if (last) break;
     }
+    // a2. least squares: W = V A_0^H (n x N): column c of W is V conj(A_0[c, :])^T
+    if (lsq) {
+        {
+            const ColSplit cs = col_split(N, n);
+            const int G = pick_group(cs.r1 - cs.r0, n, blockDim.x);
+            const int gpb = blockDim.x / G, g = threadIdx.x / G, lg = threadIdx.x % G;
+            for (int c = cs.c0; c < N; c += cs.cstep) {
+                ts_stage<L>(Ad + (size_t)c * VN, Ae + (size_t)c * 2 * n, n, 2, xs, xe);  // row c of A_0
+                __syncthreads();
+                for (int base = cs.r0; base < cs.r1; base += gpb) {
+                    const int p = base + g;
+                    const bool valid = p < cs.r1;
+                    const int pp = valid ? p : 0;
+                    ts_task<L>(Wr + (size_t)pp * VN, Wre + (size_t)pp * 2 * n, xs, xe, n, lg, G, valid, none, false,
+                               DigOut{Wc2 + (size_t)c * VN + pp, Wce2 + (size_t)c * 2 * n + pp, n}, nullptr, 0,
+                               scratch);
+                }
+                __syncthreads();
+            }
+        }
+        grid_sync(ctl, trace);
+        {
+            double *t = Wc;
+            Wc = Wc2;
+            Wc2 = t;
+            int *te = Wce;
+            Wce = Wce2;
+            Wce2 = te;
+        }
+        for (size_t t = tid; t < (size_t)n * N; t += nth) {  // row planes (length N) <- columns
+            const int pr = (int)(t / N), c = (int)(t % N);
+#pragma unroll
+            for (int part = 0; part < 2; part++) {
+                Wre[((size_t)pr * 2 + part) * N + c] = Wce[((size_t)c * 2 + part) * n + pr];
+#pragma unroll
+                for (int sd = 0; sd < S; sd++)
+                    Wr[(size_t)pr * VM + (size_t)(part * S + sd) * N + c] =
+                        Wc[(size_t)c * VN + (size_t)(part * S + sd) * n + pr];
+            }
+        }
+        grid_sync(ctl, trace);
+    }
 
-    // b. M = -W A_1 W (row planes in Mr): with it two coefficients per step,
+    // b. M = -W A_1 W (n x N, row planes in Mr): with it two coefficients per step,
     //      dx_j     = W r_j
     //      dx_{j+1} = W r'_{j+1} + M r_j,   r'_{j+1} = r_{j+1} before A_1 dx_j
     //    (r_{j+1} = r'_{j+1} - A_1 dx_j and dx_j = W r_j): half the dependent steps.
     if (D >= 2) {
-        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // P[:, c] = A_1 W[:, c]  (into Ec)
-            ts_stage<L>(Wc + (size_t)c * VEC, Wce + (size_t)c * 2 * n, n, false, xs, xe);
-            __syncthreads();
-            for (int base = r0; base < r1; base += gpb) {
-                const int p = base + gm;
-                const bool valid = p < r1;
-                const int pp = valid ? p : 0;
-                const size_t row = ((size_t)n + pp) * n;  // row p of A_1
-                ts_task<L>(Ad + row * 2 * S, Ae + row * 2, xs, xe, n, lgm, Gm, valid, DigRef{nullptr, nullptr, 0},
-                           false, DigOut{Ec + (size_t)c * VEC + pp, Ece + (size_t)c * 2 * n + pp, n}, nullptr, 0,
-                           scratch);
+        {
+            const ColSplit cs = col_split(N, N);
+            const int G = pick_group(cs.r1 - cs.r0, n, blockDim.x);
+            const int gpb = blockDim.x / G, g = threadIdx.x / G, lg = threadIdx.x % G;
+            for (int c = cs.c0; c < N; c += cs.cstep) {  // P[:, c] = A_1 W[:, c]  (N x N)
+                ts_stage<L>(Wc + (size_t)c * VN, Wce + (size_t)c * 2 * n, n, 0, xs, xe);
+                __syncthreads();
+                for (int base = cs.r0; base < cs.r1; base += gpb) {
+                    const int p = base + g;
+                    const bool valid = p < cs.r1;
+                    const int pp = valid ? p : 0;
+                    const size_t row = (size_t)N + pp;  // row p of A_1
+                    ts_task<L>(Ad + row * VN, Ae + row * 2 * n, xs, xe, n, lg, G, valid, none, false,
+                               DigOut{Pc + (size_t)c * VM + pp, Pce + (size_t)c * 2 * N + pp, N}, nullptr, 0, scratch);
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
         grid_sync(ctl, trace);
-        for (int c = mp_active ? cslot : n; c < n; c += ncb) {  // M[:, c] = -W P[:, c]  (columns into Wc)
-            ts_stage<L>(Ec + (size_t)c * VEC, Ece + (size_t)c * 2 * n, n, true, xs, xe);
-            __syncthreads();
-            for (int base = r0; base < r1; base += gpb) {
-                const int p = base + gm;
-                const bool valid = p < r1;
-                const int pp = valid ? p : 0;
-                ts_task<L>(Wr + (size_t)pp * n * 2 * S, Wre + (size_t)pp * n * 2, xs, xe, n, lgm, Gm, valid,
-                           DigRef{nullptr, nullptr, 0}, false,
-                           DigOut{Wc + (size_t)c * VEC + pp, Wce + (size_t)c * 2 * n + pp, n}, nullptr, 0, scratch);
+        {
+            const ColSplit cs = col_split(N, n);
+            const int G = pick_group(cs.r1 - cs.r0, N, blockDim.x);
+            const int gpb = blockDim.x / G, g = threadIdx.x / G, lg = threadIdx.x % G;
+            for (int c = cs.c0; c < N; c += cs.cstep) {  // M[:, c] = -W P[:, c]  (columns into Wc2)
+                ts_stage<L>(Pc + (size_t)c * VM, Pce + (size_t)c * 2 * N, N, 1, xs, xe);
+                __syncthreads();
+                for (int base = cs.r0; base < cs.r1; base += gpb) {
+                    const int p = base + g;
+                    const bool valid = p < cs.r1;
+                    const int pp = valid ? p : 0;
+                    ts_task<L>(Wr + (size_t)pp * VM, Wre + (size_t)pp * 2 * N, xs, xe, N, lg, G, valid, none, false,
+                               DigOut{Wc2 + (size_t)c * VN + pp, Wce2 + (size_t)c * 2 * n + pp, n}, nullptr, 0,
+                               scratch);
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
         grid_sync(ctl, trace);
-        for (size_t t = tid; t < (size_t)n * n; t += nth) {  // Mr (row planes) <- columns
-            const int p = (int)(t / n), c = (int)(t % n);
+        for (size_t t = tid; t < (size_t)n * N; t += nth) {  // Mr (row planes) <- columns
+            const int pr = (int)(t / N), c = (int)(t % N);
 #pragma unroll
             for (int part = 0; part < 2; part++) {
-                Mre[((size_t)p * 2 + part) * n + c] = Wce[((size_t)c * 2 + part) * n + p];
+                Mre[((size_t)pr * 2 + part) * N + c] = Wce2[((size_t)c * 2 + part) * n + pr];
 #pragma unroll
-                for (int s = 0; s < S; s++)
-                    Mr[(size_t)p * VEC + (size_t)(part * S + s) * n + c] =
-                        Wc[(size_t)c * VEC + (size_t)(part * S + s) * n + p];
+                for (int sd = 0; sd < S; sd++)
+                    Mr[(size_t)pr * VM + (size_t)(part * S + sd) * N + c] =
+                        Wc2[(size_t)c * VN + (size_t)(part * S + sd) * n + pr];
             }
         }
         grid_sync(ctl, trace);
     }
 
     // c. the substitution loop, two coefficients per step
-    double *Xp1 = Xp + VEC;
+    double *Xp1 = Xp + VN;
     int *Xe1 = Xe + 2 * n;
     for (int j = 0; j < D; j += 2) {
         const bool pair = j + 1 < D;
         {  // dx_j = W r_j ; dx_{j+1} = W r'_{j+1} + M r_j
-            ts_stage<L>(Rp + (size_t)j * VEC, Re + (size_t)j * 2 * n, n, false, xs, xe);
-            if (pair) ts_stage<L>(Rp + (size_t)(j + 1) * VEC, Re + (size_t)(j + 1) * 2 * n, n, false, xs1, xe1);
+            ts_stage<L>(Rp + (size_t)j * VM, Re + (size_t)j * 2 * N, N, 0, xs, xe);
+            if (pair) ts_stage<L>(Rp + (size_t)(j + 1) * VM, Re + (size_t)(j + 1) * 2 * N, N, 0, xs1, xe1);
             __syncthreads();
             const int T = pair ? 2 * n : n;
-            const int G = pick_group(T, pair ? 2 * n : n, nth);
+            const int G = pick_group(T, pair ? 2 * N : N, nth);
             const int ng = nth / G, g = tid / G, lg = tid % G;
             for (int base = 0; base < T; base += ng) {
                 const int task = base + g;
                 const bool valid = task < T;
                 const int second = valid && task >= n;
                 const int pp = valid ? task - (second ? n : 0) : 0;
-                const double *wr = Wr + (size_t)pp * n * 2 * S;
-                const int *wre = Wre + (size_t)pp * n * 2;
+                const double *wr = Wr + (size_t)pp * VM;
+                const int *wre = Wre + (size_t)pp * 2 * N;
                 if (!second)
-                    ts_task<L>(wr, wre, xs, xe, n, lg, G, valid, DigRef{nullptr, nullptr, 0}, false,
-                               DigOut{Xp + pp, Xe + pp, n}, dx + (size_t)pp * 2 * L * D + j, D, scratch);
+                    ts_task<L>(wr, wre, xs, xe, N, lg, G, valid, none, false, DigOut{Xp + pp, Xe + pp, n},
+                               dx + (size_t)pp * 2 * L * D + j, D, scratch);
                 else
-                    ts_task<L>(wr, wre, xs1, xe1, n, lg, G, valid, DigRef{nullptr, nullptr, 0}, false,
-                               DigOut{Xp1 + pp, Xe1 + pp, n}, dx + (size_t)pp * 2 * L * D + j + 1, D, scratch,
-                               Seg{Mr + (size_t)pp * n * 2 * S, Mre + (size_t)pp * n * 2, xs, xe});
+                    ts_task<L>(wr, wre, xs1, xe1, N, lg, G, valid, none, false, DigOut{Xp1 + pp, Xe1 + pp, n},
+                               dx + (size_t)pp * 2 * L * D + j + 1, D, scratch,
+                               Seg{Mr + (size_t)pp * VM, Mre + (size_t)pp * 2 * N, xs, xe});
             }
         }
         grid_sync(ctl, trace);
         if (j + 2 >= D) break;
         {  // r_k -= A_{k-j} dx_j + A_{k-j-1} dx_{j+1}, k = j+2..d
-            ts_stage<L>(Xp, Xe, n, true, xs, xe);
-            ts_stage<L>(Xp1, Xe1, n, true, xs1, xe1);
+            ts_stage<L>(Xp, Xe, n, 1, xs, xe);
+            ts_stage<L>(Xp1, Xe1, n, 1, xs1, xe1);
             __syncthreads();
-            const int T = (D - 2 - j) * n;
+            const int T = (D - 2 - j) * N;
             const int G = pick_group(T, 2 * n, nth);
             const int ng = nth / G, g = tid / G, lg = tid % G;
             for (int base = 0; base < T; base += ng) {
                 const int task = base + g;
                 const bool valid = task < T;
-                const int k = j + 2 + (valid ? task / n : 0), p = valid ? task % n : 0;
-                const size_t row0 = ((size_t)(k - j) * n + p) * n, row1 = ((size_t)(k - j - 1) * n + p) * n;
-                double *rk = Rp + (size_t)k * VEC + p;
-                int *rke = Re + (size_t)k * 2 * n + p;
-                ts_task<L>(Ad + row0 * 2 * S, Ae + row0 * 2, xs, xe, n, lg, G, valid, DigRef{rk, rke, n}, false,
-                           DigOut{rk, rke, n}, nullptr, 0, scratch,
-                           Seg{Ad + row1 * 2 * S, Ae + row1 * 2, xs1, xe1});
+                const int k = j + 2 + (valid ? task / N : 0), p = valid ? task % N : 0;
+                const size_t row0 = (size_t)(k - j) * N + p, row1 = (size_t)(k - j - 1) * N + p;
+                double *rk = Rp + (size_t)k * VM + p;
+                int *rke = Re + (size_t)k * 2 * N + p;
+                ts_task<L>(Ad + row0 * VN, Ae + row0 * 2 * n, xs, xe, n, lg, G, valid, DigRef{rk, rke, N}, false,
+                           DigOut{rk, rke, N}, nullptr, 0, scratch, Seg{Ad + row1 * VN, Ae + row1 * 2 * n, xs1, xe1});
             }
         }
         grid_sync(ctl, trace);
@@ -711,12 +840,14 @@ __global__ void __launch_bounds__(128) ts_update_kernel(double *__restrict__ x, 
 using namespace mdps;
 
 struct mdps_solver {
-    int n = 0, D = 0, L = 0, S = 0;
+    int N = 0, n = 0, D = 0, L = 0, S = 0;  // N equations (rows) >= n unknowns
     int device = 0;
-    double *Ad = nullptr, *M = nullptr, *Wr = nullptr, *Wc = nullptr, *Ec = nullptr, *Rp = nullptr, *Xp = nullptr;
-    int *Ae = nullptr, *Wre = nullptr, *Wce = nullptr, *Ece = nullptr, *Re = nullptr, *Xe = nullptr;
-    double *Mr = nullptr;  // -W A_1 W, row planes
-    int *Mre = nullptr;
+    double *Ad = nullptr, *Ac = nullptr, *M = nullptr, *Wr = nullptr, *Wc = nullptr, *Wc2 = nullptr, *Er = nullptr,
+           *Pc = nullptr, *Mr = nullptr, *Rp = nullptr, *Xp = nullptr;
+    int *Ae = nullptr, *Ace = nullptr, *Wre = nullptr, *Wce = nullptr, *Wce2 = nullptr, *Ere = nullptr,
+        *Pce = nullptr, *Mre = nullptr, *Re = nullptr, *Xe = nullptr;
+    double *Gc = nullptr;  // least squares: A_0^H A_0, column planes
+    int *Gce = nullptr;
     int *piv = nullptr;
     ts::Ctl *ctl = nullptr;
     long long *trace = nullptr;
@@ -743,9 +874,9 @@ struct TsGeom {
         int dev = 0, sms = 0, per = 0;
         TS_TRY(cudaGetDevice(&dev), MDPS_ECUDA);
         TS_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), MDPS_ECUDA);
-        s->smem_main = ts::ts_main_smem(digits_for(L), s->n, ts::main_threads(L));
+        s->smem_main = ts::ts_main_smem(digits_for(L), s->N, ts::main_threads(L));
         if (s->smem_main > 227 * 1024) {
-            mdps_internal_set_error("mdps_solver_create: n too large for this limb count (two staged digit vectors "
+            mdps_internal_set_error("mdps_solver_create: N too large for this limb count (two staged digit vectors "
                                     "exceed 227 KB of shared memory)");
             return MDPS_EINVAL;
         }
@@ -767,21 +898,23 @@ struct TsGeom {
 template <int L>
 struct TsRun {
     static int run(mdps_solver *s, const double *J, const double *b, double *dx, int negate, cudaStream_t st) {
-        const int n = s->n, D = s->D;
-        const size_t total = (size_t)n * n * D + (size_t)n * D;
+        const int N = s->N, n = s->n, D = s->D;
+        const size_t total = (size_t)N * n * D + (size_t)N * D;
         const int pb = (int)std::min<size_t>((total + 127) / 128, 148 * 32);
         TS_TRY(cudaMemsetAsync(s->ctl, 0, sizeof(ts::Ctl), st), MDPS_ECUDA);
-        ts::ts_pack_kernel<L><<<pb, 128, 0, st>>>(J, b, s->Ad, s->Ae, s->Rp, s->Re, n, D, negate);
+        ts::ts_pack_kernel<L><<<pb, 128, 0, st>>>(J, b, s->Ad, s->Ae, s->Ac, s->Ace, s->Rp, s->Re, N, n, D, negate);
         TS_TRY(cudaGetLastError(), MDPS_ECUDA);
-        ts::ts_gj_kernel<L><<<1, ts::GJ_THREADS, 0, st>>>(J, s->M, s->piv, s->ctl, s->Wr, s->Wre, s->Wc, s->Wce, n,
-                                                          D);
+        ts::ts_gj_kernel<L><<<1, ts::GJ_THREADS, 0, st>>>(J, s->M, s->piv, s->ctl, s->Wr, s->Wre, s->Wc, s->Wce, N,
+                                                          n, D);
         TS_TRY(cudaGetLastError(), MDPS_ECUDA);
-        const double *Ad = s->Ad;
-        const int *Ae = s->Ae;
-        void *args[] = {(void *)&Ad,     (void *)&Ae,     (void *)&s->Wr,  (void *)&s->Wre, (void *)&s->Wc,
-                        (void *)&s->Wce, (void *)&s->Ec,  (void *)&s->Ece, (void *)&s->Mr,  (void *)&s->Mre,
-                        (void *)&s->Rp,  (void *)&s->Re,  (void *)&s->Xp,  (void *)&s->Xe,  (void *)&dx,
-                        (void *)&s->n,   (void *)&s->D,   (void *)&s->ctl, (void *)&s->trace};
+        const double *Ad = s->Ad, *Ac = s->Ac;
+        const int *Ae = s->Ae, *Ace = s->Ace;
+        void *args[] = {(void *)&Ad,     (void *)&Ae,    (void *)&Ac,    (void *)&Ace,    (void *)&s->Wr,
+                        (void *)&s->Wre, (void *)&s->Wc, (void *)&s->Wce, (void *)&s->Wc2, (void *)&s->Wce2,
+                        (void *)&s->Er,  (void *)&s->Ere, (void *)&s->Pc, (void *)&s->Pce, (void *)&s->Mr,
+                        (void *)&s->Mre, (void *)&s->Rp, (void *)&s->Re, (void *)&s->Xp,  (void *)&s->Xe,
+                        (void *)&dx,     (void *)&s->Gc, (void *)&s->Gce, (void *)&s->N,  (void *)&s->n,
+                        (void *)&s->D,   (void *)&s->ctl, (void *)&s->trace};
         TS_TRY(cudaLaunchCooperativeKernel((const void *)ts::ts_main_kernel<L>, dim3(s->grid_main),
                                            dim3(ts::main_threads(L)), args, s->smem_main, st),
                MDPS_ECUDA);
@@ -808,16 +941,17 @@ static void solver_free(mdps_solver *s) {
     cudaFree(s->nj);
     cudaFree(s->ndx);
     cudaFree(s->nnorm);
-    void *ptrs[] = {s->Ad, s->Ae, s->M,  s->Wr, s->Wre, s->Wc, s->Wce, s->Ec,
-                    s->Ece, s->Rp, s->Re, s->Xp, s->Xe,  s->piv, s->ctl, s->trace, s->Mr, s->Mre};
+    void *ptrs[] = {s->Ad, s->Ae,  s->Ac,  s->Ace, s->M,  s->Wr, s->Wre, s->Wc,  s->Wce, s->Wc2, s->Wce2, s->Er,
+                    s->Ere, s->Pc, s->Pce, s->Mr, s->Mre, s->Rp, s->Re, s->Xp, s->Xe, s->piv, s->ctl, s->trace,
+                    s->Gc, s->Gce};
     for (void *p : ptrs) cudaFree(p);
 }
 
-extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t limbs) {
-    if (n < 1 || n > 256 || degree < 0 || degree > 255 ||
+extern "C" mdps_solver *mdps_solver_create_ls(int32_t N, int32_t n, int32_t degree, int32_t limbs) {
+    if (n < 1 || n > 256 || N < n || N > 256 || degree < 0 || degree > 255 ||
         !(limbs == 2 || limbs == 3 || limbs == 4 || limbs == 5 || limbs == 8 || limbs == 10)) {
         mdps_internal_set_error(
-            "mdps_solver_create: need 1 <= n <= 256, 0 <= degree <= 255, limbs in {2,3,4,5,8,10}");
+            "mdps_solver_create: need 1 <= n <= N <= 256, 0 <= degree <= 255, limbs in {2,3,4,5,8,10}");
         return nullptr;
     }
     mdps_solver *s = new (std::nothrow) mdps_solver();
@@ -825,22 +959,35 @@ extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t li
         mdps_internal_set_error("out of host memory");
         return nullptr;
     }
+    s->N = N;
     s->n = n;
     s->D = degree + 1;
     s->L = limbs;
     s->S = digits_for(limbs);
     cudaGetDevice(&s->device);
-    const size_t nn = (size_t)n * n, D = s->D, S = s->S, VEC = 2 * S * n;
-    const size_t sz[] = {nn * D * 2 * S * 8, nn * D * 2 * 4, nn * 4 * 8,  // Ad, Ae, M ([n][2n] complex)
-                         nn * 2 * S * 8,     nn * 2 * 4,     n * VEC * 8,  // Wr, Wre, Wc
-                         nn * 2 * 4,         n * VEC * 8,    nn * 2 * 4,   // Wce, Ec, Ece
-                         D * VEC * 8,        D * 2 * n * 4,  2 * VEC * 8,  // Rp, Re, Xp (two vectors)
-                         4 * (size_t)n * 4,  n * sizeof(int), sizeof(ts::Ctl),  // Xe, piv, ctl
-                         ts::TRACE_MAX * sizeof(long long), nn * 2 * S * 8, nn * 2 * 4};  // trace, Mr, Mre
-    void **ptrs[] = {(void **)&s->Ad, (void **)&s->Ae,  (void **)&s->M,  (void **)&s->Wr,  (void **)&s->Wre,
-                     (void **)&s->Wc, (void **)&s->Wce, (void **)&s->Ec, (void **)&s->Ece, (void **)&s->Rp,
-                     (void **)&s->Re, (void **)&s->Xp,  (void **)&s->Xe, (void **)&s->piv, (void **)&s->ctl,
-                     (void **)&s->trace, (void **)&s->Mr, (void **)&s->Mre};
+    const size_t D = s->D, S = s->S, VN = 2 * S * n, VM = 2 * S * N, Nn = (size_t)N * n;
+    const size_t sz[] = {
+        D * Nn * 2 * S * 8, D * Nn * 2 * 4,          // Ad, Ae: rows of A_k
+        Nn * 2 * S * 8,     Nn * 2 * 4,              // Ac, Ace: columns of A_0
+        (size_t)n * 2 * n * 2 * 8,                  // M: Gauss-Jordan [n][2n] complex
+        n * VM * 8,         (size_t)n * 2 * N * 4,   // Wr, Wre
+        N * VN * 8,         (size_t)N * 2 * n * 4,   // Wc, Wce
+        N * VN * 8,         (size_t)N * 2 * n * 4,   // Wc2, Wce2
+        n * VN * 8,         (size_t)n * 2 * n * 4,   // Er, Ere
+        N * VM * 8,         (size_t)N * 2 * N * 4,   // Pc, Pce
+        n * VM * 8,         (size_t)n * 2 * N * 4,   // Mr, Mre
+        D * VM * 8,         D * 2 * N * 4,           // Rp, Re
+        2 * VN * 8,         4 * (size_t)n * 4,       // Xp, Xe (two vectors)
+        n * sizeof(int),    sizeof(ts::Ctl),         // piv, ctl
+        ts::TRACE_MAX * sizeof(long long),           // trace
+        (size_t)n * VN * 8, (size_t)n * 2 * n * 4};  // Gc, Gce
+    void **ptrs[] = {(void **)&s->Ad,  (void **)&s->Ae,   (void **)&s->Ac,  (void **)&s->Ace, (void **)&s->M,
+                     (void **)&s->Wr,  (void **)&s->Wre,  (void **)&s->Wc,  (void **)&s->Wce, (void **)&s->Wc2,
+                     (void **)&s->Wce2, (void **)&s->Er,  (void **)&s->Ere, (void **)&s->Pc,  (void **)&s->Pce,
+                     (void **)&s->Mr,  (void **)&s->Mre,  (void **)&s->Rp,  (void **)&s->Re,  (void **)&s->Xp,
+                     (void **)&s->Xe,  (void **)&s->piv,  (void **)&s->ctl, (void **)&s->trace, (void **)&s->Gc,
+                     (void **)&s->Gce};
+    static_assert(sizeof(sz) / sizeof(sz[0]) == sizeof(ptrs) / sizeof(ptrs[0]), "buffer table");
     bool ok = true;
     for (size_t i = 0; i < sizeof(sz) / sizeof(sz[0]) && ok; i++) {
         ok = cudaMalloc(ptrs[i], sz[i]) == cudaSuccess;
@@ -863,6 +1010,10 @@ extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t li
     return s;
 }
 
+extern "C" mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t limbs) {
+    return mdps_solver_create_ls(n, n, degree, limbs);
+}
+
 int mdps_solve_internal(mdps_solver *s, const double *J, const double *b, double *dx, int negate,
                         cudaStream_t st) {
     if (!s || !J || !b || !dx) {
@@ -875,7 +1026,7 @@ int mdps_solve_internal(mdps_solver *s, const double *J, const double *b, double
         const char *a = (const char *)p;
         return a < x1 && x0 < a + bytes;
     };
-    if (overlaps(J, (size_t)s->n * s->n * ser * sizeof(double)) || overlaps(b, (size_t)s->n * ser * sizeof(double))) {
+    if (overlaps(J, (size_t)s->N * s->n * ser * sizeof(double)) || overlaps(b, (size_t)s->N * ser * sizeof(double))) {
         mdps_internal_set_error("mdps_solve: dx_out aliases an input");
         return MDPS_EINVAL;
     }
@@ -903,8 +1054,8 @@ extern "C" int mdps_solver_status(mdps_solver *s, int32_t *pivots, int32_t *sing
 }
 
 // Algorithmic work of one solve in complex md multiply-adds: the substitution
-// loop (d+1 products W r_j and n^2 d(d+1)/2 right-hand-side terms) plus one
-// Newton-Schulz step (2 n^3: I - A_0 W and W E).  FP64
+// loop (d+1 products W r_j and N n d(d+1)/2 right-hand-side terms) plus one
+// Newton-Schulz step (I - W A_0 and E W: 2 n^2 N).  FP64
 // instructions: 4 truncated S x S digit triangles per complex term.
 extern "C" int mdps_solver_stats(const mdps_solver *s, mdps_solver_info *out) {
     if (!s || !out) {
@@ -912,8 +1063,8 @@ extern "C" int mdps_solver_stats(const mdps_solver *s, mdps_solver_info *out) {
         return MDPS_EINVAL;
     }
     std::memset(out, 0, sizeof *out);
-    const int64_t n = s->n, D = s->D;
-    const int64_t loop = D * n * n + n * n * D * (D - 1) / 2, refine = 2 * n * n * n;
+    const int64_t N = s->N, n = s->n, D = s->D;
+    const int64_t loop = D * n * N + N * n * D * (D - 1) / 2, refine = n * n * N + n * N * n;
     out->complex_fma = loop + refine;
     out->fp64_ops = out->complex_fma * 4 * (int64_t)(s->S * (s->S + 1) / 2);
     out->launches = 3;
@@ -960,24 +1111,23 @@ extern "C" int mdps_newton_step(mdps_system *sys, mdps_solver *s, double *x, dou
         mdps_internal_set_error("mdps_newton_step: NULL argument");
         return MDPS_EINVAL;
     }
-    int sn = 0, sD = 0, sL = 0;
-    mdps_internal_system_shape(sys, &sn, &sD, &sL);
-    if (sn != s->n || sD != s->D || sL != s->L) {
-        mdps_internal_set_error("mdps_newton_step: system and solver differ in n, degree or limbs (or the system "
-                                "is not square)");
+    int sN = 0, sn = 0, sD = 0, sL = 0;
+    mdps_internal_system_shape(sys, &sN, &sn, &sD, &sL);
+    if (sN != s->N || sn != s->n || sD != s->D || sL != s->L) {
+        mdps_internal_set_error("mdps_newton_step: system and solver differ in N, n, degree or limbs");
         return MDPS_EINVAL;
     }
     const size_t ser = (size_t)2 * s->L * s->D;
     if (!s->nv) {
-        if (cudaMalloc(&s->nv, (size_t)s->n * ser * 8) != cudaSuccess ||
-            cudaMalloc(&s->nj, (size_t)s->n * s->n * ser * 8) != cudaSuccess ||
+        if (cudaMalloc(&s->nv, (size_t)s->N * ser * 8) != cudaSuccess ||
+            cudaMalloc(&s->nj, (size_t)s->N * s->n * ser * 8) != cudaSuccess ||
             cudaMalloc(&s->ndx, (size_t)s->n * ser * 8) != cudaSuccess ||
             cudaMalloc(&s->nnorm, sizeof(unsigned long long)) != cudaSuccess) {
             cudaGetLastError();
             mdps_internal_set_error("mdps_newton_step: device allocation failed");
             return MDPS_ENOMEM;
         }
-        s->bytes += (size_t)(2 * s->n + s->n * s->n) * ser * 8 + 8;
+        s->bytes += (size_t)(s->N + s->n + s->N * s->n) * ser * 8 + 8;
     }
     cudaStream_t cs = (cudaStream_t)stream;
     int rc = mdps_eval_diff(sys, x, s->nv, s->nj, stream);

@@ -77,3 +77,38 @@ def test_shape_mismatch_rejected(mdps):
     with mdps.System.from_inputs(si) as sys_, mdps.Solver(si.n, si.degree + 1, 2) as sol:
         with pytest.raises(mdps.MdpsError, match="differ"):
             sol.newton_step(sys_, cuda(si.x))
+
+
+@pytest.mark.parametrize("L", (2, 4, 8))
+def test_overdetermined_circle(mdps, L):
+    """The circle system plus the redundant equation f_0 + f_1 (N = 3 > n = 2):
+    Newton with least-squares steps still converges to (cos, sin)."""
+    import torch
+    from fractions import Fraction as Fr
+    from tests.test_oracle_evaldiff import const_series
+    si = circle_system(L)
+    D = si.D
+    s_coef = [Fr(c) for c in GOLD["s_coefficients"]]
+    # f2 = s(t) - y + x^2 + y^2 - 1
+    pp = np.concatenate([si.poly_ptr, [si.poly_ptr[-1] + 5]]).astype(np.int32)
+    mono_vars = [[], [(1, 1)], [(0, 2)], [(1, 2)], []]
+    mp, vv, ee = list(si.mono_ptr), list(si.vars), list(si.exps)
+    for mono in mono_vars:
+        for v, a in mono:
+            vv.append(v)
+            ee.append(a)
+        mp.append(len(vv))
+    coeffs = np.concatenate([si.coeffs, np.stack([const_series(s_coef, L, D), const_series([-1], L, D),
+                                                  const_series([1], L, D), const_series([1], L, D),
+                                                  const_series([-1], L, D)])])
+    sys_in = mdinputs.SystemInputs("circle3", 2, si.degree, L, pp, np.asarray(mp, np.int32),
+                                   np.asarray(vv, np.int32), np.asarray(ee, np.int32), coeffs, si.x)
+    with mdps.System.from_inputs(sys_in) as sys_, mdps.Solver(2, si.degree, L, n_eqs=3) as sol:
+        x = cuda(si.x)
+        steps, norm = sol.newton(sys_, x, 10, 1e-32)
+        torch.cuda.synchronize()
+        xg = x.cpu().numpy()
+    cos = [(Fr(c), Fr(0)) for c in GOLD["cos_coefficients"]]
+    sin = [(Fr(c), Fr(0)) for c in GOLD["s_coefficients"]]
+    assert series_err_exact(xg[0], cos) <= TOL[L]
+    assert series_err_exact(xg[1], sin) <= TOL[L]

@@ -129,3 +129,31 @@ def test_singular_flag(mdps):
     jac[:, 1, :, :, 0] = 0.0
     _, _, sing = gpu_solve(mdps, t, jac)
     assert sing
+
+
+@pytest.mark.parametrize("L", LEVELS)
+@pytest.mark.parametrize("N,n,degree", [(3, 2, 0), (5, 3, 4), (9, 4, 7), (12, 12, 3)])
+def test_least_squares_small(mdps, N, n, degree, L):
+    """N >= n: against the oracle's least-squares forward
+    substitution (normal equations formed exactly, reading R18)."""
+    import torch
+    t = mdinputs.random_toeplitz_rect(500 + 7 * N + n + degree, N, n, degree, L)
+    with mdps.Solver(n, degree, L, n_eqs=N) as s:
+        dx = s.solve(cuda(t.jac), cuda(t.rhs))
+        torch.cuda.synchronize()
+        dx = dx.cpu().numpy()
+    want = oracle.toeplitz_lstsq(t.jac, t.rhs, nthreads=NTHREADS)
+    err = oracle.series_err(dx, want)
+    assert err.max() <= TOL[L], err.max()
+
+
+def test_least_squares_config_shape(mdps):
+    """od-like limbs and degree, 2n x n."""
+    import torch
+    t = mdinputs.random_toeplitz_rect(77, 48, 24, 15, 8)
+    with mdps.Solver(24, 15, 8, n_eqs=48) as s:
+        dx = s.solve(cuda(t.jac), cuda(t.rhs))
+        torch.cuda.synchronize()
+        dx = dx.cpu().numpy()
+    want = oracle.toeplitz_lstsq(t.jac, t.rhs, nthreads=NTHREADS)
+    assert oracle.series_err(dx, want).max() <= TOL[8]
