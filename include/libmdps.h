@@ -68,6 +68,10 @@ typedef struct {
     int32_t algo;        /* MDPS_ALGO_* */
     int32_t use_graph;   /* 1: capture the launch sequence in a CUDA graph,
                             re-captured when the pointers or stream change */
+    int32_t real;        /* 1: a real system — every coefficient and input series
+                            has zero imaginary limbs (not checked); one real md
+                            product per term (1/4 of the complex work), and the
+                            imaginary limbs of values and Jacobian are 0 */
 } mdps_options;
 
 /* Create a system.  exponents: HOST [nnz] aligned with

@@ -249,6 +249,15 @@ def truncate(si: SystemInputs, degree: int, limbs: int, name: Optional[str] = No
                         np.ascontiguousarray(si.x[:, :, :limbs, :D]))
 
 
+def realify(si: SystemInputs, name: Optional[str] = None) -> SystemInputs:
+    """The same system with every imaginary limb set to 0 (a real system:
+    coefficients cos(theta), inputs cos(theta) with their lower limbs)."""
+    c, x = si.coeffs.copy(), si.x.copy()
+    c[:, 1] = 0.0
+    x[:, 1] = 0.0
+    return dataclasses.replace(si, name=name or f"{si.name}_real", coeffs=c, x=x)
+
+
 def sweep_cell(degree: int, limbs: int) -> SystemInputs:
     """One cell of config 4 (the precision sweep), derived from the fixed system."""
     assert degree in SWEEP_DEGREES and limbs in SWEEP_LIMBS

@@ -68,8 +68,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
         : "memory");
 }
 
-// one product pass over this thread's fold iterations
-template <int L, int DT>
+// one product pass over this thread's fold iterations.  REAL: real series
+// (imaginary parts zero and never read): one product per term.
+template <int L, int DT, bool REAL = false>
 __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, const double *__restrict__ sy,
                                               const int *__restrict__ ex, const int *__restrict__ ey, int Drt,
                                               int part, int t, int f, int F, int eacc1, int eacc2,
@@ -106,30 +107,30 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
 #pragma unroll
         for (int s = 0; s < S; s++) {
             Ur[s] = ux[s * D];
-            Ui[s] = __longlong_as_double(__double_as_longlong(ux[(S + s) * D]) ^ sgn);
+            Ui[s] = REAL ? 0.0 : __longlong_as_double(__double_as_longlong(ux[(S + s) * D]) ^ sgn);
         }
-        const int exr = ex[i], exi = ex[D + i];
-        const int ey1 = ey[w1part * D + kk], ey2 = ey[w2part * D + kk];
+        const int exr = ex[i], exi = REAL ? ZERO_E : ex[D + i];
+        const int ey1 = ey[w1part * D + kk], ey2 = REAL ? 0 : ey[w2part * D + kk];
         int d1 = eacc - exr - ey1, d2 = eacc - exi - ey2;
         if (exr + ey1 <= ZERO_E / 2) d1 = 0;  // zero product: any plane will do
-        if (exi + ey2 <= ZERO_E / 2) d2 = 0;
+        if (REAL || exi + ey2 <= ZERO_E / 2) d2 = 0;
         const bool fast = d1 <= PADZ && d2 <= PADZ;
         if (__all_sync(__activemask(), fast)) {
             const double *W1 = sy + (w1part * P2 + PADZ - d1) * D + kk;
             const double *W2 = sy + (w2part * P2 + PADZ - d2) * D + kk;
             // software pipelined: row l+1's two digits load while row l's FMAs run
-            double w1 = W1[0], w2 = W2[0];
+            double w1 = W1[0], w2 = REAL ? 0.0 : W2[0];
 #pragma unroll
             for (int l = 0; l < S; l++) {
                 double w1n = 0.0, w2n = 0.0;
                 if (l + 1 < S) {
                     w1n = W1[(l + 1) * D];
-                    w2n = W2[(l + 1) * D];
+                    if (!REAL) w2n = W2[(l + 1) * D];
                 }
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
-                    A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
+                    if (!REAL) A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
                 w1 = w1n;
                 w2 = w2n;
@@ -140,11 +141,11 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
 #pragma unroll
             for (int l = 0; l < S; l++) {
                 const double w1 = (l >= d1) ? W1[(PADZ + l - d1) * D] : 0.0;
-                const double w2 = (l >= d2) ? W2[(PADZ + l - d2) * D] : 0.0;
+                const double w2 = (!REAL && l >= d2) ? W2[(PADZ + l - d2) * D] : 0.0;
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
-                    A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
+                    if (!REAL) A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
             }
         }
@@ -219,10 +220,11 @@ __device__ __forceinline__ void conv_dig_emit_digits(const double (&A)[digits_fo
     ze[part * D + k] = e;
 }
 
-template <int L, int DT>
+template <int L, int DT, bool REAL = false>
 // register budget per SM: 4 blocks of 128 up to L = 4 (<= 128 registers),
 // 3 up to L = 8 (<= 170), 2 above; 256-thread blocks for D = 128 and the
-// generic-D build
+// generic-D build.  REAL: real systems (mdps_options.real): only the real
+// part is computed; the imaginary limbs of the limb outputs are written as 0.
 __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
                                   DT == 128 || DT == 0 ? 1 : (L <= 4 ? 4 : (L <= 8 ? 3 : 2)))
     conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
         const bool first = j <= t;
         const int i = first ? j : j - t - 1;
         const int kk = (first ? t : D - 1 - t) - i;
-        const int xr = ex[i], xi = ex[D + i], yr = ey[kk], yi = ey[D + kk];
+        const int xr = ex[i], xi = REAL ? ZERO_E : ex[D + i], yr = ey[kk], yi = REAL ? ZERO_E : ey[D + kk];
         const int er = max(xr + yr, xi + yi), ei = max(xr + yi, xi + yr);
         if (first) {
             ea1r = max(ea1r, er);
@@ -351,11 +353,18 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
         if (code & 2) zl = lpool + (size_t)(code >> 2) * 2 * L * D;
     }
     const int k1 = t, k2 = D - 1 - t;
+    if (REAL && zl) {  // real system: the imaginary limbs of the outputs are exactly 0
+        if (F == 1 || f < 2)
+            for (int p = 0; p < L; p++) {
+                if (F == 1 || f == 0) zl[(L + p) * D + k1] = 0.0;
+                if (F == 1 || f == 1) zl[(L + p) * D + k2] = 0.0;
+            }
+    }
 #pragma unroll 1
-    for (int part = 0; part < 2; part++) {
+    for (int part = 0; part < (REAL ? 1 : 2); part++) {
         double A[S];
         const int e1 = part ? ea1i : ea1r, e2 = part ? ea2i : ea2r;
-        conv_dig_pass<L, DT>(sx, sy, ex, ey, D, part, t, f, F, e1, e2, A, park);
+        conv_dig_pass<L, DT, REAL>(sx, sy, ex, ey, D, part, t, f, F, e1, e2, A, park);
         // k2: sum the F lanes' partials (exact) with shuffles; every lane has it
         for (int off = F >> 1; off > 0; off >>= 1) {
 #pragma unroll

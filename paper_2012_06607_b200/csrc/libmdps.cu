@@ -133,7 +133,8 @@ struct ConvEft {
 
 template <int L>
 struct ConvDig {
-    static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, cudaStream_t st) {
+    static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, int real,
+                   cudaStream_t st) {
         if (njobs <= 0) return MDPS_OK;
         // product kernel: 0 = two passes, one per part (conv_dig.cuh, default);
         // opt-in variants via MDPS_CONV_KERNEL: 1 = three products per term
@@ -142,7 +143,11 @@ struct ConvDig {
         static const int kind = getenv("MDPS_CONV_KERNEL") ? atoi(getenv("MDPS_CONV_KERNEL")) : 0;
         using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
         KernT kern;
-        if (kind == 1)
+        if (real)  // real systems: the two-pass kernel with one product per term
+            kern = D == 16 ? conv_dig_kernel<L, 16, true> : D == 32 ? conv_dig_kernel<L, 32, true>
+                 : D == 64 ? conv_dig_kernel<L, 64, true> : D == 128 ? conv_dig_kernel<L, 128, true>
+                 : conv_dig_kernel<L, 0, true>;
+        else if (kind == 1)
             kern = D == 16 ? conv_g_kernel<L, 16> : D == 32 ? conv_g_kernel<L, 32> : D == 64 ? conv_g_kernel<L, 64>
                  : D == 128 ? conv_g_kernel<L, 128> : conv_g_kernel<L, 0>;
         else if (kind == 2)
@@ -152,19 +157,20 @@ struct ConvDig {
             kern = D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> : D == 64 ? conv_dig_kernel<L, 64>
                  : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
         // geometry per D, computed once (benign race: every writer stores the same value)
-        static DigGeom cache[257];
-        static bool cached[257];
-        if (!cached[D]) {
+        static DigGeom cache[2 * 257];
+        static bool cached[2 * 257];
+        const int key = D + (real ? 257 : 0);
+        if (!cached[key]) {
             cudaFuncAttributes fa;
             int regs = 255, maxt = 128;
             if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
                 regs = fa.numRegs;
                 maxt = std::min(fa.maxThreadsPerBlock, 256);
             }
-            cache[D] = dig_geom(L, D, regs, maxt, kind);
-            cached[D] = true;
+            cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind);
+            cached[key] = true;
         }
-        const DigGeom g = cache[D];
+        const DigGeom g = cache[key];
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
         kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, lpool, jobs, njobs, D, g.T, g.F, g.P);
@@ -200,6 +206,7 @@ struct ToDigits {
 // ---------------------------------------------------------------------------
 struct mdps_system {
     int n = 0, N = 0, D = 0, L = 0, M = 0, algo = MDPS_ALGO_DIGITS, S = 0;  // n variables, N polynomials
+    int real = 0;  // mdps_options.real: every series real, one product per term
     int use_graph = 0;
     int64_t nslots = 0, products = 0, add_terms = 0;
     std::vector<int64_t> level_off, level_cnt;  // in jobs
@@ -299,7 +306,10 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
         return nullptr;
     }
     const int D = degree + 1;
+    const int real = opt ? (opt->real != 0) : 0;
+    if (real && algo == MDPS_ALGO_EFT) { set_err("real systems need the digits algorithm"); return nullptr; }
     if (algo == MDPS_ALGO_AUTO) algo = (D <= 128) ? MDPS_ALGO_DIGITS : MDPS_ALGO_EFT;
+    if (real && algo != MDPS_ALGO_DIGITS) { set_err("real systems need degree <= 127"); return nullptr; }
     if (algo == MDPS_ALGO_DIGITS && D > 128) { set_err("the digits algorithm supports degree <= 127"); return nullptr; }
 
     Schedule S;
@@ -320,6 +330,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->algo = algo;
     s->S = algo == MDPS_ALGO_DIGITS ? digits_for(limbs) : 0;
     s->use_graph = opt ? opt->use_graph : 0;
+    s->real = real;
     s->nslots = S.nslots;
     s->products = S.products;
     s->add_terms = (int64_t)S.ent_slot.size();
@@ -432,7 +443,7 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
     for (size_t lv = 0; lv < s->level_cnt.size(); lv++) {
         TimedGroup tg(s, st, 0);
         rc = dispatch_L<ConvDig>(L, s->pool, s->epool, s->lpool, (const int *)(s->jobs + 4 * s->level_off[lv]),
-                                 (int)s->level_cnt[lv], D, st);
+                                 (int)s->level_cnt[lv], D, s->real, st);
         if (rc) return rc;
     }
     // the addition jobs read the limb pool (the product jobs wrote limbs for
@@ -563,7 +574,7 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     memset(out, 0, sizeof *out);
     out->products = s->products;
     out->add_terms = s->add_terms;
-    out->fp64_ops_conv = s->products * conv_ops_per_product(s->algo, s->L, s->D);
+    out->fp64_ops_conv = s->products * conv_ops_per_product(s->algo, s->L, s->D) / (s->real ? 4 : 1);
     int64_t add_ops;
     if (s->algo == MDPS_ALGO_EFT)
         add_ops = s->add_terms * s->D * 2 * ops_bins_add(s->L);
@@ -704,7 +715,7 @@ struct SeriesMulDig {
             cudaMemcpyAsync(jobs, hj.data(), hj.size() * 4, cudaMemcpyHostToDevice, st);
             rc = ToDigits<L>::run(x, count, D, dp, ep, 0, st);
             if (!rc) rc = ToDigits<L>::run(y, count, D, dp, ep, count, st);
-            if (!rc) rc = ConvDig<L>::run(dp, ep, z, jobs, count, D, st);
+            if (!rc) rc = ConvDig<L>::run(dp, ep, z, jobs, count, D, 0, st);
             if (!rc && cudaStreamSynchronize(st) != cudaSuccess) {
                 set_err("series_mul kernel failed");
                 rc = MDPS_ECUDA;
