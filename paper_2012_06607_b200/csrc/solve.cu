@@ -39,6 +39,8 @@
 #include <new>
 #include <string>
 
+#include <cooperative_groups.h>
+
 #include "../../include/libmdps.h"
 #include "conv_dig.cuh"
 
@@ -274,6 +276,180 @@ __global__ void __launch_bounds__(GJ_THREADS) ts_gj_kernel(const double *__restr
             for (int s = 0; s < S; s++) {
                 Wr[(((size_t)p * 2 + part) * S + s) * n + q] = d[s];
                 Wc[(((size_t)q * 2 + part) * S + s) * n + p] = d[s];
+            }
+        }
+    }
+}
+
+// The same Gauss-Jordan on a thread-block cluster: the rows of [left | I] are
+// distributed over the C CTAs' shared memory; the pivot candidates, the row
+// swap and the pivot row travel through distributed shared memory (DSMEM),
+// phases are separated by cluster barriers (hardware, ~0.2 us) instead of
+// L2 round trips — n dependent steps at DSMEM latency rather than one SM's
+// L2 bandwidth.
+constexpr int GJC_THREADS = 512;
+
+__device__ __forceinline__ void gj_argmax_merge(double &bm, int &bi, double m2, int i2) {
+    if (m2 > bm || (m2 == bm && i2 < bi)) {
+        bm = m2;
+        bi = i2;
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(GJC_THREADS) ts_gj_cluster_kernel(const double *__restrict__ J,
+                                                                    int *__restrict__ piv, Ctl *ctl,
+                                                                    double *__restrict__ Wr, int *__restrict__ Wre,
+                                                                    double *__restrict__ Wc, int *__restrict__ Wce,
+                                                                    int N, int n, int D, int rows_per) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    constexpr int S = digits_for(L);
+    const int rank = (int)cluster.block_rank();
+    const int tx = threadIdx.x, nt = blockDim.x, lane = tx & 31, warp = tx >> 5;
+    const int W2 = 2 * n;
+    extern __shared__ __align__(16) double smraw[];
+    double2 *Mloc = reinterpret_cast<double2 *>(smraw);    // [rows_per][W2]
+    double2 *rowk = Mloc + (size_t)rows_per * W2;           // [W2] swap / pivot-row buffer
+    double *slot_m = reinterpret_cast<double *>(rowk + W2);  // this CTA's pivot candidate
+    int *slot_i = reinterpret_cast<int *>(slot_m + 1);
+    __shared__ double s_m[32];
+    __shared__ int s_i[32];
+    __shared__ int s_p;
+    __shared__ double s_inv[2];
+    const int r0 = rank * rows_per, r1 = min(n, r0 + rows_per);
+    auto a0 = [&](int r, int c) {
+        const double *src = J + ((size_t)r * n + c) * 2 * L * D;
+        return make_double2(src[0], src[(size_t)L * D]);
+    };
+    for (int t = tx; t < (r1 - r0) * W2; t += nt) {
+        const int i = r0 + t / W2, c = t % W2;
+        double2 v;
+        if (c >= n) {
+            v = make_double2(c - n == i ? 1.0 : 0.0, 0.0);
+        } else if (N == n) {
+            v = a0(i, c);
+        } else {
+            double re = 0.0, im = 0.0;
+            for (int r = 0; r < N; r++) {
+                const double2 x = a0(r, i), y = a0(r, c);
+                re = __fma_rn(x.x, y.x, __fma_rn(x.y, y.y, re));
+                im = __fma_rn(x.x, y.y, __fma_rn(-x.y, y.x, im));
+            }
+            v = make_double2(re, im);
+        }
+        Mloc[t] = v;
+    }
+    bool singular = false;
+    cluster.sync();
+    for (int k = 0; k < n; k++) {
+        double bm = -1.0;
+        int bi = n;
+        for (int i = max(k, r0) + tx; i < r1; i += nt) {
+            const double2 a = Mloc[(size_t)(i - r0) * W2 + k];
+            gj_argmax_merge(bm, bi, __dadd_rn(fabs(a.x), fabs(a.y)), i);
+        }
+        for (int off = 16; off > 0; off >>= 1)
+            gj_argmax_merge(bm, bi, __shfl_xor_sync(0xffffffffu, bm, off), __shfl_xor_sync(0xffffffffu, bi, off));
+        if (lane == 0) {
+            s_m[warp] = bm;
+            s_i[warp] = bi;
+        }
+        __syncthreads();
+        if (tx == 0) {
+            for (int w = 1; w < nt / 32; w++) gj_argmax_merge(bm, bi, s_m[w], s_i[w]);
+            *slot_m = bm;
+            *slot_i = bi;
+        }
+        cluster.sync();
+        if (tx == 0) {  // every CTA merges all candidates the same way
+            double m = -1.0;
+            int p = n;
+            for (int r = 0; r < (int)cluster.num_blocks(); r++)
+                gj_argmax_merge(m, p, *cluster.map_shared_rank(slot_m, r), *cluster.map_shared_rank(slot_i, r));
+            const bool sing = !(m > 0.0) || p >= n;
+            s_p = sing ? -1 - k : p;
+        }
+        __syncthreads();
+        const bool sing = s_p < 0;
+        const int p = sing ? k : s_p;
+        singular |= sing;
+        const int ok = k / rows_per, op = p / rows_per;
+        if (p != k) {  // swap rows k and p (through the owners' shared memory)
+            if (ok == op) {
+                if (rank == ok)
+                    for (int c = tx; c < W2; c += nt) {
+                        const double2 v = Mloc[(size_t)(k - r0) * W2 + c];
+                        Mloc[(size_t)(k - r0) * W2 + c] = Mloc[(size_t)(p - r0) * W2 + c];
+                        Mloc[(size_t)(p - r0) * W2 + c] = v;
+                    }
+                cluster.sync();
+            } else {
+                if (rank == ok) {
+                    const double2 *src = cluster.map_shared_rank(Mloc, op) + (size_t)(p - op * rows_per) * W2;
+                    for (int c = tx; c < W2; c += nt) rowk[c] = src[c];
+                } else if (rank == op) {
+                    const double2 *src = cluster.map_shared_rank(Mloc, ok) + (size_t)(k - ok * rows_per) * W2;
+                    for (int c = tx; c < W2; c += nt) rowk[c] = src[c];
+                }
+                cluster.sync();
+                if (rank == ok)
+                    for (int c = tx; c < W2; c += nt) Mloc[(size_t)(k - r0) * W2 + c] = rowk[c];
+                else if (rank == op)
+                    for (int c = tx; c < W2; c += nt) Mloc[(size_t)(p - r0) * W2 + c] = rowk[c];
+                cluster.sync();
+            }
+        }
+        if (rank == ok) {  // invert the pivot, scale row k
+            if (tx == 0) {
+                const double2 a = Mloc[(size_t)(k - r0) * W2 + k];
+                const double den = __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+                s_inv[0] = sing ? 0.0 : __ddiv_rn(a.x, den);
+                s_inv[1] = sing ? 0.0 : __ddiv_rn(-a.y, den);
+                piv[k] = p;
+            }
+            __syncthreads();
+            const double ir = s_inv[0], ii = s_inv[1];
+            for (int c = k + tx; c < W2; c += nt) {
+                const double2 v = Mloc[(size_t)(k - r0) * W2 + c];
+                Mloc[(size_t)(k - r0) * W2 + c] = make_double2(__dsub_rn(__dmul_rn(v.x, ir), __dmul_rn(v.y, ii)),
+                                                               __dadd_rn(__dmul_rn(v.x, ii), __dmul_rn(v.y, ir)));
+            }
+        }
+        cluster.sync();
+        {  // the scaled pivot row into every CTA
+            const double2 *src = cluster.map_shared_rank(Mloc, ok) + (size_t)(k - ok * rows_per) * W2;
+            for (int c = k + tx; c < W2; c += nt) rowk[c] = src[c];
+        }
+        __syncthreads();
+        const int cols = W2 - k - 1;
+        for (int t = tx; t < (r1 - r0) * cols; t += nt) {  // eliminate column k from the local rows i != k
+            const int li = t / cols, i = r0 + li;
+            if (i == k) continue;
+            const int c = k + 1 + (t - li * cols);
+            const double2 f = Mloc[(size_t)li * W2 + k], u = rowk[c], v = Mloc[(size_t)li * W2 + c];
+            Mloc[(size_t)li * W2 + c] =
+                make_double2(__dsub_rn(v.x, __dsub_rn(__dmul_rn(f.x, u.x), __dmul_rn(f.y, u.y))),
+                             __dsub_rn(v.y, __dadd_rn(__dmul_rn(f.x, u.y), __dmul_rn(f.y, u.x))));
+        }
+        cluster.sync();  // row k read by everyone before its owner changes it again
+    }
+    if (tx == 0 && rank == 0 && singular) atomicOr(&ctl->status, 1);
+    for (int t = tx; t < (r1 - r0) * n; t += nt) {  // the local rows of W_0 (or V_0) -> digits
+        const int p = r0 + t / n, q = t % n;
+        const double2 w = Mloc[(size_t)(p - r0) * W2 + n + q];
+#pragma unroll 1
+        for (int part = 0; part < 2; part++) {
+            double v[L], d[S];
+#pragma unroll
+            for (int l = 0; l < L; l++) v[l] = l == 0 ? (part ? w.y : w.x) : 0.0;
+            const int e = limbs_to_digits<L, S>(v, d);
+            Wre[((size_t)p * 2 + part) * n + q] = e;
+            Wce[((size_t)q * 2 + part) * n + p] = e;
+#pragma unroll
+            for (int sd = 0; sd < S; sd++) {
+                Wr[(((size_t)p * 2 + part) * S + sd) * n + q] = d[sd];
+                Wc[(((size_t)q * 2 + part) * S + sd) * n + p] = d[sd];
             }
         }
     }
@@ -855,6 +1031,8 @@ struct mdps_solver {
     unsigned long long *nnorm = nullptr;
     int grid_main = 0;
     size_t smem_main = 0;
+    int gj_cluster = 0, gj_rows = 0;  // cluster Gauss-Jordan: CTAs, rows per CTA (0: single-block kernel)
+    size_t gj_smem = 0;
     size_t bytes = 0;
     cudaStream_t last = nullptr;
 };
@@ -891,6 +1069,42 @@ struct TsGeom {
             return MDPS_ECUDA;
         }
         s->grid_main = sms * per;
+        // Gauss-Jordan on a cluster: C CTAs (8, or 16 non-portable) holding
+        // ceil(n / C) rows of [left | I] each; else the single-block kernel
+        const int C = s->n > 128 ? 16 : std::min(8, s->n);
+        const int rows = (s->n + C - 1) / C;
+        const size_t gsm = ((size_t)rows * 2 * s->n + 2 * s->n) * 16 + 16;
+        const char *env = getenv("MDPS_GJ_CLUSTER");
+        const bool want = !(env && env[0] == '0');
+        if (want && gsm <= 200 * 1024) {
+            bool ok = cudaFuncSetAttribute(ts::ts_gj_cluster_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)gsm) == cudaSuccess;
+            if (ok && C > 8)
+                ok = cudaFuncSetAttribute(ts::ts_gj_cluster_kernel<L>,
+                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+            if (ok) {
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(C);
+                cfg.blockDim = dim3(ts::GJC_THREADS);
+                cfg.dynamicSmemBytes = gsm;
+                cudaLaunchAttribute attr[1];
+                attr[0].id = cudaLaunchAttributeClusterDimension;
+                attr[0].val.clusterDim.x = C;
+                attr[0].val.clusterDim.y = 1;
+                attr[0].val.clusterDim.z = 1;
+                cfg.attrs = attr;
+                cfg.numAttrs = 1;
+                int nclusters = 0;
+                ok = cudaOccupancyMaxActiveClusters(&nclusters, ts::ts_gj_cluster_kernel<L>, &cfg) == cudaSuccess &&
+                     nclusters >= 1;
+            }
+            cudaGetLastError();
+            if (ok) {
+                s->gj_cluster = C;
+                s->gj_rows = rows;
+                s->gj_smem = gsm;
+            }
+        }
         return MDPS_OK;
     }
 };
@@ -904,9 +1118,27 @@ struct TsRun {
         TS_TRY(cudaMemsetAsync(s->ctl, 0, sizeof(ts::Ctl), st), MDPS_ECUDA);
         ts::ts_pack_kernel<L><<<pb, 128, 0, st>>>(J, b, s->Ad, s->Ae, s->Ac, s->Ace, s->Rp, s->Re, N, n, D, negate);
         TS_TRY(cudaGetLastError(), MDPS_ECUDA);
-        ts::ts_gj_kernel<L><<<1, ts::GJ_THREADS, 0, st>>>(J, s->M, s->piv, s->ctl, s->Wr, s->Wre, s->Wc, s->Wce, N,
-                                                          n, D);
-        TS_TRY(cudaGetLastError(), MDPS_ECUDA);
+        if (s->gj_cluster > 0) {  // Gauss-Jordan on a thread-block cluster (DSMEM)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(s->gj_cluster);
+            cfg.blockDim = dim3(ts::GJC_THREADS);
+            cfg.dynamicSmemBytes = s->gj_smem;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = s->gj_cluster;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            TS_TRY(cudaLaunchKernelEx(&cfg, ts::ts_gj_cluster_kernel<L>, J, s->piv, s->ctl, s->Wr, s->Wre, s->Wc,
+                                      s->Wce, N, n, D, s->gj_rows),
+                   MDPS_ECUDA);
+        } else {
+            ts::ts_gj_kernel<L><<<1, ts::GJ_THREADS, 0, st>>>(J, s->M, s->piv, s->ctl, s->Wr, s->Wre, s->Wc, s->Wce,
+                                                              N, n, D);
+            TS_TRY(cudaGetLastError(), MDPS_ECUDA);
+        }
         const double *Ad = s->Ad, *Ac = s->Ac;
         const int *Ae = s->Ae, *Ace = s->Ace;
         void *args[] = {(void *)&Ad,     (void *)&Ae,    (void *)&Ac,    (void *)&Ace,    (void *)&s->Wr,
