@@ -207,6 +207,21 @@ def bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal,
         t_newton = timed(lambda: sol.newton_step(sys_, xw), prep=lambda: xw.copy_(x))
         _, refine = sol.trace()
     achieved = info["fp64_ops"] / (t_solve * 1e-3)
+    # the real path (mdps_options.real) on the same system with its imaginary
+    # parts dropped: one product per term
+    real = None
+    try:
+        sr = mdinputs.realify(si)
+        with mdps.System.from_inputs(sr, real=True) as sysr:
+            xr = torch.from_numpy(sr.x).cuda()
+            vr, jr = torch.empty_like(vals), torch.empty_like(jac)
+            t_real = timed(lambda: sysr.eval_diff(xr, vr, jr))
+            str_ = sysr.stats()
+        real = {"ms": t_real, "value": str_["products"] / (t_real * 1e-3), "unit": "products/s",
+                "fp64_instr_per_s": str_["fp64_ops_total"] / (t_real * 1e-3),
+                "input": "the same system with every imaginary limb 0 (mdps_options.real)"}
+    except Exception as e:  # noqa: BLE001 - reported, not fatal
+        real = {"error": str(e)}
     # the oracle's forward substitution on a bounded sample of the same solve:
     # the first coefficients (dx_0..dx_dc depend only on A_0..A_dc, b_0..b_dc)
     cpu = None
@@ -235,6 +250,7 @@ def bench_next(mdps, torch, sys_, si, x, vals, jac, flush, stream, peak_nominal,
             "cpu_baseline": cpu},
         "newton_step": {"ms": t_newton, "of_which_eval_ms": None,
                         "api": "mdps_newton_step (eval/diff + solve + update)"},
+        "real_eval": real,
     }
 
 
