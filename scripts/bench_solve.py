@@ -48,11 +48,6 @@ def trace(name):
     J, b = torch.from_numpy(t.jac).cuda(), torch.from_numpy(t.rhs).cuda()
     s.solve(J, b)
     s.solve(J, b)
-    raw = (__import__("ctypes").c_int64 * 1024)()
-    st = __import__("ctypes").c_int32(0)
-    mdps.lib().mdps_solver_trace(s.handle, raw, 1024, __import__("ctypes").byref(st))
-    dbg = list(raw[899:912])
-    print("DBG", [round((x - dbg[0]) / 1e3, 2) for x in dbg])
     tr, steps = s.trace()
     tr = [x for x in tr[:200] if x >= 0][:2 * t.D + 3 * 8 + 2]
     d = [round((tr[i + 1] - tr[i]) / 1e3, 1) for i in range(len(tr) - 1)]
