@@ -460,11 +460,14 @@ __global__ void __launch_bounds__(GJC_THREADS) ts_gj_cluster_kernel(const double
 // in planes [2][S][n] read from global memory, x a digit vector staged in shared
 // memory as planes [part][PADZ + S][n] (PADZ zero planes for the alignment
 // shift).  One real part per pass, one DFMA per digit pair.
-template <int L>
+template <int L, int SE = digits_for(L)>
 __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, const int *__restrict__ aexp,
                                             const double *__restrict__ xs, const int *__restrict__ xe, int n,
                                             int q0, int G, int part, int eacc, double (&A)[digits_for(L)],
                                             bool zero = true) {
+    // SE <= S: the digit triangle is truncated at SE (only digit pairs with
+    // u + l < SE are formed) — products needed to fewer bits than the md
+    // precision (the early Newton-Schulz steps); the accumulator stays S wide
     constexpr int S = digits_for(L);
     constexpr int NORM = norm_every(S);
     constexpr int P2 = PADZ + S;
@@ -475,9 +478,9 @@ __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, con
     int cnt = 0;
     for (int q = q0; q < n; q += G) {
         const double *a = arow + q;
-        double Ur[S], Ui[S];
+        double Ur[SE], Ui[SE];
 #pragma unroll
-        for (int s = 0; s < S; s++) {
+        for (int s = 0; s < SE; s++) {
             Ur[s] = a[(size_t)s * n];
             Ui[s] = __longlong_as_double(__double_as_longlong(a[(size_t)(S + s) * n]) ^ sgn);
         }
@@ -492,14 +495,14 @@ __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, con
             const double *V1 = W1 + (size_t)(PADZ - d1) * n, *V2 = W2 + (size_t)(PADZ - d2) * n;
             double w1 = V1[0], w2 = V2[0];
 #pragma unroll
-            for (int l = 0; l < S; l++) {
+            for (int l = 0; l < SE; l++) {
                 double w1n = 0.0, w2n = 0.0;
-                if (l + 1 < S) {
+                if (l + 1 < SE) {
                     w1n = V1[(size_t)(l + 1) * n];
                     w2n = V2[(size_t)(l + 1) * n];
                 }
 #pragma unroll
-                for (int u = 0; u < S - l; u++) {
+                for (int u = 0; u < SE - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
                     A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
@@ -508,11 +511,11 @@ __device__ __forceinline__ void ts_dot_pass(const double *__restrict__ arow, con
             }
         } else {
 #pragma unroll
-            for (int l = 0; l < S; l++) {
+            for (int l = 0; l < SE; l++) {
                 const double w1 = (l >= d1) ? W1[(size_t)(PADZ + l - d1) * n] : 0.0;
                 const double w2 = (l >= d2) ? W2[(size_t)(PADZ + l - d2) * n] : 0.0;
 #pragma unroll
-                for (int u = 0; u < S - l; u++) {
+                for (int u = 0; u < SE - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
                     A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
@@ -579,7 +582,7 @@ struct Seg {
     const int *xe;
 };
 
-template <int L>
+template <int L, int SE = digits_for(L)>
 __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const int *__restrict__ aexp,
                                        const double *xs, const int *xe, int n, int lg, int G, bool valid,
                                        DigRef init, bool one, DigOut out, double *zl, int lstride,
@@ -622,8 +625,8 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
             for (int t = 0; t < S; t++) scratch[t] = __ldcg(src + (size_t)t * init.stride);
         }
         double A[S];
-        ts_dot_pass<L>(arow, aexp, xs, xe, valid ? n : 0, lg, G, part, eacc, A);
-        if (seg2.a) ts_dot_pass<L>(seg2.a, seg2.ae, seg2.xs, seg2.xe, valid ? n : 0, lg, G, part, eacc, A, false);
+        ts_dot_pass<L, SE>(arow, aexp, xs, xe, valid ? n : 0, lg, G, part, eacc, A);
+        if (seg2.a) ts_dot_pass<L, SE>(seg2.a, seg2.ae, seg2.xs, seg2.xe, valid ? n : 0, lg, G, part, eacc, A, false);
         if (valid && lg == 0) {
             if (init.d && eI > ZERO_E / 2) {  // digit s of the init value has weight R^(eI-1-s): slot s + eacc-1-eI
                 const int dI = eacc - 1 - eI;
@@ -657,6 +660,12 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
     }
     return eout;
 }
+
+template <int V>
+struct IC {
+    static constexpr int value = V;
+};
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 
 // lanes per task: as many as keep >= 4 terms per lane (G <= 32): the lanes of
 // a group read consecutive q of one row, so wide groups make every digit-plane
@@ -741,6 +750,10 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
     const int *RAe = lsq ? Gce : Ace;
     const size_t VR = (size_t)2 * S * RL;
     for (int it = 0; it < MAX_REFINE; it++) {
+        // digits kept in this step's products: step it squares an error of
+        // ~2^-(48 * 2^it) (double-precision start), so its products need about
+        // 2 * 48 * 2^it + 40 bits below the largest term: 8, 13, 21 digits, then S
+        const int se_level = it < 3 ? it : 3;
         if (threadIdx.x == 0) s_emax = ZERO_E;
         {
             const ColSplit cs = col_split(n, n);
@@ -753,9 +766,14 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
                     const int p = base + g;
                     const bool valid = p < cs.r1;
                     const int pp = valid ? p : 0;
-                    const int e = ts_task<L>(Wr + (size_t)pp * VR, Wre + (size_t)pp * 2 * RL, xs, xe, RL, lg, G, valid,
-                                             none, pp == c, DigOut{Er + (size_t)pp * VN + c, Ere + (size_t)pp * 2 * n + c, n},
-                                             nullptr, 0, scratch);
+                    auto task = [&](auto se) {
+                        return ts_task<L, decltype(se)::value>(
+                            Wr + (size_t)pp * VR, Wre + (size_t)pp * 2 * RL, xs, xe, RL, lg, G, valid, none, pp == c,
+                            DigOut{Er + (size_t)pp * VN + c, Ere + (size_t)pp * 2 * n + c, n}, nullptr, 0, scratch);
+                    };
+                    const int e = se_level == 0 ? task(IC<cmin(8, S)>{})
+                                : se_level == 1 ? task(IC<cmin(13, S)>{})
+                                : se_level == 2 ? task(IC<cmin(21, S)>{}) : task(IC<S>{});
                     if (valid && lg == 0) atomicMax(&s_emax, e);
                 }
                 __syncthreads();
@@ -778,10 +796,16 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
                     const int p = base + g;
                     const bool valid = p < cs.r1;
                     const int pp = valid ? p : 0;
-                    ts_task<L>(Er + (size_t)pp * VN, Ere + (size_t)pp * 2 * n, xs, xe, n, lg, G, valid,
-                               DigRef{Wc + (size_t)c * VN + pp, Wce + (size_t)c * 2 * n + pp, n}, false,
-                               DigOut{Wc2 + (size_t)c * VN + pp, Wce2 + (size_t)c * 2 * n + pp, n}, nullptr, 0,
-                               scratch);
+                    auto task = [&](auto se) {
+                        ts_task<L, decltype(se)::value>(
+                            Er + (size_t)pp * VN, Ere + (size_t)pp * 2 * n, xs, xe, n, lg, G, valid,
+                            DigRef{Wc + (size_t)c * VN + pp, Wce + (size_t)c * 2 * n + pp, n}, false,
+                            DigOut{Wc2 + (size_t)c * VN + pp, Wce2 + (size_t)c * 2 * n + pp, n}, nullptr, 0, scratch);
+                    };
+                    if (se_level == 0) task(IC<cmin(8, S)>{});
+                    else if (se_level == 1) task(IC<cmin(13, S)>{});
+                    else if (se_level == 2) task(IC<cmin(21, S)>{});
+                    else task(IC<S>{});
                 }
                 __syncthreads();
             }
