@@ -158,13 +158,12 @@ int mdps_system_level_jobs(const mdps_system *sys, int64_t *jobs_per_level, int3
  * ------------------------------------------------------------------------- */
 typedef struct mdps_solver mdps_solver; /* opaque; owns its device workspace */
 
-/* n in [1, 256], degree in [0, 255], limbs in {2,3,4,5,8,10}.  Allocates the
- * workspace (about 2x the Jacobian) on the current device.  NULL on error
- * (also when the shared-memory footprint of the solver kernel for this n and
- * limb count exceeds 227 KB: n > ~230 at 10 limbs). */
+/* n in [1, 128], degree in [0, 255], limbs in {2,3,4,5,8,10} (n <= 128 keeps
+ * every exact digit accumulation of the solver below 2^53).  Allocates the
+ * workspace (about 2x the Jacobian) on the current device.  NULL on error. */
 mdps_solver *mdps_solver_create(int32_t n, int32_t degree, int32_t limbs);
 
-/* A solver for N >= n equations in n unknowns (least squares):
+/* A solver for N >= n equations in n unknowns, N <= 128 (least squares):
  * each dx_j minimises |A_0 dx_j - r_j| with r_j = b_j - sum_{i>=1} A_i dx_{j-i};
  * the GPU applies A_0^+ (refined to md precision from the normal equations'
  * double-precision solution).  Then jacobian is [N][n][...], rhs [N][...] and

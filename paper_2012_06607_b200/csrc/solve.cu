@@ -1095,7 +1095,7 @@ struct TsGeom {
         s->grid_main = sms * per;
         // Gauss-Jordan on a cluster: C CTAs (8, or 16 non-portable) holding
         // ceil(n / C) rows of [left | I] each; else the single-block kernel
-        const int C = s->n > 128 ? 16 : std::min(8, s->n);
+        const int C = std::min(8, s->n);
         const int rows = (s->n + C - 1) / C;
         const size_t gsm = ((size_t)rows * 2 * s->n + 2 * s->n) * 16 + 16;
         const char *env = getenv("MDPS_GJ_CLUSTER");
@@ -1204,10 +1204,12 @@ static void solver_free(mdps_solver *s) {
 }
 
 extern "C" mdps_solver *mdps_solver_create_ls(int32_t N, int32_t n, int32_t degree, int32_t limbs) {
-    if (n < 1 || n > 256 || N < n || N > 256 || degree < 0 || degree > 255 ||
+    // N <= 128 keeps every exact digit accumulator below 2^53: a dot product
+    // has at most 2N terms (two segments), each < 2^44 units of the top digit
+    if (n < 1 || N < n || N > 128 || degree < 0 || degree > 255 ||
         !(limbs == 2 || limbs == 3 || limbs == 4 || limbs == 5 || limbs == 8 || limbs == 10)) {
         mdps_internal_set_error(
-            "mdps_solver_create: need 1 <= n <= N <= 256, 0 <= degree <= 255, limbs in {2,3,4,5,8,10}");
+            "mdps_solver_create: need 1 <= n <= N <= 128, 0 <= degree <= 255, limbs in {2,3,4,5,8,10}");
         return nullptr;
     }
     mdps_solver *s = new (std::nothrow) mdps_solver();

@@ -86,7 +86,7 @@ def test_product_path_has_no_oracle_or_fallback():
             assert "oracle" not in src.replace("CPU oracle (oracle/)", "").replace("oracle/)", ""), f
 
 
-@pytest.mark.parametrize("n,degree,limbs", [(0, 3, 2), (300, 3, 2), (4, -1, 2), (4, 300, 2), (4, 3, 7)])
+@pytest.mark.parametrize("n,degree,limbs", [(0, 3, 2), (129, 3, 2), (4, -1, 2), (4, 300, 2), (4, 3, 7)])
 def test_solver_create_rejects_invalid_arguments(lib, n, degree, limbs):
     with pytest.raises(mdps.MdpsError, match="mdps_solver_create"):
         mdps.Solver(n, degree, limbs)
