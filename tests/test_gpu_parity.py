@@ -244,3 +244,16 @@ def test_host_entry_point(mdps):
     with mdps.System.from_inputs(si) as s:
         v, j = s.eval_diff_host(si.x)
     assert np.array_equal(v, v0) and np.array_equal(j, j0)
+
+
+@pytest.mark.parametrize("name,nv,nj,seed", [("od", 3, 13, 11), ("deca", 1, 15, 12)])
+def test_config_wide_sample(mdps, name, nv, nj, seed):
+    """A wider sample of the full-size od and deca outputs (16 each, another
+    seed): one oracle worker per host core."""
+    si = mdinputs.make_config(name)
+    vals, jac, st = gpu_eval(si, 0)
+    sup = structural_support(si)
+    err, errs = check_against_oracle(si, vals, jac, sample_entries(si, nv, nj, seed=seed, sup=sup), TOL[si.limbs])
+    assert err <= TOL[si.limbs], err
+    # the error is far below the tolerance: report the margin in units of 2^-53L
+    assert err <= 2.0 ** (-53 * si.limbs) * 4096
