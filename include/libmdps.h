@@ -72,6 +72,11 @@ typedef struct {
                             has zero imaginary limbs (not checked); one real md
                             product per term (1/4 of the complex work), and the
                             imaginary limbs of values and Jacobian are 0 */
+    int32_t batch;       /* >= 1 (0 = 1): evaluate the system at `batch` points per
+                            call — series_in [batch][n][...], values_out
+                            [batch][N][...], jacobian_out [batch][N][n][...] —
+                            in one launch per level (small systems fill the GPU;
+                            mdps_newton_step needs batch = 1) */
 } mdps_options;
 
 /* Create a system.  exponents: HOST [nnz] aligned with

@@ -49,7 +49,8 @@ class _Supports(ctypes.Structure):
 
 
 class _Options(ctypes.Structure):
-    _fields_ = [("algo", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("real", ctypes.c_int32)]
+    _fields_ = [("algo", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("real", ctypes.c_int32),
+                ("batch", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -163,12 +164,13 @@ def _dptr(t) -> int:
 
 
 def mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n: int, degree: int,
-                       limbs: int, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False) -> int:
+                       limbs: int, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False,
+                       batch: int = 1) -> int:
     """Create a system; returns the opaque handle (int).  Host numpy inputs."""
     pp, mp, vv, ee = _i32(poly_ptr), _i32(mono_ptr), _i32(vars_), _i32(exponents)
     coeffs = np.ascontiguousarray(np.asarray(coefficients, dtype=np.float64))
     sup = _Supports(len(pp) - 1, _ptr_i32(pp), _ptr_i32(mp), _ptr_i32(vv))
-    opts = _Options(algo, 1 if use_graph else 0, 1 if real else 0)
+    opts = _Options(algo, 1 if use_graph else 0, 1 if real else 0, int(batch))
     h = lib().mdps_system_create_ex(ctypes.byref(sup), _ptr_i32(ee),
                                     coeffs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                     n, degree, limbs, ctypes.byref(opts))
@@ -208,17 +210,19 @@ class System:
     """RAII wrapper: a polynomial system on the device (see libmdps.h)."""
 
     def __init__(self, poly_ptr, mono_ptr, vars_, exponents, coefficients, n, degree, limbs,
-                 algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False):
+                 algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False, batch: int = 1):
         self.n, self.degree, self.limbs = int(n), int(degree), int(limbs)
         self.n_polys = int(len(poly_ptr) - 1)
+        self.batch = int(batch)
         self.handle = mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n,
-                                         degree, limbs, algo, use_graph, real)
+                                         degree, limbs, algo, use_graph, real, batch)
 
     @classmethod
-    def from_inputs(cls, si, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False) -> "System":
+    def from_inputs(cls, si, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False,
+                    batch: int = 1) -> "System":
         """From an mdinputs.SystemInputs-like object (poly_ptr, mono_ptr, vars, exps, coeffs)."""
         return cls(si.poly_ptr, si.mono_ptr, si.vars, si.exps, si.coeffs, si.n, si.degree, si.limbs,
-                   algo, use_graph, real)
+                   algo, use_graph, real, batch)
 
     @property
     def series_shape(self):
@@ -226,18 +230,20 @@ class System:
 
     def eval_diff(self, series_in, values_out=None, jacobian_out=None, stream=None):
         import torch
+        lead = (self.batch,) if self.batch > 1 else ()
         if values_out is None:
-            values_out = torch.empty((self.n_polys,) + self.series_shape, dtype=torch.float64,
+            values_out = torch.empty(lead + (self.n_polys,) + self.series_shape, dtype=torch.float64,
                                      device=series_in.device)
         if jacobian_out is None:
-            jacobian_out = torch.empty((self.n_polys, self.n) + self.series_shape, dtype=torch.float64,
+            jacobian_out = torch.empty(lead + (self.n_polys, self.n) + self.series_shape, dtype=torch.float64,
                                        device=series_in.device)
         mdps_eval_diff(self.handle, series_in, values_out, jacobian_out, stream)
         return values_out, jacobian_out
 
     def eval_diff_host(self, series_in: np.ndarray, stream=None):
-        vals = np.empty((self.n_polys,) + self.series_shape)
-        jac = np.empty((self.n_polys, self.n) + self.series_shape)
+        lead = (self.batch,) if self.batch > 1 else ()
+        vals = np.empty(lead + (self.n_polys,) + self.series_shape)
+        jac = np.empty(lead + (self.n_polys, self.n) + self.series_shape)
         mdps_eval_diff_host(self.handle, np.ascontiguousarray(series_in, dtype=np.float64), vals, jac, stream)
         return vals, jac
 

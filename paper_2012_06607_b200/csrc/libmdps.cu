@@ -207,6 +207,7 @@ struct ToDigits {
 struct mdps_system {
     int n = 0, N = 0, D = 0, L = 0, M = 0, algo = MDPS_ALGO_DIGITS, S = 0;  // n variables, N polynomials
     int real = 0;  // mdps_options.real: every series real, one product per term
+    int batch = 1; // mdps_options.batch: points per evaluation (n, N are per point)
     int use_graph = 0;
     int64_t nslots = 0, products = 0, add_terms = 0;
     std::vector<int64_t> level_off, level_cnt;  // in jobs
@@ -319,6 +320,14 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
         return nullptr;
     }
     if (S.M > 0 && !coefficients) { set_err("NULL coefficients"); return nullptr; }
+    const int B = opt && opt->batch > 1 ? opt->batch : 1;
+    if (opt && opt->batch < 0) { set_err("batch must be >= 1"); return nullptr; }
+    const std::vector<int32_t> limb_slot1(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + S.M));
+    const int64_t nlimb1 = S.nlimb;
+    if (B > 1 && !replicate_schedule(S, n, B, err)) {
+        set_err(err);
+        return nullptr;
+    }
 
     mdps_system *s = new (std::nothrow) mdps_system();
     if (!s) { set_err("host allocation failed"); return nullptr; }
@@ -331,10 +340,11 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->S = algo == MDPS_ALGO_DIGITS ? digits_for(limbs) : 0;
     s->use_graph = opt ? opt->use_graph : 0;
     s->real = real;
+    s->batch = B;
     s->nslots = S.nslots;
     s->products = S.products;
     s->add_terms = (int64_t)S.ent_slot.size();
-    s->ntasks = S.N + S.N * n;
+    s->ntasks = B * (S.N + S.N * n);
 
     std::vector<int32_t> alljobs;  // (in1, in2, out, code) per job, level by level
     for (auto &lv : S.levels4) {
@@ -365,24 +375,29 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
         // summed coefficient series (constant terms, m = 1 without common
         // factor) are copied once into the limb pool; summed inputs x_j (none
         // with the current DAG) are copied at every eval
+        // (one copy per point of a batch, each point with its own limb-pool block)
         for (int64_t slot = 0; ok && slot < (int64_t)n + S.M; slot++) {
-            const int32_t ls = S.limb_slot[(size_t)slot];
-            if (ls < 0) continue;
-            if (slot < n)
-                s->x_lslots.emplace_back((int32_t)slot, ls);
-            else
-                ok = up(s->lpool + (size_t)ls * limb_ser, coefficients + (size_t)(slot - n) * limb_ser, limb_ser * 8);
+            const int32_t ls1 = limb_slot1[(size_t)slot];
+            if (ls1 < 0) continue;
+            for (int b = 0; ok && b < B; b++) {
+                const int32_t ls = (int32_t)(ls1 + (int64_t)b * nlimb1);
+                if (slot < n)
+                    s->x_lslots.emplace_back((int32_t)((int64_t)b * n + slot), ls);
+                else
+                    ok = up(s->lpool + (size_t)ls * limb_ser, coefficients + (size_t)(slot - n) * limb_ser,
+                            limb_ser * 8);
+            }
         }
     }
     if (ok && S.M > 0) {
         if (algo == MDPS_ALGO_EFT) {
-            ok = up(s->pool + (size_t)n * ser, coefficients, (size_t)S.M * limb_ser * 8);
+            ok = up(s->pool + (size_t)B * n * ser, coefficients, (size_t)S.M * limb_ser * 8);
         } else {
             double *tmp = nullptr;
             ok = cudaMalloc((void **)&tmp, (size_t)S.M * limb_ser * 8) == cudaSuccess &&
                  up(tmp, coefficients, (size_t)S.M * limb_ser * 8);
             if (ok) {
-                const int rc = dispatch_L<ToDigits>(limbs, (const double *)tmp, S.M, D, s->pool, s->epool, n,
+                const int rc = dispatch_L<ToDigits>(limbs, (const double *)tmp, S.M, D, s->pool, s->epool, B * n,
                                                     (cudaStream_t)0);
                 ok = rc == MDPS_OK && cudaDeviceSynchronize() == cudaSuccess;
             }
@@ -412,7 +427,7 @@ extern "C" void mdps_system_destroy(mdps_system *s) {
 
 // the launch sequence of one eval (also what the CUDA graph captures)
 static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, cudaStream_t st) {
-    const int L = s->L, D = s->D, n = s->n;
+    const int L = s->L, D = s->D, n = s->n * s->batch;  // input series of all points
     int rc;
     if (s->timing) s->timed_evals++;
     if (s->algo == MDPS_ALGO_EFT) {
@@ -429,7 +444,8 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
         }
         TimedGroup tg(s, st, 1);
         return dispatch_L<AccumEft>(L, (const double *)s->pool, (const int *)s->task_ptr,
-                                    (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, s->N, D, vals, jac, st);
+                                    (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, s->N * s->batch, D, vals,
+                                    jac, st);
     }
     {
         TimedGroup tg(s, st, 2);
@@ -450,7 +466,7 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
     // exactly the series they sum)
     TimedGroup tg(s, st, 1);
     return dispatch_L<AccumEft>(L, (const double *)s->lpool, (const int *)s->task_ptr, (const int *)s->ent_lslot,
-                                (const int *)s->ent_w, s->ntasks, s->N, D, vals, jac, st);
+                                (const int *)s->ent_w, s->ntasks, s->N * s->batch, D, vals, jac, st);
 }
 
 extern "C" int mdps_system_set_timing(mdps_system *s, int32_t enable) {
@@ -495,7 +511,7 @@ extern "C" int mdps_eval_diff(mdps_system *s, const double *in, double *vals, do
         return MDPS_EINVAL;
     }
     const size_t ser = (size_t)2 * s->L * s->D * 8;
-    const size_t nin = ser * s->n, nval = ser * s->N, njac = ser * s->N * s->n;
+    const size_t nin = ser * s->n * s->batch, nval = ser * s->N * s->batch, njac = ser * s->N * s->n * s->batch;
     if (overlaps(in, nin, vals, nval) || overlaps(in, nin, jac, njac) || overlaps(vals, nval, jac, njac)) {
         set_err("outputs alias each other or the input");
         return MDPS_EINVAL;
@@ -534,16 +550,18 @@ extern "C" int mdps_eval_diff_host(mdps_system *s, const double *in_h, double *v
     }
     const size_t ser = (size_t)2 * s->L * s->D;
     if (!s->dev_in) {
-        if (!dalloc(s, &s->dev_in, ser * s->n) || !dalloc(s, &s->dev_vals, ser * s->N) ||
-            !dalloc(s, &s->dev_jac, ser * s->N * s->n))
+        if (!dalloc(s, &s->dev_in, ser * s->n * s->batch) || !dalloc(s, &s->dev_vals, ser * s->N * s->batch) ||
+            !dalloc(s, &s->dev_jac, ser * s->N * s->n * s->batch))
             return MDPS_ENOMEM;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(cudaMemcpyAsync(s->dev_in, in_h, ser * s->n * 8, cudaMemcpyHostToDevice, st), MDPS_ECUDA);
+    CUDA_TRY(cudaMemcpyAsync(s->dev_in, in_h, ser * s->n * s->batch * 8, cudaMemcpyHostToDevice, st), MDPS_ECUDA);
     int rc = mdps_eval_diff(s, s->dev_in, s->dev_vals, s->dev_jac, stream);
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(vals_h, s->dev_vals, ser * s->N * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
-    CUDA_TRY(cudaMemcpyAsync(jac_h, s->dev_jac, ser * s->N * s->n * 8, cudaMemcpyDeviceToHost, st), MDPS_ECUDA);
+    CUDA_TRY(cudaMemcpyAsync(vals_h, s->dev_vals, ser * s->N * s->batch * 8, cudaMemcpyDeviceToHost, st),
+             MDPS_ECUDA);
+    CUDA_TRY(cudaMemcpyAsync(jac_h, s->dev_jac, ser * s->N * s->n * s->batch * 8, cudaMemcpyDeviceToHost, st),
+             MDPS_ECUDA);
     CUDA_TRY(cudaStreamSynchronize(st), MDPS_ECUDA);
     return MDPS_OK;
 }
@@ -559,7 +577,7 @@ static int64_t conv_ops_per_product(int algo, int L, int D) {
 // shape of a system for solve.cu (the Newton step checks it against the solver)
 int mdps_internal_system_shape(const mdps_system *s, int *N, int *n, int *D, int *L) {
     if (!s) return MDPS_EINVAL;
-    *N = s->N;
+    *N = s->batch == 1 ? s->N : -1;  // the Newton step works on one point
     *n = s->n;
     *D = s->D;
     *L = s->L;
@@ -582,7 +600,7 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
         add_ops = s->add_terms * s->D * 2 * (digits_for(s->L) + 1);
     out->fp64_ops_total = out->fp64_ops_conv + add_ops;
     const int64_t ser = (int64_t)2 * s->L * s->D * 8;
-    out->compulsory_bytes = ser * ((int64_t)s->n + s->M + s->N + (int64_t)s->N * s->n);
+    out->compulsory_bytes = ser * (((int64_t)s->n + s->N + (int64_t)s->N * s->n) * s->batch + s->M);
     out->levels = (int32_t)s->level_cnt.size();
     out->algo = s->algo;
     out->digits = s->S;

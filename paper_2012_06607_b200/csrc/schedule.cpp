@@ -153,4 +153,61 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
     return true;
 }
 
+bool replicate_schedule(Schedule &S, int32_t n, int32_t B, std::string &err) {
+    const int64_t M = S.M, J = S.nslots - n - M, nl = S.nlimb;
+    const int64_t total = (int64_t)B * n + M + (int64_t)B * J;
+    if (total > INT32_MAX / 4) { err = "batch too large (slots overflow int32)"; return false; }
+    if ((int64_t)B * nl >= (1LL << 29)) { err = "batch too large (limb slots overflow the job code)"; return false; }
+    const int64_t ntasks0 = (int64_t)S.N + (int64_t)S.N * n;
+    if ((int64_t)B * ntasks0 + 1 > INT32_MAX || (int64_t)B * (int64_t)S.ent_slot.size() > INT32_MAX) {
+        err = "batch too large (addition jobs overflow int32)";
+        return false;
+    }
+    auto map = [&](int32_t slot, int32_t b) -> int32_t {
+        if (slot < n) return (int32_t)((int64_t)b * n + slot);
+        if (slot < n + M) return (int32_t)((int64_t)B * n + (slot - n));
+        return (int32_t)((int64_t)B * n + M + (int64_t)b * J + (slot - n - M));
+    };
+    std::vector<std::vector<int32_t>> lv4;
+    for (auto &lv : S.levels4) {
+        std::vector<int32_t> v;
+        v.reserve(lv.size() * (size_t)B);
+        for (int32_t b = 0; b < B; b++)
+            for (size_t q = 0; q < lv.size(); q += 4) {
+                v.push_back(map(lv[q], b));
+                v.push_back(map(lv[q + 1], b));
+                v.push_back(map(lv[q + 2], b));
+                int32_t code = lv[q + 3];
+                if (code & 2) code = (int32_t)((((int64_t)(code >> 2) + (int64_t)b * nl) << 2) | (code & 3));
+                v.push_back(code);
+            }
+        lv4.push_back(std::move(v));
+    }
+    std::vector<int32_t> tp{0}, es, ew, el;
+    auto copy_task = [&](int64_t t, int32_t b) {
+        for (int32_t e = S.task_ptr[(size_t)t]; e < S.task_ptr[(size_t)t + 1]; e++) {
+            es.push_back(map(S.ent_slot[(size_t)e], b));
+            ew.push_back(S.ent_w[(size_t)e]);
+            el.push_back(S.ent_lslot.empty() ? -1 : (int32_t)(S.ent_lslot[(size_t)e] + (int64_t)b * nl));
+        }
+        tp.push_back((int32_t)es.size());
+    };
+    for (int32_t b = 0; b < B; b++)
+        for (int64_t t = 0; t < S.N; t++) copy_task(t, b);
+    for (int32_t b = 0; b < B; b++)
+        for (int64_t t = S.N; t < ntasks0; t++) copy_task(t, b);
+    S.limb_slot1.assign(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + M));
+    S.nlimb1 = nl;
+    S.levels4 = std::move(lv4);
+    S.task_ptr = std::move(tp);
+    S.ent_slot = std::move(es);
+    S.ent_w = std::move(ew);
+    S.ent_lslot = std::move(el);
+    S.nslots = total;
+    S.nlimb = (int64_t)B * nl;
+    S.products *= B;
+    S.batch = B;
+    return true;
+}
+
 }  // namespace mdps

@@ -37,6 +37,11 @@ struct Schedule {
     // per level: (in1, in2, out, code) with code = lslot << 2 | 2 (write limbs)
     // | 1 (write digits: the output is a product input)
     std::vector<std::vector<int32_t>> levels4;
+    // batch of B points (replicate_schedule): per-point limb slots of the
+    // x and coefficient series and the per-point limb-pool size
+    int batch = 1;
+    std::vector<int32_t> limb_slot1;
+    int64_t nlimb1 = 0;
 };
 
 // Validates the inputs (libmdps.h) and builds the schedule.  Pool slots:
@@ -44,5 +49,12 @@ struct Schedule {
 bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mono_ptr,
                     const int32_t *vars, const int32_t *exps, int32_t n, Schedule &S,
                     std::string &err);
+
+// The same system at B points in one schedule (mdps_options.batch): slots
+// [0, B n) = the points' x, [B n, B n + M) = the shared coefficients, then B
+// blocks of product slots; every level holds the B copies of its jobs, the
+// addition jobs are the B N values then the B N n Jacobian entries, each
+// point with its own limb-pool block.  The kernels are unchanged.
+bool replicate_schedule(Schedule &S, int32_t n, int32_t B, std::string &err);
 
 }  // namespace mdps
