@@ -39,6 +39,7 @@ CONFIG_TEXT = {
     "od": "BASELINE configs[2]: octo double, n=64, 128 monomials x 8..16 vars, degree 63",
     "deca": "BASELINE configs[3]: deca double, n=128, 128 monomials x 16 vars, degree 63",
 }
+METRIC = "series products/s (mdps_eval_diff)"
 TOL = {2: 1e-29, 3: 1e-45, 4: 1e-61, 5: 1e-77, 8: 1e-124, 10: 1e-156}
 
 
@@ -54,6 +55,21 @@ def workload(name: str):
         _, d, L = name.split("_")
         return mdinputs.sweep_cell(int(d[1:]), int(L[1:]))
     return mdinputs.make_config(name)
+
+
+def bench_config(si, name: str, world: int = 1, sharded: bool = False) -> dict:
+    """The `config` object of the JSON line: identical for both arms (host-only
+    facts about the workload; the GPU schedule's own figures go under
+    `schedule`)."""
+    from paper_2012_06607_b200 import shard
+    return {"workload": CONFIG_TEXT.get(name, name), "name": name,
+            "n": si.n, "monomials": si.M, "degree": si.degree, "limbs": si.limbs,
+            "products_per_step": int(sum(shard.row_products(si.poly_ptr, si.mono_ptr, si.exps))),
+            "parallelism": (f"rows sharded over {world} GPUs" if sharded else f"replicas x{world}")
+            if world > 1 else "single GPU",
+            "l2": "256 MiB buffer written between timed steps (L2 flushed)",
+            "seed": mdinputs.CONFIGS[si.name].seed if si.name in mdinputs.CONFIGS else None,
+            "input_sha256": si.sha256()[:16]}
 
 
 # ---------------------------------------------------------------------------
@@ -145,11 +161,11 @@ def run_reference(args):
         prods += p
     dt = time.perf_counter() - t0
     value = prods / dt
-    line = {"impl": "reference", "metric": "series products/s", "value": value, "unit": "products/s",
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "products/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * dt / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64 (exact superaccumulator)", "data": "synthetic",
-            "config": {"workload": CONFIG_TEXT.get(args.config, args.config), "name": args.config},
+            "config": bench_config(si, args.config, args.gpus),
             "cpu_baseline": {"value": value, "unit": "products/s", "cores": cores, "kind": "oracle",
                              "sample": f"one Jacobian entry of {si.name} per step (naive products)"},
             "e2e": {"value": value, "unit": "products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -291,7 +307,7 @@ def main():
         dist.barrier()
     mdps.lib()
 
-    si = workload(args.config)
+    si = si_full = workload(args.config)
     sharded = args.shard == "rows" and world > 1
     if sharded:  # strong scaling: this rank evaluates its share of the rows
         import dataclasses
@@ -412,19 +428,13 @@ def main():
 
     if rank == 0:
         line = {
-            "metric": "series products/s (mdps_eval_diff)",
+            "metric": METRIC,
             "value": value, "unit": "products/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": CONFIG_TEXT.get(args.config, args.config), "name": args.config,
-                       "n": si.n, "monomials": si.M, "degree": si.degree, "limbs": si.limbs,
-                       "algo": {1: "eft", 2: "digits"}[st["algo"]], "digits": st["digits"],
-                       "products_per_step": products_per_step, "levels": st["levels"],
-                       "parallelism": (f"rows sharded over {world} GPUs" if sharded else f"replicas x{world}")
-                       if world > 1 else "single GPU",
-                       "l2": "256 MiB buffer written between timed steps (L2 flushed)",
-                       "seed": mdinputs.CONFIGS[si.name].seed if si.name in mdinputs.CONFIGS else None,
-                       "input_sha256": si.sha256()[:16]},
+            "config": bench_config(si_full, args.config, world, sharded),
+            "schedule": {"algo": {1: "eft", 2: "digits"}[st["algo"]], "digits": st["digits"],
+                         "products_per_step": products_per_step, "levels": st["levels"]},
             "fp64_ops_per_s": fp64_per_s,
             "fp64_ops_per_step": st["fp64_ops_total"],
             "roofline": roofline,

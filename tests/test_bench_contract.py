@@ -8,6 +8,8 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
 
 
 def run_bench(*args, timeout=900):
@@ -29,6 +31,9 @@ def test_reference_arm_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"] and cb["sample"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # the driver divides the two arms: same metric, unit, direction and config
+    assert d["metric"] == bench.METRIC and d["unit"] == "products/s" and d["higher_is_better"] is True
+    assert d["config"] == bench.bench_config(bench.workload("dd"), "dd", 1)
 
 
 @pytest.mark.gpu
@@ -40,7 +45,7 @@ def test_gpu_arm_line():
         assert k in d, k
     assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] >= 3 and d["higher_is_better"] is True
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] > 0
-    assert "workload" in d["config"]
+    assert d["metric"] == bench.METRIC and d["config"] == bench.bench_config(bench.workload("dd"), "dd", 1)
     r = d["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in r, k
