@@ -81,57 +81,90 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     constexpr int P2 = PADZ + S;
     // part 0 (re): Ur*Wr - Ui*Wi ;  part 1 (im): Ur*Wi + Ui*Wr.  One code
     // copy serves both passes (instruction-cache footprint): the part only
-    // selects the y planes and the sign applied to Ui (a sign-bit flip).
+    // selects the y planes and the sign applied to Wi (a sign-bit flip).
     const int w1part = part, w2part = 1 - part;
     const long long sgn = part == 0 ? (long long)0x8000000000000000ULL : 0LL;
     md_zero(A);
     int cnt = 0;
     bool switched = false;
-    for (int j = f; j <= D; j += F) {
+    // Software pipeline, one term ahead.  Everything the next term needs
+    // (its x digits, its y offset kk and its alignment shifts d1, d2, read
+    // from the exponents) is prepared INSIDE the current term's body, where
+    // the integer work and the shared-memory latency hide behind the DFMAs:
+    // after digit row l the operand digit u = S-1-l has had its last use, so
+    // its register takes the next term's digit u (no extra registers).  The
+    // per-term preamble shrinks to the warp vote on the fast path.
+    auto term_index = [&](int j) { return j <= t ? j : j - t - 1; };
+    auto term_meta = [&](int j, int &kk, int &d1, int &d2) {
         const bool first = j <= t;
-        if (!first && !switched) {  // k1 partial complete: park it, start k2
+        const int i = term_index(j);
+        kk = (first ? t : D - 1 - t) - i;
+        const int eacc = first ? eacc1 : eacc2;
+        const int exr = ex[i], exi = REAL ? ZERO_E : ex[D + i];
+        const int ey1 = ey[w1part * D + kk], ey2 = REAL ? 0 : ey[w2part * D + kk];
+        d1 = eacc - exr - ey1;
+        d2 = eacc - exi - ey2;
+        if (exr + ey1 <= ZERO_E / 2) d1 = 0;  // zero product: any plane will do
+        if (REAL || exi + ey2 <= ZERO_E / 2) d2 = 0;
+    };
+    double Ur[S], Ui[S];
+    int kk, d1, d2;
+    {
+        const int j0 = min(f, D);  // a lane with f > D has no terms (clamped reads only)
+        term_meta(j0, kk, d1, d2);
+        const double *ux = sx + term_index(j0);
+#pragma unroll
+        for (int s = 0; s < S; s++) {
+            Ur[s] = ux[s * D];
+            Ui[s] = REAL ? 0.0 : ux[(S + s) * D];
+        }
+    }
+    // part 0's sign (-Ui*Wi) is applied to the streamed y digit w2 (one flip
+    // per digit row, inside the body) rather than to the S held x digits
+    auto neg = [&](double w) { return __longlong_as_double(__double_as_longlong(w) ^ sgn); };
+    for (int j = f; j <= D; j += F) {
+        if (j > t && !switched) {  // k1 partial complete: park it (raw), start k2
+            // no carry here: lanes of a warp cross the fold at different
+            // iterations, so anything done here runs divergently.  The raw
+            // partial is below 2^53 (< NORM terms since the last carry) and
+            // is carried after the loop, by all lanes at once.  cnt is not
+            // reset, so the periodic carries stay warp-uniform too.
             switched = true;
-            carry_pass(A);
 #pragma unroll
             for (int s = 0; s < S; s++) {
                 park[s] = A[s];
                 A[s] = 0.0;
             }
-            cnt = 0;
         }
-        const int i = first ? j : j - t - 1;
-        const int kk = (first ? t : D - 1 - t) - i;
-        const int eacc = first ? eacc1 : eacc2;
-        double Ur[S], Ui[S];
-        const double *ux = sx + i;
-#pragma unroll
-        for (int s = 0; s < S; s++) {
-            Ur[s] = ux[s * D];
-            Ui[s] = REAL ? 0.0 : __longlong_as_double(__double_as_longlong(ux[(S + s) * D]) ^ sgn);
-        }
-        const int exr = ex[i], exi = REAL ? ZERO_E : ex[D + i];
-        const int ey1 = ey[w1part * D + kk], ey2 = REAL ? 0 : ey[w2part * D + kk];
-        int d1 = eacc - exr - ey1, d2 = eacc - exi - ey2;
-        if (exr + ey1 <= ZERO_E / 2) d1 = 0;  // zero product: any plane will do
-        if (REAL || exi + ey2 <= ZERO_E / 2) d2 = 0;
+        // the next term (this term again on the last iteration: harmless)
+        const int jn = j + F <= D ? j + F : j;
+        const double *uxn = sx + term_index(jn);
+        int kkn, d1n, d2n;
+        auto ahead = [&](int l) {  // called after digit row l of the body
+            if (l == 1) term_meta(jn, kkn, d1n, d2n);
+            const int u = S - 1 - l;
+            Ur[u] = uxn[u * D];
+            if (!REAL) Ui[u] = uxn[(S + u) * D];
+        };
         const bool fast = d1 <= PADZ && d2 <= PADZ;
         if (__all_sync(__activemask(), fast)) {
             const double *W1 = sy + (w1part * P2 + PADZ - d1) * D + kk;
             const double *W2 = sy + (w2part * P2 + PADZ - d2) * D + kk;
             // software pipelined: row l+1's two digits load while row l's FMAs run
-            double w1 = W1[0], w2 = REAL ? 0.0 : W2[0];
+            double w1 = W1[0], w2 = REAL ? 0.0 : neg(W2[0]);
 #pragma unroll
             for (int l = 0; l < S; l++) {
                 double w1n = 0.0, w2n = 0.0;
                 if (l + 1 < S) {
                     w1n = W1[(l + 1) * D];
-                    if (!REAL) w2n = W2[(l + 1) * D];
+                    if (!REAL) w2n = neg(W2[(l + 1) * D]);
                 }
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
                     if (!REAL) A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
+                ahead(l);
                 w1 = w1n;
                 w2 = w2n;
             }
@@ -141,14 +174,18 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
 #pragma unroll
             for (int l = 0; l < S; l++) {
                 const double w1 = (l >= d1) ? W1[(PADZ + l - d1) * D] : 0.0;
-                const double w2 = (!REAL && l >= d2) ? W2[(PADZ + l - d2) * D] : 0.0;
+                const double w2 = (!REAL && l >= d2) ? neg(W2[(PADZ + l - d2) * D]) : 0.0;
 #pragma unroll
                 for (int u = 0; u < S - l; u++) {
                     A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
                     if (!REAL) A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
                 }
+                ahead(l);
             }
         }
+        kk = kkn;
+        d1 = d1n;
+        d2 = d2n;
         if (++cnt == NORM) {
             carry_pass(A);
             cnt = 0;
@@ -370,25 +407,27 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
 #pragma unroll
             for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
         }
-        if (F == 1) {
-            double B[S];
+        // k1: every lane carries its parked (raw) partial, then the same
+        // shuffle reduction — warp-uniform work, no lane sums alone
+        double B[S];
 #pragma unroll
-            for (int s = 0; s < S; s++) B[s] = park[s];
+        for (int s = 0; s < S; s++) B[s] = park[s];
+        carry_pass(B);
+        for (int off = F >> 1; off > 0; off >>= 1) {
+#pragma unroll
+            for (int s = 0; s < S; s++) B[s] = __dadd_rn(B[s], __shfl_xor_sync(0xffffffffu, B[s], off));
+        }
+        __syncwarp();  // parked partials consumed before the emit scratch reuses them
+        if (F == 1) {
             if (writer && k2 != k1) conv_dig_emit<L>(A, e2, wdig ? zd : nullptr, ze, zl, D, k2, part, park);
             if (writer) conv_dig_emit<L>(B, e1, wdig ? zd : nullptr, ze, zl, D, k1, part, park);
-        } else {
-            if (f == 0) {  // k1: lane 0 sums the F parked partials of its pair
-#pragma unroll
-                for (int s = 0; s < S; s++) A[s] = park[s];
-                for (int g = 1; g < F; g++) {
-#pragma unroll
-                    for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], park[g * PSTR + s]);
-                }
-            }
-            __syncwarp();  // parked partials consumed before the emit scratch reuses them
+        } else if (writer && f < 2 && (f == 0 || k2 != k1)) {
             // lanes 0 and 1 emit k1 and k2 in one (lane-dependent) call
-            if (writer && f < 2 && (f == 0 || k2 != k1))
-                conv_dig_emit<L>(A, f == 0 ? e1 : e2, wdig ? zd : nullptr, ze, zl, D, f == 0 ? k1 : k2, part, park);
+            if (f == 0) {
+#pragma unroll
+                for (int s = 0; s < S; s++) A[s] = B[s];
+            }
+            conv_dig_emit<L>(A, f == 0 ? e1 : e2, wdig ? zd : nullptr, ze, zl, D, f == 0 ? k1 : k2, part, park);
         }
         __syncwarp();
     }
