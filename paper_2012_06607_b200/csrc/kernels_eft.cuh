@@ -110,14 +110,32 @@ __global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict
     double Br[L + 1], Bi[L + 1];
     md_zero(Br);
     md_zero(Bi);
-    for (int e = task_ptr[task]; e < task_ptr[task + 1]; e++) {
-        const double *s = pool + (size_t)ent_slot[e] * LD2;
-        const int w = ent_w[e];
-        double ar[L], ai[L];
+    // software pipeline over the entries: entry e+1's limbs (and e+2's slot
+    // index) are loaded while entry e is summed — the loop is bound by the
+    // chained loads (slot index, then limbs), not by the bins arithmetic
+    const int e0 = task_ptr[task], e1 = task_ptr[task + 1];
+    auto load = [&](int e, double (&ar)[L], double (&ai)[L], int slot) {
+        const double *s = pool + (size_t)slot * LD2;
 #pragma unroll
         for (int p = 0; p < L; p++) {
             ar[p] = s[p * D + k];
             ai[p] = s[(L + p) * D + k];
+        }
+    };
+    double ar[L], ai[L];
+    int w = 0, slot_next = 0;
+    if (e0 < e1) {
+        load(e0, ar, ai, ent_slot[e0]);
+        w = ent_w[e0];
+        if (e0 + 1 < e1) slot_next = ent_slot[e0 + 1];
+    }
+    for (int e = e0; e < e1; e++) {
+        double nr[L], ni[L];
+        int nw = 0, slot_nn = 0;
+        if (e + 1 < e1) {
+            load(e + 1, nr, ni, slot_next);
+            nw = ent_w[e + 1];
+            if (e + 2 < e1) slot_nn = ent_slot[e + 2];
         }
         if (w == 1) {
             bins_add<L>(Br, ar);
@@ -126,6 +144,13 @@ __global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict
             bins_add_scaled<L>(Br, ar, (double)w);
             bins_add_scaled<L>(Bi, ai, (double)w);
         }
+#pragma unroll
+        for (int p = 0; p < L; p++) {
+            ar[p] = nr[p];
+            ai[p] = ni[p];
+        }
+        w = nw;
+        slot_next = slot_nn;
     }
     double zr[L], zi[L];
     md_renorm(Br, zr);
