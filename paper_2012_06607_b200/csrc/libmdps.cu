@@ -309,8 +309,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     const int D = degree + 1;
     const int real = opt ? (opt->real != 0) : 0;
     if (real && algo == MDPS_ALGO_EFT) { set_err("real systems need the digits algorithm"); return nullptr; }
-    if (algo == MDPS_ALGO_AUTO) algo = (D <= 128) ? MDPS_ALGO_DIGITS : MDPS_ALGO_EFT;
-    if (real && algo != MDPS_ALGO_DIGITS) { set_err("real systems need degree <= 127"); return nullptr; }
+    if (real && D > 128) { set_err("real systems need degree <= 127"); return nullptr; }
     if (algo == MDPS_ALGO_DIGITS && D > 128) { set_err("the digits algorithm supports degree <= 127"); return nullptr; }
 
     Schedule S;
@@ -322,6 +321,14 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     if (S.M > 0 && !coefficients) { set_err("NULL coefficients"); return nullptr; }
     const int B = opt && opt->batch > 1 ? opt->batch : 1;
     if (opt && opt->batch < 0) { set_err("batch must be >= 1"); return nullptr; }
+    // MDPS_ALGO_AUTO (measured): digits, except above degree 127
+    // (digits cap) and for L <= 3 on systems with enough product jobs to fill
+    // the GPU (counted per point: a batch picks what its points pick) — there
+    // the digit kernel is shared-memory bound (S = 7, 10 digits: 4S loads per
+    // S(S+1) DFMAs) and the EFT kernel is faster (d = 63: L = 2 1.55x, L = 3
+    // 1.08x); small systems stay latency-bound, where digits win
+    if (algo == MDPS_ALGO_AUTO)
+        algo = D > 128 || (!real && limbs <= 3 && S.products >= 4096) ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
     const std::vector<int32_t> limb_slot1(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + S.M));
     const int64_t nlimb1 = S.nlimb;
     if (B > 1 && !replicate_schedule(S, n, B, err)) {
