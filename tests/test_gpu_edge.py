@@ -91,3 +91,20 @@ def test_tiny_and_huge_magnitudes(scale_exp):
                 continue
             e = 2.0 ** -int(np.floor(np.log2(s)))        # rescale to O(1), exactly
             assert oracle.series_err(a * e, b * e).max() <= TOL[L]
+
+
+@pytest.mark.parametrize("algo", (1, 2))
+@pytest.mark.parametrize("L", (2, 4, 8))
+def test_constant_series_inputs(algo, L):
+    """Constant series (only t^0 nonzero) and constant coefficients at D > 1:
+    every higher coefficient of f and J is exactly 0 on the GPU (every term
+    of z_k, k >= 1, has an exact-zero factor), t^0 matches the oracle (which is
+    pinned to plain polynomial evaluation, test_oracle_evaldiff)."""
+    si = mdinputs.random_system(300 + L, n=4, monos=5, m_range=(0, 4), exps=(1, 2, 3), degree=6, limbs=L)
+    si.x[..., 1:] = 0.0
+    si.coeffs[..., 1:] = 0.0
+    vals, jac, _ = gpu_eval(si, algo)
+    assert not vals[..., 1:].any() and not jac[..., 1:].any()
+    ov, oj, _ = oracle.eval_diff(si)
+    assert oracle.series_err(vals, ov).max() <= TOL[L]
+    assert oracle.series_err(jac, oj).max() <= TOL[L]

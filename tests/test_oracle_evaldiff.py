@@ -17,7 +17,7 @@ import pytest
 
 import mdinputs
 import oracle
-from tests.exact import conv, greedy, series_err_exact, series_from_exact, series_value
+from tests.exact import conv, greedy, series_err_exact, series_from_exact, series_value, value
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
 LEVELS = (2, 3, 4, 5, 8, 10)
@@ -240,3 +240,65 @@ def test_entries_match_full_eval():
     vals, jac, prods = oracle.eval_diff(si, nthreads=3)
     out, _ = oracle.eval_entries(si, [(2, -1), (1, 3), (0, 0)], nthreads=1)
     assert np.array_equal(out[0], vals[2]) and np.array_equal(out[1], jac[1, 3]) and np.array_equal(out[2], jac[0, 0])
+
+
+@pytest.mark.parametrize("L", (2, 4, 8))
+def test_constant_series_reduce_to_polynomial_values(L):
+    """SURVEY §8(c) C3 'eval/diff special case': at
+    constant series (only t^0 nonzero) with constant coefficients, every
+    coefficient t^k, k >= 1, of f and J is exactly 0 and t^0 is the plain
+    complex polynomial value and derivative — written out here with exact
+    rationals on scalars (no series arithmetic)."""
+    si = mdinputs.random_system(300 + L, n=4, monos=5, m_range=(0, 4), exps=(1, 2, 3), degree=6, limbs=L)
+    si.x[..., 1:] = 0.0
+    si.coeffs[..., 1:] = 0.0
+    vals, jac, _ = oracle.eval_diff(si)
+    assert not vals[..., 1:].any() and not jac[..., 1:].any()
+    xs = [(value(si.x[j, 0, :, 0]), value(si.x[j, 1, :, 0])) for j in range(si.n)]
+
+    def cmul_(a, b):
+        return (a[0] * b[0] - a[1] * b[1], a[0] * b[1] + a[1] * b[0])
+
+    bound = 64 * 2.0 ** (-53 * L)
+    for i in range(si.n):
+        f = (Fraction(0), Fraction(0))
+        df = [(Fraction(0), Fraction(0)) for _ in range(si.n)]
+        for r in range(si.poly_ptr[i], si.poly_ptr[i + 1]):
+            c = (value(si.coeffs[r, 0, :, 0]), value(si.coeffs[r, 1, :, 0]))
+            mono = list(zip(si.vars[si.mono_ptr[r]:si.mono_ptr[r + 1]].tolist(),
+                            si.exps[si.mono_ptr[r]:si.mono_ptr[r + 1]].tolist()))
+            term = c
+            for v, a in mono:
+                for _ in range(a):
+                    term = cmul_(term, xs[v])
+            f = (f[0] + term[0], f[1] + term[1])
+            for vl, al in mono:  # d/dx_vl: al * c * x_vl^(al-1) * prod_{v != vl} x_v^a
+                term = (al * c[0], al * c[1])
+                for v, a in mono:
+                    for _ in range(a - (1 if v == vl else 0)):
+                        term = cmul_(term, xs[v])
+                df[vl] = (df[vl][0] + term[0], df[vl][1] + term[1])
+        assert series_err_exact(vals[i][..., :1], [f]) <= bound
+        for j in range(si.n):
+            assert series_err_exact(jac[i, j][..., :1], [df[j]]) <= bound
+
+
+@pytest.mark.parametrize("L", (2, 5, 10))
+def test_monomial_quotient_identity(L):
+    """Per monomial f = c prod x_l^(a_l): x_l * df/dx_l = a_l * f exactly
+    (SURVEY §8(c) C3 'eval/diff identities'; the north star's
+    exponent-weighted monomial quotients), checked on the oracle's rounded
+    outputs with exact rational series products."""
+    for seed in range(3):
+        si = mdinputs.random_system(400 + 10 * L + seed, n=5, monos=1, m_range=(3, 5), exps=(1, 2, 3),
+                                    degree=5, limbs=L)
+        vals, jac, _ = oracle.eval_diff(si)
+        D = si.degree + 1
+        F0 = series_value(vals[0])
+        scale = max(max(abs(a), abs(b)) for a, b in F0) + 1
+        r = si.poly_ptr[0]
+        for v, a in zip(si.vars[si.mono_ptr[r]:si.mono_ptr[r + 1]].tolist(),
+                        si.exps[si.mono_ptr[r]:si.mono_ptr[r + 1]].tolist()):
+            lhs = conv(series_value(si.x[v]), series_value(jac[0, v]), D)
+            diff = max(max(abs(p[0] - a * q[0]), abs(p[1] - a * q[1])) for p, q in zip(lhs, F0))
+            assert diff <= 256 * 2.0 ** (-53 * L) * scale, (seed, v, float(diff))
