@@ -326,9 +326,11 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     // the GPU (counted per point: a batch picks what its points pick) — there
     // the digit kernel is shared-memory bound (S = 7, 10 digits: 4S loads per
     // S(S+1) DFMAs) and the EFT kernel is faster (d = 63: L = 2 1.55x, L = 3
-    // 1.08x); small systems stay latency-bound, where digits win
+    // 1.08x; at d = 127 digits win from L = 3 on); small systems stay
+    // latency-bound, where digits win
     if (algo == MDPS_ALGO_AUTO)
-        algo = D > 128 || (!real && limbs <= 3 && S.products >= 4096) ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
+        algo = D > 128 || (!real && (limbs == 2 || (limbs == 3 && D <= 64)) && S.products >= 4096)
+                   ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
     const std::vector<int32_t> limb_slot1(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + S.M));
     const int64_t nlimb1 = S.nlimb;
     if (B > 1 && !replicate_schedule(S, n, B, err)) {
