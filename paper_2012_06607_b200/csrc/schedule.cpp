@@ -84,10 +84,35 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
                 lists[i].emplace_back(c, 1);
                 continue;
             }
-            // common factor c' = c * prod x^(a-1)
+            // common factor c' = c * prod x^(a-1): the same sum(a-1) products as a
+            // chain, multiplied out as a tree — always the two operands of lowest
+            // level first (ties in creation order, deterministic) — so c' sits
+            // at level ceil(log2(1 + sum(a-1))) instead of sum(a-1): the
+            // forward chain and everything after it start earlier (qd's
+            // exponent-2 monomials)
             int32_t cp = c;
-            for (int l = 0; l < m; l++)
-                for (int a = 1; a < mono[l].second; a++) cp = B.job(cp, mono[l].first);
+            {
+                std::vector<std::pair<int32_t, int32_t>> q;  // (level, slot), in creation order
+                q.emplace_back(0, c);
+                for (int l = 0; l < m; l++)
+                    for (int a = 1; a < mono[l].second; a++) q.emplace_back(0, mono[l].first);
+                while (q.size() > 1) {
+                    // the two lowest levels (stable: earliest first)
+                    size_t i0 = 0;
+                    for (size_t t = 1; t < q.size(); t++)
+                        if (q[t].first < q[i0].first) i0 = t;
+                    const auto a0 = q[i0];
+                    q.erase(q.begin() + (long)i0);
+                    size_t i1 = 0;
+                    for (size_t t = 1; t < q.size(); t++)
+                        if (q[t].first < q[i1].first) i1 = t;
+                    const auto a1 = q[i1];
+                    q.erase(q.begin() + (long)i1);
+                    const int32_t o = B.job(a0.second, a1.second);
+                    q.emplace_back(B.level[(size_t)o], o);
+                }
+                cp = q[0].second;
+            }
             for (int l = 0; l < m; l++) S.max_weight = std::max(S.max_weight, mono[l].second);
             if (m == 1) {
                 lists[i].emplace_back(B.job(cp, mono[0].first), 1);

@@ -3,7 +3,9 @@
 // Per monomial c * prod_l x_{v_l}^{a_l} (variables ascending)
 // the product jobs of algorithmic differentiation (all n
 // partials at ~3x the cost of one evaluation):
-//   common factor  c' = c * prod_l x_{v_l}^{a_l - 1}     (only when some a_l >= 2)
+//   common factor  c' = c * prod_l x_{v_l}^{a_l - 1}     (only when some a_l >= 2;
+//                  multiplied out as a tree, lowest levels first: depth
+//                  ceil(log2(1 + sum(a_l - 1))), the same product count)
 //   forward        f_1 = c' x_{v_1},  f_l = f_{l-1} x_{v_l};  value = f_m
 //   backward       B_0 = x_{v_m} (alias),  B_k = B_{k-1} x_{v_{m-k}},  k = 1..m-2
 //   cross          d_1 = c' B_{m-2},  d_l = f_{l-1} B_{m-l-1} (l = 2..m-1),  d_m = f_{m-1}
