@@ -85,6 +85,10 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int 
     DigGeom best{T, 1, 1, 32, 0};
     double best_score = -1.0;
     const char *ef = getenv("MDPS_CONV_F"), *ep = getenv("MDPS_CONV_P");
+    // resident warps count up to 16 per SM; measured (profiles/r01_sweep.json
+    // history): at L = 4, D >= 32 more terms per lane beat the 16th warp
+    // (qd 1.03 -> 0.97 ms, d = 31 -12%, d = 63 -7%), elsewhere 16 is right
+    const int warp_cap = (L == 4 && D >= 32) ? 12 : 16;
     for (int F = 1; F <= 8; F *= 2) {
         if (ef && atoi(ef) != F) continue;
         for (int P = 1; P <= 32; P *= 2) {
@@ -106,7 +110,7 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int 
             const int iters = (D + 1 + F - 1) / F;
             const double balance = (double)(D + 1) / (F * iters) * (double)(P * T * F) / g.threads;
             const double amort = (double)iters / (iters + 3.0);
-            const double score = std::min(warps, 16) * balance * amort;
+            const double score = std::min(warps, warp_cap) * balance * amort;
             if (score > best_score) {
                 best_score = score;
                 best = g;
