@@ -33,7 +33,7 @@ EXPORTED_SYMBOLS = (
     "mdps_system_create", "mdps_system_create_ex", "mdps_eval_diff", "mdps_eval_diff_host",
     "mdps_system_destroy", "mdps_last_error", "mdps_system_stats", "mdps_system_level_jobs",
     "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
-    "mdps_fp64_peak", "mdps_system_set_timing", "mdps_system_timing",
+    "mdps_fp64_peak", "mdps_test_force_geometry", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
     "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls",
 )
@@ -111,6 +111,7 @@ def lib() -> ctypes.CDLL:
     L.mdps_test_norm2sq.argtypes = [vp, i32, i32, vp, vp]
     L.mdps_test_digits_roundtrip.argtypes = [vp, vp, i32, i32, i32, vp]
     L.mdps_fp64_peak.argtypes = [i64, P(ctypes.c_double), vp]
+    L.mdps_test_force_geometry.argtypes = [i32, i32]
     L.mdps_system_set_timing.argtypes = [vp, i32]
     L.mdps_system_timing.argtypes = [vp, P(Timing), i32]
     L.mdps_solver_create.restype = vp
@@ -394,6 +395,11 @@ def test_digits_roundtrip(x, stream=None):
     _check(lib().mdps_test_digits_roundtrip(_dptr(x), _dptr(y), count, D - 1, L, _stream_handle(stream)),
            "mdps_test_digits_roundtrip")
     return y
+
+
+def force_geometry(F: int = 0, P: int = 0) -> None:
+    """Tuning only: force the digit product kernel's (F, P); 0, 0 = the model."""
+    _check(lib().mdps_test_force_geometry(F, P), "mdps_test_force_geometry")
 
 
 def fp64_peak(iters: int = 20000, stream=None) -> float:

@@ -79,12 +79,39 @@ struct DigGeom {
 // by registers, shared memory and 64 warps), lane balance of the folded
 // triangle ((D+1) terms over F lanes) and the per-lane term count that
 // amortises the per-output epilogue.  MDPS_CONV_F / MDPS_CONV_P override.
-static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int kind) {
+// forced geometry of the product kernel (mdps_test_force_geometry; tuning only)
+static int g_force_F = 0, g_force_P = 0;
+
+// Measured best (F, P) of the complex two-pass digit kernel where it beats the
+// model by > 1% (scripts/tune_table.py, every fitting (F, P) timed on the
+// sweep cells and configs; profiles/r01_tune_table.json): {L, D, F, P}.
+static const int kTunedGeom[][4] = {
+    {3, 64, 2, 1},  {4, 32, 2, 2},  {5, 64, 2, 1},  {8, 16, 2, 2},  {8, 32, 2, 1},
+    {10, 16, 2, 4}, {10, 32, 2, 2}, {10, 64, 2, 1},
+};
+
+static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int kind, int forceF = 0,
+                        int forceP = 0, bool tuned = false) {
     const int S = digits_for(L);
     const int T = (D + 1) / 2;
     DigGeom best{T, 1, 1, 32, 0};
     double best_score = -1.0;
     const char *ef = getenv("MDPS_CONV_F"), *ep = getenv("MDPS_CONV_P");
+    if (tuned && !ef && !ep && forceF == 0 && forceP == 0)
+        for (const auto &t : kTunedGeom)
+            if (t[0] == L && t[1] == D) {
+                forceF = t[2];
+                forceP = t[3];
+            }
+    char fbuf[16], pbuf[16];
+    if (forceF > 0) {
+        snprintf(fbuf, sizeof fbuf, "%d", forceF);
+        ef = fbuf;
+    }
+    if (forceP > 0) {
+        snprintf(pbuf, sizeof pbuf, "%d", forceP);
+        ep = pbuf;
+    }
     // resident warps count up to 16 per SM; measured (profiles/r01_sweep.json
     // history): at L = 4, D >= 32 more terms per lane beat the 16th warp
     // (qd 1.03 -> 0.97 ms, d = 31 -12%, d = 63 -7%), elsewhere 16 is right
@@ -162,6 +189,7 @@ struct ConvDig {
                  : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
         // geometry per D, computed once (benign race: every writer stores the same value)
         static DigGeom cache[2 * 257];
+        static int cregs[2 * 257], cmaxt[2 * 257];
         static bool cached[2 * 257];
         const int key = D + (real ? 257 : 0);
         if (!cached[key]) {
@@ -171,10 +199,17 @@ struct ConvDig {
                 regs = fa.numRegs;
                 maxt = std::min(fa.maxThreadsPerBlock, 256);
             }
-            cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind);
+            cregs[key] = regs;
+            cmaxt[key] = maxt;
+            cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind, 0, 0, !real && kind == 0);
+            if (cache[key].smem == 0) cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind);  // tuned entry does not fit
             cached[key] = true;
         }
-        const DigGeom g = cache[key];
+        DigGeom g = cache[key];
+        if (g_force_F > 0 || g_force_P > 0) {  // tuning: a forced (F, P), checked against the limits
+            g = dig_geom(L, D, cregs[key], cmaxt[key], real ? 0 : kind, g_force_F, g_force_P);
+            if (g.smem == 0) { set_err("forced geometry does not fit"); return MDPS_EINVAL; }
+        }
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
         kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, lpool, jobs, njobs, D, g.T, g.F, g.P);
@@ -326,14 +361,15 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     const int B = opt && opt->batch > 1 ? opt->batch : 1;
     if (opt && opt->batch < 0) { set_err("batch must be >= 1"); return nullptr; }
     // MDPS_ALGO_AUTO (measured): digits, except above degree 127
-    // (digits cap) and for L <= 3 on systems with enough product jobs to fill
+    // (digits cap) and for L = 2 (L = 3 up to degree 31) on systems with enough
+    // product jobs to fill
     // the GPU (counted per point: a batch picks what its points pick) — there
-    // the digit kernel is shared-memory bound (S = 7, 10 digits: 4S loads per
-    // S(S+1) DFMAs) and the EFT kernel is faster (d = 63: L = 2 1.55x, L = 3
-    // 1.08x; at d = 127 digits win from L = 3 on); small systems stay
-    // latency-bound, where digits win
+    // the digit kernel is shared-memory bound (S = 7 digits: 4S loads per
+    // S(S+1) DFMAs) and the EFT kernel is faster (1.4-1.5x at every degree),
+    // at L = 3 up to degree 31 (by 2-7%; digits with the tuned geometry win
+    // from degree 63 on); small systems stay latency-bound, where digits win
     if (algo == MDPS_ALGO_AUTO)
-        algo = D > 128 || (!real && (limbs == 2 || (limbs == 3 && D <= 64)) && S.products >= 4096)
+        algo = D > 128 || (!real && (limbs == 2 || (limbs == 3 && D <= 32)) && S.products >= 4096)
                    ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
     const std::vector<int32_t> limb_slot1(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + S.M));
     const int64_t nlimb1 = S.nlimb;
@@ -849,6 +885,16 @@ __global__ void fp64_peak_kernel(int64_t iters, double *sink) {
     }
     const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
     if (s == 12345.678) sink[0] = s;
+}
+
+extern "C" int mdps_test_force_geometry(int32_t F, int32_t P) {
+    if (F < 0 || F > 8 || (F & (F - 1)) || P < 0 || P > 32 || (P & (P - 1))) {
+        set_err("forced geometry: F in {0,1,2,4,8}, P in {0,1,...,32} (powers of two)");
+        return MDPS_EINVAL;
+    }
+    g_force_F = F;
+    g_force_P = P;
+    return MDPS_OK;
 }
 
 extern "C" int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t stream) {
