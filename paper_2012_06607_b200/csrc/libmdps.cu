@@ -90,19 +90,33 @@ static const int kTunedGeom[][4] = {
     {10, 16, 2, 4}, {10, 32, 2, 2}, {10, 64, 2, 1},
 };
 
+// The same for the real-system kernel (mdps_options.real; TUNE_REAL=1,
+// profiles/r01_tune_table_real.json).
+static const int kTunedGeomReal[][4] = {
+    {2, 32, 2, 2},  {3, 16, 2, 4},  {3, 64, 2, 1},  {3, 128, 2, 1}, {4, 16, 2, 2},  {4, 32, 2, 2},
+    {5, 16, 2, 2},  {5, 32, 2, 1},  {5, 64, 2, 1},  {8, 16, 2, 2},  {10, 16, 2, 4}, {10, 32, 2, 2},
+    {10, 64, 2, 1},
+};
+
+// tuned: 0 the model only, 1 the complex table, 2 the real table
 static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int kind, int forceF = 0,
-                        int forceP = 0, bool tuned = false) {
+                        int forceP = 0, int tuned = 0) {
     const int S = digits_for(L);
     const int T = (D + 1) / 2;
     DigGeom best{T, 1, 1, 32, 0};
     double best_score = -1.0;
     const char *ef = getenv("MDPS_CONV_F"), *ep = getenv("MDPS_CONV_P");
-    if (tuned && !ef && !ep && forceF == 0 && forceP == 0)
-        for (const auto &t : kTunedGeom)
-            if (t[0] == L && t[1] == D) {
-                forceF = t[2];
-                forceP = t[3];
-            }
+    if (tuned && !ef && !ep && forceF == 0 && forceP == 0) {
+        auto pick = [&](const auto &table) {
+            for (const auto &t : table)
+                if (t[0] == L && t[1] == D) {
+                    forceF = t[2];
+                    forceP = t[3];
+                }
+        };
+        if (tuned == 1) pick(kTunedGeom);
+        else pick(kTunedGeomReal);
+    }
     char fbuf[16], pbuf[16];
     if (forceF > 0) {
         snprintf(fbuf, sizeof fbuf, "%d", forceF);
@@ -201,7 +215,7 @@ struct ConvDig {
             }
             cregs[key] = regs;
             cmaxt[key] = maxt;
-            cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind, 0, 0, !real && kind == 0);
+            cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind, 0, 0, real ? 2 : (kind == 0 ? 1 : 0));
             if (cache[key].smem == 0) cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind);  // tuned entry does not fit
             cached[key] = true;
         }

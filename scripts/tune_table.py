@@ -40,9 +40,12 @@ def conv_ms(s, x, v, j, flush, reps):
 
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 out = []
+REAL = os.environ.get("TUNE_REAL") == "1"  # the real-system kernel (mdps_options.real)
 for c in CELLS:
     si = workload(c)
-    with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS) as s:
+    if REAL:
+        si = mdinputs.realify(si)
+    with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS, real=REAL) as s:
         x = torch.from_numpy(si.x).cuda()
         v = torch.empty((si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
         j = torch.empty((si.n, si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
@@ -56,7 +59,7 @@ for c in CELLS:
                 pass
         mdps.force_geometry(0, 0)
     best = min((k for k in res if k != "0,0"), key=lambda k: res[k])
-    row = {"cell": c, "L": si.limbs, "D": si.D, "model_ms": res.get("0,0"), "best": best, "best_ms": res[best],
+    row = {"cell": c, "real": REAL, "L": si.limbs, "D": si.D, "model_ms": res.get("0,0"), "best": best, "best_ms": res[best],
            "gain": res.get("0,0", 0) / res[best], "all": res}
     out.append(row)
     print(json.dumps(row), flush=True)
