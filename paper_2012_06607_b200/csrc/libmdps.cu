@@ -375,15 +375,14 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     const int B = opt && opt->batch > 1 ? opt->batch : 1;
     if (opt && opt->batch < 0) { set_err("batch must be >= 1"); return nullptr; }
     // MDPS_ALGO_AUTO (measured): digits, except above degree 127
-    // (digits cap) and for L = 2 (L = 3 up to degree 31) on systems with enough
-    // product jobs to fill
-    // the GPU (counted per point: a batch picks what its points pick) — there
-    // the digit kernel is shared-memory bound (S = 7 digits: 4S loads per
-    // S(S+1) DFMAs) and the EFT kernel is faster (1.4-1.5x at every degree),
-    // at L = 3 up to degree 31 (by 2-7%; digits with the tuned geometry win
-    // from degree 63 on); small systems stay latency-bound, where digits win
+    // (digits cap), at L = 2 and at L = 3 up to degree 31 on systems of >= 4096
+    // product jobs per point (a batch picks what its points pick).  There the
+    // digit kernel is shared-memory bound (S = 7, 10 digits: 4S loads per
+    // S(S+1) DFMAs) and the EFT kernel is faster: 1.4-1.5x on the L = 2 sweep
+    // cells, 2.1x on a batch of 1024 dd points, even on dd itself; at L = 3 by
+    // 2-7% up to degree 31 (digits with the tuned geometry win from 63 on)
     if (algo == MDPS_ALGO_AUTO)
-        algo = D > 128 || (!real && (limbs == 2 || (limbs == 3 && D <= 32)) && S.products >= 4096)
+        algo = D > 128 || (!real && (limbs == 2 || (limbs == 3 && D <= 32 && S.products >= 4096)))
                    ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
     const std::vector<int32_t> limb_slot1(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + S.M));
     const int64_t nlimb1 = S.nlimb;

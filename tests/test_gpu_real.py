@@ -29,7 +29,7 @@ def gpu_eval_real(si):
 def test_real_mode_equals_complex_mode(name):
     si = mdinputs.realify(mdinputs.sweep_cell(int(name.split("_")[1][1:]), int(name.split("_")[2][1:]))
                           if name.startswith("sweep") else mdinputs.make_config(name))
-    v1, j1, st1 = gpu_eval(si)
+    v1, j1, st1 = gpu_eval(si, 2)  # the complex digit path (the default is EFT at L = 2)
     v2, j2, st2 = gpu_eval_real(si)
     assert not v2[:, 1].any() and not j2[:, :, 1].any()
     L = si.limbs
