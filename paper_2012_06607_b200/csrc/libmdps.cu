@@ -13,6 +13,7 @@
 #include "../../include/mdps_test.h"
 #include "conv_dig.cuh"
 #include "conv_gauss.cuh"
+#include "conv_quad.cuh"
 #include "conv_single.cuh"
 #include "kernels_dig.cuh"
 #include "kernels_eft.cuh"
@@ -102,7 +103,7 @@ static const int kTunedGeomReal[][4] = {
 static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int kind, int forceF = 0,
                         int forceP = 0, int tuned = 0) {
     const int S = digits_for(L);
-    const int T = (D + 1) / 2;
+    const int T = kind == 3 ? D / 4 : (D + 1) / 2;  // kind 3: quads of outputs (conv_quad.cuh)
     DigGeom best{T, 1, 1, 32, 0};
     double best_score = -1.0;
     const char *ef = getenv("MDPS_CONV_F"), *ep = getenv("MDPS_CONV_P");
@@ -141,7 +142,8 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int 
             g.threads = (P * T * F + 31) / 32 * 32;  // whole warps (full-mask shuffles)
             if (g.threads > max_threads) continue;
             g.smem = kind == 1 ? conv_g_smem(S, D, P, T)
-                               : kind == 2 ? conv_s_smem(S, D, P, T) : conv_dig_smem(S, D, P, g.threads);
+                               : kind == 2 ? conv_s_smem(S, D, P, T)
+                               : kind == 3 ? conv_q_smem(S, D, P, g.threads) : conv_dig_smem(S, D, P, g.threads);
             if (g.smem > 227 * 1024) continue;
             const int blocks_smem = (int)(228 * 1024 / (g.smem + 1024));
             const int blocks_regs = 65536 / (std::max(regs_per_thread, 32) * g.threads);
@@ -185,7 +187,9 @@ struct ConvDig {
         // opt-in variants via MDPS_CONV_KERNEL: 1 = three products per term
         // (conv_gauss.cuh; shared-memory bound, od 72 ms vs 47 ms), 2 = one pass
         // for both parts (conv_single.cuh; two blocks/SM, od 56 ms vs 47 ms)
-        static const int kind = getenv("MDPS_CONV_KERNEL") ? atoi(getenv("MDPS_CONV_KERNEL")) : 0;
+        static const int kind0 = getenv("MDPS_CONV_KERNEL") ? atoi(getenv("MDPS_CONV_KERNEL")) : 0;
+        // 3 = two outputs per lane and phase (conv_quad.cuh): D a multiple of 4, complex
+        const int kind = (kind0 == 3 && (D % 4 != 0 || real)) ? 0 : kind0;
         using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
         KernT kern;
         if (real)  // real systems: the two-pass kernel with one product per term
@@ -198,6 +202,9 @@ struct ConvDig {
         else if (kind == 2)
             kern = D == 16 ? conv_s_kernel<L, 16> : D == 32 ? conv_s_kernel<L, 32> : D == 64 ? conv_s_kernel<L, 64>
                  : D == 128 ? conv_s_kernel<L, 128> : conv_s_kernel<L, 0>;
+        else if (kind == 3)
+            kern = D == 16 ? conv_q_kernel<L, 16> : D == 32 ? conv_q_kernel<L, 32> : D == 64 ? conv_q_kernel<L, 64>
+                 : D == 128 ? conv_q_kernel<L, 128> : conv_q_kernel<L, 0>;
         else
             kern = D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> : D == 64 ? conv_dig_kernel<L, 64>
                  : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
