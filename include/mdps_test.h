@@ -67,7 +67,8 @@ int mdps_system_timing(mdps_system *sys, mdps_timing *out, int32_t reset);
 
 /* Phase trace of the last solve (synchronises): globaltimer nanoseconds at the
  * start of the persistent solver kernel and at the completion of each of its
- * grid barriers (refinement phases, then two per coefficient).  Returns the
+ * grid barriers (refinement phases, then one per coefficient pair of the
+ * substitution loop, two where the dx step cannot overlap the updates).  Returns the
  * number of stamps written to ns (<= max) or < 0; refine_steps (optional) =
  * Newton-Schulz steps run. */
 int mdps_solver_trace(mdps_solver *solver, int64_t *ns, int32_t max, int32_t *refine_steps);

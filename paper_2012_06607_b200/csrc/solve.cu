@@ -63,7 +63,8 @@ struct Ctl {              // device control block (memset to 0 before every solv
     int status;           // bit 0: singular A_0
     int refine_steps;     // Newton-Schulz steps run
     int ntrace;           // entries of the phase trace written
-    int pad[2];
+    unsigned int rdy;     // substitution loop: right-hand-side entries final (cumulative)
+    int pad[1];
 };
 constexpr int TRACE_MAX = 1024;
 
@@ -937,55 +938,103 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
         grid_sync(ctl, trace);
     }
 
-    // c. the substitution loop, two coefficients per step
-    double *Xp1 = Xp + VN;
-    int *Xe1 = Xe + 2 * n;
-    for (int j = 0; j < D; j += 2) {
+    // c. the substitution loop, two coefficients per step.  Dataflow overlap:
+    //    the update phase for pair j computes r_{j+2}, r_{j+3} first (tasks
+    //    0 .. 2N-1, all in the first sweep of its groups, on the first blocks),
+    //    each task's writer signals ctl->rdy, and the LAST blocks of the grid,
+    //    after their own share of the updates, wait for those 2N signals and
+    //    compute dx_{j+2}, dx_{j+3} right there — so the dependent dx step of
+    //    the next pair runs under the bulk of the updates and the loop takes one
+    //    grid barrier per pair instead of two.  dx vectors are double-buffered
+    //    (pair parity): blocks may still stage dx_j while dx_{j+2} is written.
+    //    Falls back to a separate dx phase when the grid is too small for the
+    //    first-sweep / disjoint-blocks guarantee (no spinning block ever waits
+    //    on work assigned to itself or to a block behind it).
+    auto xbuf = [&](int j, int which) { return Xp + (size_t)(((j >> 1) & 1) * 2 + which) * VN; };
+    auto xebuf = [&](int j, int which) { return Xe + (size_t)(((j >> 1) & 1) * 2 + which) * 2 * n; };
+    // dx_j = W r_j ; dx_{j+1} = W r'_{j+1} + M r_j on blocks [b0, gridDim)
+    auto dx_phase = [&](int j, int b0) {
         const bool pair = j + 1 < D;
-        {  // dx_j = W r_j ; dx_{j+1} = W r'_{j+1} + M r_j
-            ts_stage<L>(Rp + (size_t)j * VM, Re + (size_t)j * 2 * N, N, 0, xs, xe);
-            if (pair) ts_stage<L>(Rp + (size_t)(j + 1) * VM, Re + (size_t)(j + 1) * 2 * N, N, 0, xs1, xe1);
-            __syncthreads();
-            const int T = pair ? 2 * n : n;
-            const int G = pick_group(T, pair ? 2 * N : N, nth);
-            const int ng = nth / G, g = tid / G, lg = tid % G;
-            for (int base = 0; base < T; base += ng) {
-                const int task = base + g;
-                const bool valid = task < T;
-                const int second = valid && task >= n;
-                const int pp = valid ? task - (second ? n : 0) : 0;
-                const double *wr = Wr + (size_t)pp * VM;
-                const int *wre = Wre + (size_t)pp * 2 * N;
-                if (!second)
-                    ts_task<L>(wr, wre, xs, xe, N, lg, G, valid, none, false, DigOut{Xp + pp, Xe + pp, n},
-                               dx + (size_t)pp * 2 * L * D + j, D, scratch);
-                else
-                    ts_task<L>(wr, wre, xs1, xe1, N, lg, G, valid, none, false, DigOut{Xp1 + pp, Xe1 + pp, n},
-                               dx + (size_t)pp * 2 * L * D + j + 1, D, scratch,
-                               Seg{Mr + (size_t)pp * VM, Mre + (size_t)pp * 2 * N, xs, xe});
+        ts_stage<L>(Rp + (size_t)j * VM, Re + (size_t)j * 2 * N, N, 0, xs, xe);
+        if (pair) ts_stage<L>(Rp + (size_t)(j + 1) * VM, Re + (size_t)(j + 1) * 2 * N, N, 0, xs1, xe1);
+        __syncthreads();
+        const int nthd = ((int)gridDim.x - b0) * blockDim.x;
+        const int tidd = ((int)blockIdx.x - b0) * blockDim.x + threadIdx.x;
+        const int T = pair ? 2 * n : n;
+        const int G = pick_group(T, pair ? 2 * N : N, nthd);
+        const int ng = nthd / G, g = tidd / G, lg = tidd % G;
+        double *X0 = xbuf(j, 0), *X1 = xbuf(j, 1);
+        int *E0 = xebuf(j, 0), *E1 = xebuf(j, 1);
+        for (int base = 0; base < T; base += ng) {
+            const int task = base + g;
+            const bool valid = task < T;
+            const int second = valid && task >= n;
+            const int pp = valid ? task - (second ? n : 0) : 0;
+            const double *wr = Wr + (size_t)pp * VM;
+            const int *wre = Wre + (size_t)pp * 2 * N;
+            if (!second)
+                ts_task<L>(wr, wre, xs, xe, N, lg, G, valid, none, false, DigOut{X0 + pp, E0 + pp, n},
+                           dx + (size_t)pp * 2 * L * D + j, D, scratch);
+            else
+                ts_task<L>(wr, wre, xs1, xe1, N, lg, G, valid, none, false, DigOut{X1 + pp, E1 + pp, n},
+                           dx + (size_t)pp * 2 * L * D + j + 1, D, scratch,
+                           Seg{Mr + (size_t)pp * VM, Mre + (size_t)pp * 2 * N, xs, xe});
+        }
+    };
+    dx_phase(0, 0);
+    grid_sync(ctl, trace);
+    unsigned int rdy_target = 0;
+    for (int j = 0; j + 2 < D; j += 2) {
+        // r_k -= A_{k-j} dx_j + A_{k-j-1} dx_{j+1}, k = j+2..d
+        const int T = (D - 2 - j) * N;
+        const int G = pick_group(T, 2 * n, nth);
+        const int ng = nth / G, g = tid / G, lg = tid % G;
+        const int nnext = j + 3 < D ? 2 * N : N;  // tasks of r_{j+2}, r_{j+3}
+        // the dx blocks of the next pair: the last ones, disjoint from the
+        // blocks holding the r_{j+2}, r_{j+3} tasks
+        const bool pair2 = j + 3 < D;
+        const int Tdx = pair2 ? 2 * n : n, lendx = pair2 ? 2 * N : N;
+        int nbdx = 0;
+        {
+            const int Gd = pick_group(Tdx, lendx, nth);  // upper bound of the subset's group width
+            nbdx = (int)(((long long)Tdx * Gd + blockDim.x - 1) / blockDim.x);
+        }
+        const int rblocks = (int)(((long long)nnext * G + blockDim.x - 1) / blockDim.x);
+        const bool overlap = ng >= nnext && rblocks + nbdx <= (int)gridDim.x;
+        const int b0 = (int)gridDim.x - nbdx;
+        ts_stage<L>(xbuf(j, 0), xebuf(j, 0), n, 1, xs, xe);
+        ts_stage<L>(xbuf(j, 1), xebuf(j, 1), n, 1, xs1, xe1);
+        __syncthreads();
+        for (int base = 0; base < T; base += ng) {
+            const int task = base + g;
+            const bool valid = task < T;
+            const int k = j + 2 + (valid ? task / N : 0), p = valid ? task % N : 0;
+            const size_t row0 = (size_t)(k - j) * N + p, row1 = (size_t)(k - j - 1) * N + p;
+            double *rk = Rp + (size_t)k * VM + p;
+            int *rke = Re + (size_t)k * 2 * N + p;
+            ts_task<L>(Ad + row0 * VN, Ae + row0 * 2 * n, xs, xe, n, lg, G, valid, DigRef{rk, rke, N}, false,
+                       DigOut{rk, rke, N}, nullptr, 0, scratch, Seg{Ad + row1 * VN, Ae + row1 * 2 * n, xs1, xe1});
+            if (overlap && valid && lg == 0 && task < nnext) {  // r_{j+2} / r_{j+3} entry final
+                __threadfence();
+                atomicAdd(&ctl->rdy, 1u);
             }
         }
-        grid_sync(ctl, trace);
-        if (j + 2 >= D) break;
-        {  // r_k -= A_{k-j} dx_j + A_{k-j-1} dx_{j+1}, k = j+2..d
-            ts_stage<L>(Xp, Xe, n, 1, xs, xe);
-            ts_stage<L>(Xp1, Xe1, n, 1, xs1, xe1);
-            __syncthreads();
-            const int T = (D - 2 - j) * N;
-            const int G = pick_group(T, 2 * n, nth);
-            const int ng = nth / G, g = tid / G, lg = tid % G;
-            for (int base = 0; base < T; base += ng) {
-                const int task = base + g;
-                const bool valid = task < T;
-                const int k = j + 2 + (valid ? task / N : 0), p = valid ? task % N : 0;
-                const size_t row0 = (size_t)(k - j) * N + p, row1 = (size_t)(k - j - 1) * N + p;
-                double *rk = Rp + (size_t)k * VM + p;
-                int *rke = Re + (size_t)k * 2 * N + p;
-                ts_task<L>(Ad + row0 * VN, Ae + row0 * 2 * n, xs, xe, n, lg, G, valid, DigRef{rk, rke, N}, false,
-                           DigOut{rk, rke, N}, nullptr, 0, scratch, Seg{Ad + row1 * VN, Ae + row1 * 2 * n, xs1, xe1});
+        rdy_target += overlap ? (unsigned)nnext : 0u;
+        if (overlap && (int)blockIdx.x >= b0) {
+            __syncthreads();  // this block's update tasks no longer read xs / xs1
+            if (threadIdx.x == 0) {
+                volatile unsigned int *vr = &ctl->rdy;
+                while (*vr < rdy_target) __nanosleep(64);
+                __threadfence();
             }
+            __syncthreads();
+            dx_phase(j + 2, b0);
         }
         grid_sync(ctl, trace);
+        if (!overlap) {
+            dx_phase(j + 2, 0);
+            grid_sync(ctl, trace);
+        }
     }
 }
 
@@ -1235,7 +1284,7 @@ extern "C" mdps_solver *mdps_solver_create_ls(int32_t N, int32_t n, int32_t degr
         N * VM * 8,         (size_t)N * 2 * N * 4,   // Pc, Pce
         n * VM * 8,         (size_t)n * 2 * N * 4,   // Mr, Mre
         D * VM * 8,         D * 2 * N * 4,           // Rp, Re
-        2 * VN * 8,         4 * (size_t)n * 4,       // Xp, Xe (two vectors)
+        4 * VN * 8,         8 * (size_t)n * 4,       // Xp, Xe (two vectors, double-buffered)
         n * sizeof(int),    sizeof(ts::Ctl),         // piv, ctl
         ts::TRACE_MAX * sizeof(long long),           // trace
         (size_t)n * VN * 8, (size_t)n * 2 * n * 4};  // Gc, Gce
