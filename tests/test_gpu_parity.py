@@ -65,7 +65,7 @@ def test_ex1_norm_on_device(mdps, L):
 
 @pytest.mark.parametrize("L", LEVELS)
 def test_digits_roundtrip(mdps, L):
-    """limbs -> 22-bit digit planes -> limbs preserves the value to the md unit."""
+    """limbs -> 23-bit digit planes -> limbs preserves the value to the md unit."""
     si = mdinputs.random_system(7, 4, 2, (1, 2), (1,), 20, L)
     y = mdps.test_digits_roundtrip(cuda(si.x)).cpu().numpy()
     err = oracle.series_err(y, si.x)
