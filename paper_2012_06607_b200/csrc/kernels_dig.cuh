@@ -191,55 +191,6 @@ __global__ void __launch_bounds__(128) to_digits_kernel(const double *__restrict
     }
 }
 
-// ---------------------------------------------------------------------------
-// accum_dig: addition jobs on digit planes -> limb outputs.
-// one thread per (task, k); two parts.
-template <int L>
-__global__ void __launch_bounds__(128) accum_dig_kernel(const double *__restrict__ dpool,
-                                                       const int *__restrict__ epool,
-                                                       const int *__restrict__ task_ptr,
-                                                       const int *__restrict__ ent_slot,
-                                                       const int *__restrict__ ent_w, int ntasks, int n,
-                                                       int D, double *__restrict__ values,
-                                                       double *__restrict__ jac) {
-    constexpr int S = digits_for(L);
-    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= (long long)ntasks * D) return;
-    const int task = (int)(g / D), k = (int)(g - (long long)task * D);
-    const int e0 = task_ptr[task], e1 = task_ptr[task + 1];
-    double *o = task < n ? values + (size_t)task * 2 * L * D : jac + (size_t)(task - n) * 2 * L * D;
-#pragma unroll 1
-    for (int part = 0; part < 2; part++) {
-        int eacc = ZERO_E;
-        for (int e = e0; e < e1; e++) eacc = max(eacc, epool[(size_t)ent_slot[e] * 2 * D + part * D + k]);
-        // weights up to 2^20: the sum of up to 2^11 entries stays exact; one
-        // headroom digit keeps the top accumulator digit small
-        double A[S + 1];
-        md_zero(A);
-        int cnt = 0;
-        for (int e = e0; e < e1; e++) {
-            const int slot = ent_slot[e];
-            const double w = (double)ent_w[e];
-            const int delta = eacc - epool[(size_t)slot * 2 * D + part * D + k] + 1;
-            const double *d = dpool + (size_t)slot * dig_slot_stride(S, D) + (size_t)part * S * D + k;
-#pragma unroll
-            for (int s = 0; s <= S; s++) {
-                const int src = s - delta;
-                const double v = (src >= 0 && src < S) ? d[(size_t)src * D] : 0.0;
-                A[s] = __fma_rn(w, v, A[s]);
-            }
-            if (++cnt == 1024) {
-                carry_normalize(A);
-                cnt = 0;
-            }
-        }
-        double out[L];
-        digits_to_limbs<L, S + 1>(A, eacc + 1, out);
-#pragma unroll
-        for (int p = 0; p < L; p++) o[(part * L + p) * D + k] = out[p];
-    }
-}
-
 // limbs -> digits -> limbs round trip (unit test of the staging format)
 template <int L>
 __global__ void digits_roundtrip_kernel(const double *__restrict__ x, double *__restrict__ y, int count,

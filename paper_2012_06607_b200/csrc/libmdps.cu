@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -12,9 +13,6 @@
 #include "../../include/libmdps.h"
 #include "../../include/mdps_test.h"
 #include "conv_dig.cuh"
-#include "conv_gauss.cuh"
-#include "conv_quad.cuh"
-#include "conv_single.cuh"
 #include "kernels_dig.cuh"
 #include "kernels_eft.cuh"
 #include "schedule.hpp"
@@ -79,7 +77,7 @@ struct DigGeom {
 // per block, chosen by modelled throughput — resident warps per SM (limited
 // by registers, shared memory and 64 warps), lane balance of the folded
 // triangle ((D+1) terms over F lanes) and the per-lane term count that
-// amortises the per-output epilogue.  MDPS_CONV_F / MDPS_CONV_P override.
+// amortises the per-output epilogue — unless a measured table entry exists.
 // forced geometry of the product kernel (mdps_test_force_geometry; tuning only)
 static int g_force_F = 0, g_force_P = 0;
 
@@ -99,15 +97,15 @@ static const int kTunedGeomReal[][4] = {
     {10, 64, 2, 1},
 };
 
-// tuned: 0 the model only, 1 the complex table, 2 the real table
-static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int kind, int forceF = 0,
-                        int forceP = 0, int tuned = 0) {
+// tuned: 0 the model only, 1 the complex table, 2 the real table; forceF/P > 0
+// restrict the search to that F / P
+static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int forceF = 0, int forceP = 0,
+                        int tuned = 0) {
     const int S = digits_for(L);
-    const int T = kind == 3 ? D / 4 : (D + 1) / 2;  // kind 3: quads of outputs (conv_quad.cuh)
+    const int T = (D + 1) / 2;
     DigGeom best{T, 1, 1, 32, 0};
     double best_score = -1.0;
-    const char *ef = getenv("MDPS_CONV_F"), *ep = getenv("MDPS_CONV_P");
-    if (tuned && !ef && !ep && forceF == 0 && forceP == 0) {
+    if (tuned && forceF == 0 && forceP == 0) {
         auto pick = [&](const auto &table) {
             for (const auto &t : table)
                 if (t[0] == L && t[1] == D) {
@@ -118,32 +116,21 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int 
         if (tuned == 1) pick(kTunedGeom);
         else pick(kTunedGeomReal);
     }
-    char fbuf[16], pbuf[16];
-    if (forceF > 0) {
-        snprintf(fbuf, sizeof fbuf, "%d", forceF);
-        ef = fbuf;
-    }
-    if (forceP > 0) {
-        snprintf(pbuf, sizeof pbuf, "%d", forceP);
-        ep = pbuf;
-    }
     // resident warps count up to 16 per SM; measured (profiles/r01_sweep.json
     // history): at L = 4, D >= 32 more terms per lane beat the 16th warp
     // (qd 1.03 -> 0.97 ms, d = 31 -12%, d = 63 -7%), elsewhere 16 is right
     const int warp_cap = (L == 4 && D >= 32) ? 12 : 16;
     for (int F = 1; F <= 8; F *= 2) {
-        if (ef && atoi(ef) != F) continue;
+        if (forceF > 0 && forceF != F) continue;
         for (int P = 1; P <= 32; P *= 2) {
-            if (ep && atoi(ep) != P) continue;
+            if (forceP > 0 && forceP != P) continue;
             DigGeom g;
             g.T = T;
             g.F = F;
             g.P = P;
             g.threads = (P * T * F + 31) / 32 * 32;  // whole warps (full-mask shuffles)
             if (g.threads > max_threads) continue;
-            g.smem = kind == 1 ? conv_g_smem(S, D, P, T)
-                               : kind == 2 ? conv_s_smem(S, D, P, T)
-                               : kind == 3 ? conv_q_smem(S, D, P, g.threads) : conv_dig_smem(S, D, P, g.threads);
+            g.smem = conv_dig_smem(S, D, P, g.threads);
             if (g.smem > 227 * 1024) continue;
             const int blocks_smem = (int)(228 * 1024 / (g.smem + 1024));
             const int blocks_regs = 65536 / (std::max(regs_per_thread, 32) * g.threads);
@@ -183,52 +170,45 @@ struct ConvDig {
     static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, int real,
                    cudaStream_t st) {
         if (njobs <= 0) return MDPS_OK;
-        // product kernel: 0 = two passes, one per part (conv_dig.cuh, default);
-        // opt-in variants via MDPS_CONV_KERNEL: 1 = three products per term
-        // (conv_gauss.cuh; shared-memory bound, od 72 ms vs 47 ms), 2 = one pass
-        // for both parts (conv_single.cuh; two blocks/SM, od 56 ms vs 47 ms)
-        static const int kind0 = getenv("MDPS_CONV_KERNEL") ? atoi(getenv("MDPS_CONV_KERNEL")) : 0;
-        // 3 = two outputs per lane and phase (conv_quad.cuh): D a multiple of 4, complex
-        const int kind = (kind0 == 3 && (D % 4 != 0 || real)) ? 0 : kind0;
         using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
         KernT kern;
         if (real)  // real systems: the two-pass kernel with one product per term
             kern = D == 16 ? conv_dig_kernel<L, 16, true> : D == 32 ? conv_dig_kernel<L, 32, true>
                  : D == 64 ? conv_dig_kernel<L, 64, true> : D == 128 ? conv_dig_kernel<L, 128, true>
                  : conv_dig_kernel<L, 0, true>;
-        else if (kind == 1)
-            kern = D == 16 ? conv_g_kernel<L, 16> : D == 32 ? conv_g_kernel<L, 32> : D == 64 ? conv_g_kernel<L, 64>
-                 : D == 128 ? conv_g_kernel<L, 128> : conv_g_kernel<L, 0>;
-        else if (kind == 2)
-            kern = D == 16 ? conv_s_kernel<L, 16> : D == 32 ? conv_s_kernel<L, 32> : D == 64 ? conv_s_kernel<L, 64>
-                 : D == 128 ? conv_s_kernel<L, 128> : conv_s_kernel<L, 0>;
-        else if (kind == 3)
-            kern = D == 16 ? conv_q_kernel<L, 16> : D == 32 ? conv_q_kernel<L, 32> : D == 64 ? conv_q_kernel<L, 64>
-                 : D == 128 ? conv_q_kernel<L, 128> : conv_q_kernel<L, 0>;
         else
             kern = D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> : D == 64 ? conv_dig_kernel<L, 64>
                  : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
-        // geometry per D, computed once (benign race: every writer stores the same value)
+        // geometry per (D, real), computed once per process under a lock
+        static std::mutex mu;
         static DigGeom cache[2 * 257];
         static int cregs[2 * 257], cmaxt[2 * 257];
         static bool cached[2 * 257];
         const int key = D + (real ? 257 : 0);
-        if (!cached[key]) {
-            cudaFuncAttributes fa;
-            int regs = 255, maxt = 128;
-            if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
-                regs = fa.numRegs;
-                maxt = std::min(fa.maxThreadsPerBlock, 256);
+        DigGeom g;
+        int regs, maxt;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (!cached[key]) {
+                cudaFuncAttributes fa;
+                regs = 255;
+                maxt = 128;
+                if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
+                    regs = fa.numRegs;
+                    maxt = std::min(fa.maxThreadsPerBlock, 256);
+                }
+                cregs[key] = regs;
+                cmaxt[key] = maxt;
+                cache[key] = dig_geom(L, D, regs, maxt, 0, 0, real ? 2 : 1);
+                if (cache[key].smem == 0) cache[key] = dig_geom(L, D, regs, maxt);  // tuned entry does not fit
+                cached[key] = true;
             }
-            cregs[key] = regs;
-            cmaxt[key] = maxt;
-            cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind, 0, 0, real ? 2 : (kind == 0 ? 1 : 0));
-            if (cache[key].smem == 0) cache[key] = dig_geom(L, D, regs, maxt, real ? 0 : kind);  // tuned entry does not fit
-            cached[key] = true;
+            g = cache[key];
+            regs = cregs[key];
+            maxt = cmaxt[key];
         }
-        DigGeom g = cache[key];
         if (g_force_F > 0 || g_force_P > 0) {  // tuning: a forced (F, P), checked against the limits
-            g = dig_geom(L, D, cregs[key], cmaxt[key], real ? 0 : kind, g_force_F, g_force_P);
+            g = dig_geom(L, D, regs, maxt, g_force_F, g_force_P);
             if (g.smem == 0) { set_err("forced geometry does not fit"); return MDPS_EINVAL; }
         }
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
@@ -269,7 +249,7 @@ struct mdps_system {
     int real = 0;  // mdps_options.real: every series real, one product per term
     int batch = 1; // mdps_options.batch: points per evaluation (n, N are per point)
     int use_graph = 0;
-    int64_t nslots = 0, products = 0, add_terms = 0;
+    int64_t nslots = 0, products = 0, add_terms = 0, add_terms_w = 0;  // add_terms_w: weight != 1
     std::vector<int64_t> level_off, level_cnt;  // in jobs
     int ntasks = 0;
     // device
@@ -413,6 +393,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->nslots = S.nslots;
     s->products = S.products;
     s->add_terms = (int64_t)S.ent_slot.size();
+    for (int32_t w : S.ent_w) s->add_terms_w += w != 1;
     s->ntasks = B * (S.N + S.N * n);
 
     std::vector<int32_t> alljobs;  // (in1, in2, out, code) per job, level by level
@@ -662,11 +643,10 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     out->products = s->products;
     out->add_terms = s->add_terms;
     out->fp64_ops_conv = s->products * conv_ops_per_product(s->algo, s->L, s->D) / (s->real ? 4 : 1);
-    int64_t add_ops;
-    if (s->algo == MDPS_ALGO_EFT)
-        add_ops = s->add_terms * s->D * 2 * ops_bins_add(s->L);
-    else
-        add_ops = s->add_terms * s->D * 2 * (digits_for(s->L) + 1);
+    // both algorithms sum with accum_eft_kernel (EFT bins over limb planes):
+    // bins_add per unit-weight term, bins_add_scaled per weighted one (a_l >= 2)
+    const int64_t add_ops = ((s->add_terms - s->add_terms_w) * ops_bins_add(s->L) +
+                             s->add_terms_w * ops_bins_add_scaled(s->L)) * s->D * 2;
     out->fp64_ops_total = out->fp64_ops_conv + add_ops;
     const int64_t ser = (int64_t)2 * s->L * s->D * 8;
     out->compulsory_bytes = ser * (((int64_t)s->n + s->N + (int64_t)s->N * s->n) * s->batch + s->M);

@@ -1147,9 +1147,7 @@ struct TsGeom {
         const int C = std::min(8, s->n);
         const int rows = (s->n + C - 1) / C;
         const size_t gsm = ((size_t)rows * 2 * s->n + 2 * s->n) * 16 + 16;
-        const char *env = getenv("MDPS_GJ_CLUSTER");
-        const bool want = !(env && env[0] == '0');
-        if (want && gsm <= 200 * 1024) {
+        if (gsm <= 200 * 1024) {
             bool ok = cudaFuncSetAttribute(ts::ts_gj_cluster_kernel<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)gsm) == cudaSuccess;
             if (ok && C > 8)
