@@ -137,6 +137,11 @@ typedef struct {
     int32_t digits;            /* digits per part (digits algo), else 0 */
     int32_t launches;          /* kernel launches per eval */
     size_t workspace_bytes;    /* device memory owned by the system */
+    int32_t n;                 /* variables (series_in holds batch * n series) */
+    int32_t n_polys;           /* polynomials N (values_out: batch * N, jacobian_out: batch * N * n series) */
+    int32_t degree;            /* truncation degree d (D = d + 1 coefficients) */
+    int32_t limbs;             /* L */
+    int32_t batch;             /* points per evaluation (mdps_options.batch) */
 } mdps_stats;
 
 /* Statistics of a system (for the measurement). */

@@ -54,6 +54,9 @@ def lib() -> ctypes.CDLL:
         L.mdo_eval_entries.argtypes = [i32, i32, P(i32), P(i32), P(i32), P(i32), P(d), P(d), i32, i32,
                                        i32, P(i32), P(i32), P(d), i32, P(ll)]
         L.mdo_series_err.argtypes = [P(d), P(d), i32, i32, i32, P(d)]
+        L.mdo_eval_values_weighted.argtypes = [i32, i32, P(i32), P(i32), P(i32), P(i32), P(d), P(d), i32, i32,
+                                               i32, P(i32), P(d), P(d), i32, P(ll)]
+        L.mdo_euler_residual.argtypes = [i32, i32, i32, i32, P(d), P(d), P(d), P(d), i32]
         L.mdo_toeplitz_solve.argtypes = [i32, i32, i32, P(d), P(d), P(d), P(i32), i32]
         L.mdo_toeplitz_normal.argtypes = [i32, i32, i32, i32, P(d), P(d), i32, P(d), P(d)]
         _lib = L
@@ -192,6 +195,25 @@ def eval_entries(si, entries: Sequence[Tuple[int, int]], nthreads: Optional[int]
     return out, int(prods.value)
 
 
+def values_weighted(si, rows: Sequence[int], nthreads: Optional[int] = None):
+    """(f, g) of the given rows from one set of monomial chains: f_i the
+    value, g_i = sum_r deg(r) c_r x^{a_r} the degree-weighted value (Euler's
+    identity: sum_j x_j J_ij = g_i).  Equal to eval_entries' (i, -1) and
+    (i, -2) entries bit for bit."""
+    L, D = si.limbs, si.degree + 1
+    r = _i32(list(rows))
+    f = np.zeros((len(r), 2, L, D))
+    g = np.zeros((len(r), 2, L, D))
+    prods = ctypes.c_longlong(0)
+    n_polys = int(si.poly_ptr.shape[0] - 1)
+    rc = lib().mdo_eval_values_weighted(n_polys, si.n, _ip(_i32(si.poly_ptr)), _ip(_i32(si.mono_ptr)),
+                                        _ip(_i32(si.vars)), _ip(_i32(si.exps)), _dp(_f64(si.coeffs)), _dp(_f64(si.x)),
+                                        si.degree, L, len(r), _ip(r), _dp(g), _dp(f),
+                                        nthreads or os.cpu_count() or 1, ctypes.byref(prods))
+    _check(rc, "values_weighted")
+    return f, g
+
+
 def eval_diff(si, nthreads: Optional[int] = None, limbs: Optional[int] = None):
     """Full naive evaluation: (values[n_polys][2][L][D], jac[n_polys][n][2][L][D], products)."""
     n_polys = int(si.poly_ptr.shape[0] - 1)
@@ -213,6 +235,22 @@ def series_err(a, b) -> np.ndarray:
     err = np.zeros(count)
     _check(lib().mdo_series_err(_dp(a), _dp(b), count, D, L, _dp(err)), "series_err")
     return err.reshape(lead)
+
+
+def euler_residual(x, jac_rows, g, nthreads: Optional[int] = None) -> np.ndarray:
+    """Exact Euler residual of Jacobian rows (mdoracle.c mdo_euler_residual):
+    res[c][k] = |sum_j (x_j * J_cj)_k - g_ck|, the products truncated at t^D and
+    every sum formed exactly, rounded once.  x [n][2][L][D], jac_rows
+    [count][n][2][L][D], g [count][2][L][D] (g = deg * f for a system
+    homogeneous of degree deg, else eval_entries' (i, -2) entries)."""
+    x, jac_rows, g = _f64(x), _f64(jac_rows), _f64(g)
+    n, _, L, D = x.shape
+    count = jac_rows.shape[0]
+    assert jac_rows.shape == (count, n, 2, L, D) and g.shape == (count, 2, L, D)
+    res = np.zeros((count, D))
+    _check(lib().mdo_euler_residual(count, n, D, L, _dp(x), _dp(jac_rows), _dp(g), _dp(res),
+                                    nthreads or os.cpu_count() or 1), "euler_residual")
+    return res
 
 
 # ---- block lower-triangular Toeplitz forward substitution ------------------------

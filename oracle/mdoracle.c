@@ -503,8 +503,13 @@ int mdo_series_inv(const double *x, int D, int L, double *y) {
  * (any order; multiplied in ascending variable order), coefficient series
  * coeffs[r] ([2][L][D]).  x: [n][2][L][D].
  *
- * Entry (i, j): j < 0 -> value f_i(x); j >= 0 -> J_ij = df_i/dx_j.
+ * Entry (i, j): j = -1 -> value f_i(x); j >= 0 -> J_ij = df_i/dx_j;
+ * j = -2 -> the degree-weighted value g_i(x) of Euler's identity for
+ * polynomials, sum_j x_j df_i/dx_j = sum_r deg(r) c_r x^{a_r} (every monomial
+ * is homogeneous of its own degree deg(r) = sum_l a_l), used to check whole
+ * Jacobian rows (mdo_euler_residual below).
  *   f_i  = RN_L( sum_r  c_r * prod_l x_{v_l}^{a_l} )
+ *   g_i  = RN_L( sum_r  deg(r) * (c_r * prod_l x_{v_l}^{a_l}) )
  *   J_ij = RN_L( sum_{r : j in r}  a_j * c_r * x^{a_r - e_j} )
  * with every series product in the chains rounded to L limbs.
  * ------------------------------------------------------------------------- */
@@ -515,6 +520,7 @@ typedef struct {
     int n_entries;
     const int *rows, *cols;
     double *out; /* [n_entries][2][L][D] */
+    double *out_f; /* optional, for (i, -2) entries: f_i from the same chains */
     /* job queue: counter guarded by a binary semaphore */
     pthread_mutex_t lock;
     int next;
@@ -535,7 +541,7 @@ static int mono_order(const job_t *J, int r, int *idx) {
 }
 
 static void run_entry(job_t *J, int e, double *t0, double *t1, sa_t *acc, sa_t *sr, sa_t *si,
-                      dser_t *dx, dser_t *dy) {
+                      dser_t *dx, dser_t *dy, sa_t *acc_f) {
     int i = J->rows[e], jcol = J->cols[e], D = J->D, L = J->L;
     size_t SS = (size_t)2 * L * D;
     long long prods = 0;
@@ -548,6 +554,10 @@ static void run_entry(job_t *J, int e, double *t0, double *t1, sa_t *acc, sa_t *
             for (int t = 0; t < m; t++)
                 if (J->vars[idx[t]] == jcol) { found = 1; weight = J->exps[idx[t]]; }
             if (!found) continue;
+        } else if (jcol == -2) {
+            weight = 0;
+            for (int t = 0; t < m; t++) weight += J->exps[idx[t]];
+            if (weight == 0 && !J->out_f) continue; /* a constant term has degree 0 (but is part of f) */
         }
         /* chain: t = c_r; then multiply by each factor left to right */
         memcpy(t0, J->coeffs + (size_t)r * SS, SS * sizeof(double));
@@ -569,13 +579,19 @@ static void run_entry(job_t *J, int e, double *t0, double *t1, sa_t *acc, sa_t *
                         int neg, ex;
                         uint64_t mm;
                         dec(v, &neg, &mm, &ex);
-                        sa_dep(&acc[part * D + k], neg, (u128)mm * (u128)weight, ex);
+                        if (weight) sa_dep(&acc[part * D + k], neg, (u128)mm * (u128)weight, ex);
+                        if (jcol == -2 && J->out_f) sa_dep(&acc_f[part * D + k], neg, (u128)mm, ex);
                     }
                 }
     }
     double *o = J->out + (size_t)e * SS;
     for (int part = 0; part < 2; part++)
         for (int k = 0; k < D; k++) sa_round_limbs(&acc[part * D + k], L, &o[SIDX(part, 0, k, L, D)], D);
+    if (jcol == -2 && J->out_f) {
+        double *of = J->out_f + (size_t)e * SS;
+        for (int part = 0; part < 2; part++)
+            for (int k = 0; k < D; k++) sa_round_limbs(&acc_f[part * D + k], L, &of[SIDX(part, 0, k, L, D)], D);
+    }
     pthread_mutex_lock(&J->lock);
     J->products += prods;
     pthread_mutex_unlock(&J->lock);
@@ -586,8 +602,8 @@ static void *worker(void *arg) {
     size_t SS = (size_t)2 * J->L * J->D;
     double *t0 = (double *)malloc(SS * sizeof(double));
     double *t1 = (double *)malloc(SS * sizeof(double));
-    sa_t *acc = (sa_t *)malloc(sizeof(sa_t) * (size_t)(2 * J->D + 2));
-    for (int t = 0; t < 2 * J->D + 2; t++) sa_init(&acc[t]);
+    sa_t *acc = (sa_t *)malloc(sizeof(sa_t) * (size_t)(4 * J->D + 2));
+    for (int t = 0; t < 4 * J->D + 2; t++) sa_init(&acc[t]);
     dser_t dx, dy;
     dser_alloc(&dx, SS);
     dser_alloc(&dy, SS);
@@ -597,7 +613,7 @@ static void *worker(void *arg) {
         int e = J->next++;            /* take the next job */
         pthread_mutex_unlock(&J->lock);
         if (e >= J->n_entries) break;
-        run_entry(J, e, t0, t1, acc, &acc[2 * J->D], &acc[2 * J->D + 1], &dx, &dy);
+        run_entry(J, e, t0, t1, acc, &acc[2 * J->D], &acc[2 * J->D + 1], &dx, &dy, &acc[2 * J->D + 2]);
     }
     if (g_err) {
         pthread_mutex_lock(&J->lock);
@@ -612,14 +628,13 @@ static void *worker(void *arg) {
     return NULL;
 }
 
-/* returns 0, or <0 on error; *products (optional) = series products computed */
-int mdo_eval_entries(int n_polys, int n, const int *poly_ptr, const int *mono_ptr, const int *vars,
-                     const int *exps, const double *coeffs, const double *x, int degree, int L,
-                     int n_entries, const int *rows, const int *cols, double *out, int nthreads,
-                     long long *products) {
+static int eval_entries_impl(int n_polys, int n, const int *poly_ptr, const int *mono_ptr, const int *vars,
+                             const int *exps, const double *coeffs, const double *x, int degree, int L,
+                             int n_entries, const int *rows, const int *cols, double *out, double *out_f,
+                             int nthreads, long long *products) {
     if (L < 1 || L > MDO_MAXL || degree < 0 || n < 1) return -3;
     for (int e = 0; e < n_entries; e++)
-        if (rows[e] < 0 || rows[e] >= n_polys || cols[e] >= n) return -3;
+        if (rows[e] < 0 || rows[e] >= n_polys || cols[e] >= n || cols[e] < -2) return -3;
     for (int r = 0; r < poly_ptr[n_polys]; r++)
         if (mono_ptr[r + 1] - mono_ptr[r] > 4096) return -3;
     job_t J;
@@ -627,6 +642,7 @@ int mdo_eval_entries(int n_polys, int n, const int *poly_ptr, const int *mono_pt
     J.n_polys = n_polys; J.n = n; J.D = degree + 1; J.L = L;
     J.poly_ptr = poly_ptr; J.mono_ptr = mono_ptr; J.vars = vars; J.exps = exps;
     J.coeffs = coeffs; J.x = x; J.n_entries = n_entries; J.rows = rows; J.cols = cols; J.out = out;
+    J.out_f = out_f;
     pthread_mutex_init(&J.lock, NULL);
     if (nthreads < 1) nthreads = 1;
     if (nthreads > n_entries) nthreads = n_entries > 0 ? n_entries : 1;
@@ -637,6 +653,31 @@ int mdo_eval_entries(int n_polys, int n, const int *poly_ptr, const int *mono_pt
     pthread_mutex_destroy(&J.lock);
     if (products) *products = J.products;
     return J.err ? -1 : 0;
+}
+
+/* returns 0, or <0 on error; *products (optional) = series products computed */
+int mdo_eval_entries(int n_polys, int n, const int *poly_ptr, const int *mono_ptr, const int *vars,
+                     const int *exps, const double *coeffs, const double *x, int degree, int L,
+                     int n_entries, const int *rows, const int *cols, double *out, int nthreads,
+                     long long *products) {
+    return eval_entries_impl(n_polys, n, poly_ptr, mono_ptr, vars, exps, coeffs, x, degree, L, n_entries, rows,
+                             cols, out, NULL, nthreads, products);
+}
+
+/* both f_i and g_i of the given rows from ONE set of monomial chains (the
+ * Euler check of non-homogeneous systems): out_g[e] = entry (rows[e], -2),
+ * out_f[e] = entry (rows[e], -1), bit for bit. */
+int mdo_eval_values_weighted(int n_polys, int n, const int *poly_ptr, const int *mono_ptr, const int *vars,
+                             const int *exps, const double *coeffs, const double *x, int degree, int L,
+                             int count, const int *rows, double *out_g, double *out_f, int nthreads,
+                             long long *products) {
+    int *cols = (int *)malloc(sizeof(int) * (size_t)(count > 0 ? count : 1));
+    if (!cols) return -2;
+    for (int e = 0; e < count; e++) cols[e] = -2;
+    int rc = eval_entries_impl(n_polys, n, poly_ptr, mono_ptr, vars, exps, coeffs, x, degree, L, count, rows, cols,
+                               out_g, out_f, nthreads, products);
+    free(cols);
+    return rc;
 }
 
 /* ---------------------------------------------------------------------------
@@ -673,6 +714,95 @@ int mdo_series_err(const double *a, const double *b, int count, int D, int L, do
         err[c] = maxd / (maxb > 1.0 ? maxb : 1.0);
     }
     return g_err ? -1 : 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Euler residual of a Jacobian row (test metric for full-size outputs;
+ * SURVEY §8(c) C3 "eval/diff identities", R19).  For every
+ * polynomial f, Euler's identity for the homogeneous parts gives
+ *     sum_j x_j * df/dx_j = sum_r deg(r) c_r x^{a_r} =: g,
+ * truncated at t^D like every product.  For row c:
+ *     r_{c,k} = sum_j sum_{q<=k} x_{j,q} J_{c,j,k-q}  -  g_{c,k}
+ * formed EXACTLY (every limb product in the superaccumulator), then rounded
+ * to one double per part; res[c][k] = |r_{c,k}| (complex modulus).
+ * x: [n][2][L][D]; J: [count][n][2][L][D]; g: [count][2][L][D];
+ * res: [count][D].  Rows are jobs claimed from a counter (nthreads workers).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    int count, n, D, L;
+    const double *x, *J, *g;
+    double *res;
+    pthread_mutex_t lock;
+    int next, err;
+} euler_t;
+
+static void *euler_worker(void *arg) {
+    euler_t *E = (euler_t *)arg;
+    int n = E->n, D = E->D, L = E->L;
+    size_t SS = (size_t)2 * L * D;
+    sa_t *acc = (sa_t *)malloc(sizeof(sa_t) * (size_t)(2 * D));
+    dser_t dx, dj;
+    int ok = acc && dser_alloc(&dx, SS * (size_t)n) == 0 && dser_alloc(&dj, SS * (size_t)n) == 0;
+    g_err = 0;
+    if (ok) dser_fill(&dx, E->x, SS * (size_t)n);
+    for (;;) {
+        pthread_mutex_lock(&E->lock);
+        int c = E->next++;
+        pthread_mutex_unlock(&E->lock);
+        if (c >= E->count || !ok) break;
+        for (int t = 0; t < 2 * D; t++) sa_init(&acc[t]);
+        const double *Jc = E->J + (size_t)c * n * SS, *gc = E->g + (size_t)c * SS;
+        dser_fill(&dj, Jc, SS * (size_t)n);
+        for (int j = 0; j < n; j++) {
+            size_t xo = (size_t)j * SS, jo = (size_t)j * SS;
+            for (int k = 0; k < D; k++)
+                for (int q = 0; q <= k; q++)
+                    for (int p = 0; p < L; p++) {
+                        size_t xr = xo + SIDX(0, p, q, L, D), xi = xo + SIDX(1, p, q, L, D);
+                        for (int u = 0; u < L; u++) {
+                            size_t yr = jo + SIDX(0, u, k - q, L, D), yi = jo + SIDX(1, u, k - q, L, D);
+                            sa_dep_mm(&acc[k], dx.m[xr], dx.e[xr], dj.m[yr], dj.e[yr], 0);     /* re += a c */
+                            sa_dep_mm(&acc[k], dx.m[xi], dx.e[xi], dj.m[yi], dj.e[yi], 1);     /* re -= b d */
+                            sa_dep_mm(&acc[D + k], dx.m[xr], dx.e[xr], dj.m[yi], dj.e[yi], 0); /* im += a d */
+                            sa_dep_mm(&acc[D + k], dx.m[xi], dx.e[xi], dj.m[yr], dj.e[yr], 0); /* im += b c */
+                        }
+                    }
+        }
+        for (int k = 0; k < D; k++) {
+            double part[2];
+            for (int pt = 0; pt < 2; pt++) {
+                for (int p = 0; p < L; p++) sa_add_double(&acc[pt * D + k], -gc[SIDX(pt, p, k, L, D)]);
+                part[pt] = sa_rn(&acc[pt * D + k]);
+            }
+            E->res[(size_t)c * D + k] = hypot(part[0], part[1]);
+        }
+    }
+    if (g_err || !ok) {
+        pthread_mutex_lock(&E->lock);
+        E->err = 1;
+        pthread_mutex_unlock(&E->lock);
+    }
+    if (ok) { dser_free(&dx); dser_free(&dj); }
+    free(acc);
+    return NULL;
+}
+
+int mdo_euler_residual(int count, int n, int D, int L, const double *x, const double *J, const double *g,
+                       double *res, int nthreads) {
+    if (count < 0 || n < 1 || D < 1 || L < 1 || L > MDO_MAXL) return -3;
+    if (count == 0) return 0;
+    euler_t E;
+    memset(&E, 0, sizeof E);
+    E.count = count; E.n = n; E.D = D; E.L = L; E.x = x; E.J = J; E.g = g; E.res = res;
+    pthread_mutex_init(&E.lock, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > count) nthreads = count;
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, euler_worker, &E);
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    free(th);
+    pthread_mutex_destroy(&E.lock);
+    return E.err ? -1 : 0;
 }
 
 /* ---------------------------------------------------------------------------

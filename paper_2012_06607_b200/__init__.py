@@ -58,7 +58,8 @@ class Stats(ctypes.Structure):
                 ("fp64_ops_conv", ctypes.c_int64), ("fp64_ops_total", ctypes.c_int64),
                 ("compulsory_bytes", ctypes.c_int64), ("levels", ctypes.c_int32),
                 ("algo", ctypes.c_int32), ("digits", ctypes.c_int32), ("launches", ctypes.c_int32),
-                ("workspace_bytes", ctypes.c_size_t)]
+                ("workspace_bytes", ctypes.c_size_t), ("n", ctypes.c_int32), ("n_polys", ctypes.c_int32),
+                ("degree", ctypes.c_int32), ("limbs", ctypes.c_int32), ("batch", ctypes.c_int32)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -156,12 +157,32 @@ def _stream_handle(stream) -> int:
     return stream.cuda_stream
 
 
-def _dptr(t) -> int:
-    """device pointer of a torch CUDA float64 contiguous tensor."""
+def _dptr(t, numel: Optional[int] = None, device: Optional[int] = None, name: str = "tensor") -> int:
+    """device pointer of a torch CUDA float64 contiguous tensor; with `numel`
+    and `device` given, its size and device are checked first (the C ABI only
+    sees the pointer: a short buffer would be overrun by the kernels)."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-        raise MdpsError("expected a contiguous float64 CUDA tensor")
+        raise MdpsError(f"{name}: expected a contiguous float64 CUDA tensor")
+    if numel is not None and t.numel() != numel:
+        raise MdpsError(f"{name}: expected {numel} doubles, got {t.numel()} (shape {tuple(t.shape)})")
+    if device is not None and t.device.index != device:
+        raise MdpsError(f"{name}: on cuda:{t.device.index}, the object lives on cuda:{device}")
     return t.data_ptr()
+
+
+def _hptr(a: np.ndarray, numel: int, name: str) -> int:
+    """host pointer of a C-contiguous float64 numpy array of exactly `numel` doubles."""
+    if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
+        raise MdpsError(f"{name}: expected a C-contiguous float64 host array")
+    if a.size != numel:
+        raise MdpsError(f"{name}: expected {numel} doubles, got {a.size} (shape {a.shape})")
+    return a.ctypes.data
+
+
+def _current_device() -> int:
+    import torch
+    return torch.cuda.current_device()
 
 
 def mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n: int, degree: int,
@@ -180,20 +201,28 @@ def mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n: in
     return h
 
 
-def mdps_eval_diff(handle: int, series_in, values_out, jacobian_out, stream=None) -> None:
-    """Asynchronous eval/diff on device tensors (libmdps.h)."""
-    _check(lib().mdps_eval_diff(handle, _dptr(series_in), _dptr(values_out), _dptr(jacobian_out),
+def _sizes(handle: int):
+    """(doubles of series_in, values_out, jacobian_out) of a system, from its stats."""
+    st = mdps_system_stats(handle)
+    return st["in_doubles"], st["values_doubles"], st["jacobian_doubles"]
+
+
+def mdps_eval_diff(handle: int, series_in, values_out, jacobian_out, stream=None, device=None) -> None:
+    """Asynchronous eval/diff on device tensors (libmdps.h); sizes and device checked."""
+    nin, nval, njac = _sizes(handle)
+    _check(lib().mdps_eval_diff(handle, _dptr(series_in, nin, device, "series_in"),
+                                _dptr(values_out, nval, device, "values_out"),
+                                _dptr(jacobian_out, njac, device, "jacobian_out"),
                                 _stream_handle(stream)), "mdps_eval_diff")
 
 
 def mdps_eval_diff_host(handle: int, series_in: np.ndarray, values_out: np.ndarray,
                         jacobian_out: np.ndarray, stream=None) -> None:
-    """End-to-end eval/diff with HOST numpy buffers (synchronous)."""
-    for a in (series_in, values_out, jacobian_out):
-        if not (a.dtype == np.float64 and a.flags["C_CONTIGUOUS"]):
-            raise MdpsError("expected C-contiguous float64 host arrays")
-    _check(lib().mdps_eval_diff_host(handle, series_in.ctypes.data, values_out.ctypes.data,
-                                     jacobian_out.ctypes.data, _stream_handle(stream)),
+    """End-to-end eval/diff with HOST numpy buffers (synchronous); sizes checked."""
+    nin, nval, njac = _sizes(handle)
+    _check(lib().mdps_eval_diff_host(handle, _hptr(series_in, nin, "series_in"),
+                                     _hptr(values_out, nval, "values_out"),
+                                     _hptr(jacobian_out, njac, "jacobian_out"), _stream_handle(stream)),
            "mdps_eval_diff_host")
 
 
@@ -204,7 +233,12 @@ def mdps_system_destroy(handle: int) -> None:
 def mdps_system_stats(handle: int) -> dict:
     st = Stats()
     _check(lib().mdps_system_stats(handle, ctypes.byref(st)), "mdps_system_stats")
-    return st.as_dict()
+    d = st.as_dict()
+    ser = 2 * d["limbs"] * (d["degree"] + 1)
+    d["in_doubles"] = d["batch"] * d["n"] * ser
+    d["values_doubles"] = d["batch"] * d["n_polys"] * ser
+    d["jacobian_doubles"] = d["batch"] * d["n_polys"] * d["n"] * ser
+    return d
 
 
 class System:
@@ -217,6 +251,7 @@ class System:
         self.batch = int(batch)
         self.handle = mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n,
                                          degree, limbs, algo, use_graph, real, batch)
+        self.device = _current_device()  # the library allocated on the current device
 
     @classmethod
     def from_inputs(cls, si, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False,
@@ -238,7 +273,7 @@ class System:
         if jacobian_out is None:
             jacobian_out = torch.empty(lead + (self.n_polys, self.n) + self.series_shape, dtype=torch.float64,
                                        device=series_in.device)
-        mdps_eval_diff(self.handle, series_in, values_out, jacobian_out, stream)
+        mdps_eval_diff(self.handle, series_in, values_out, jacobian_out, stream, self.device)
         return values_out, jacobian_out
 
     def eval_diff_host(self, series_in: np.ndarray, stream=None):
@@ -294,27 +329,35 @@ class Solver:
         self.handle = lib().mdps_solver_create_ls(self.n_eqs, self.n, self.degree, self.limbs)
         if not self.handle:
             raise MdpsError(f"mdps_solver_create failed: {mdps_last_error()}")
+        self.device = _current_device()
 
     def solve(self, jacobian, rhs, dx_out=None, stream=None):
         import torch
         if dx_out is None:
             dx_out = torch.empty((self.n, 2, self.limbs, self.degree + 1), dtype=torch.float64,
                                  device=rhs.device)
-        _check(lib().mdps_solve(self.handle, _dptr(jacobian), _dptr(rhs), _dptr(dx_out), _stream_handle(stream)),
+        ser = 2 * self.limbs * (self.degree + 1)
+        _check(lib().mdps_solve(self.handle, _dptr(jacobian, self.n_eqs * self.n * ser, self.device, "jacobian"),
+                                _dptr(rhs, self.n_eqs * ser, self.device, "rhs"),
+                                _dptr(dx_out, self.n * ser, self.device, "dx_out"), _stream_handle(stream)),
                "mdps_solve")
         return dx_out
 
     def newton_step(self, system: "System", x, dx_out=None, norm_out=None, stream=None):
         """x <- x + dx with J dx = -f at x (asynchronous; device tensors)."""
-        _check(lib().mdps_newton_step(system.handle, self.handle, _dptr(x),
-                                      _dptr(dx_out) if dx_out is not None else None,
-                                      _dptr(norm_out) if norm_out is not None else None, _stream_handle(stream)),
+        ser = 2 * self.limbs * (self.degree + 1)
+        _check(lib().mdps_newton_step(system.handle, self.handle, _dptr(x, self.n * ser, self.device, "x"),
+                                      _dptr(dx_out, self.n * ser, self.device, "dx_out") if dx_out is not None
+                                      else None,
+                                      _dptr(norm_out, 1, self.device, "norm_out") if norm_out is not None else None,
+                                      _stream_handle(stream)),
                "mdps_newton_step")
 
     def newton(self, system: "System", x, max_iters: int, tol: float, stream=None):
         """Newton's method in place on x; returns (steps, last update norm)."""
         norm = ctypes.c_double(0.0)
-        rc = lib().mdps_newton(system.handle, self.handle, _dptr(x), int(max_iters), float(tol), ctypes.byref(norm),
+        ser = 2 * self.limbs * (self.degree + 1)
+        rc = lib().mdps_newton(system.handle, self.handle, _dptr(x, self.n * ser, self.device, "x"), int(max_iters), float(tol), ctypes.byref(norm),
                                _stream_handle(stream))
         if rc < 0:
             raise MdpsError(f"mdps_newton failed (rc={rc}): {mdps_last_error()}")

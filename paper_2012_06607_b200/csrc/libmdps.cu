@@ -655,6 +655,11 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     out->digits = s->S;
     out->launches = (int32_t)s->level_cnt.size() + 2;
     out->workspace_bytes = s->device_bytes;
+    out->n = s->n;
+    out->n_polys = s->N;
+    out->degree = s->D - 1;
+    out->limbs = s->L;
+    out->batch = s->batch;
     return MDPS_OK;
 }
 

@@ -108,3 +108,32 @@ def test_constant_series_inputs(algo, L):
     ov, oj, _ = oracle.eval_diff(si)
     assert oracle.series_err(vals, ov).max() <= TOL[L]
     assert oracle.series_err(jac, oj).max() <= TOL[L]
+
+
+def test_binding_rejects_wrong_buffers():
+    """The binding checks sizes, dtype and device before the C ABI (which only
+    sees pointers): a short output, a wrong-size input or host array raises
+    MdpsError instead of letting the kernels or the copies overrun memory."""
+    import torch
+    import paper_2012_06607_b200 as mdps
+    si = mdinputs.random_system(740, n=3, monos=4, m_range=(1, 3), exps=(1,), degree=7, limbs=2)
+    with mdps.System.from_inputs(si) as s:
+        x = torch.from_numpy(si.x).cuda()
+        vals, jac = s.eval_diff(x)
+        with pytest.raises(mdps.MdpsError, match="values_out"):
+            s.eval_diff(x, vals[:-1].contiguous(), jac)
+        with pytest.raises(mdps.MdpsError, match="jacobian_out"):
+            s.eval_diff(x, vals, jac.reshape(-1)[:-1].contiguous())
+        with pytest.raises(mdps.MdpsError, match="series_in"):
+            s.eval_diff(x[:2].contiguous(), vals, jac)
+        with pytest.raises(mdps.MdpsError, match="float64"):
+            s.eval_diff(x.float(), vals, jac)
+        with pytest.raises(mdps.MdpsError, match="series_in"):
+            mdps.mdps_eval_diff_host(s.handle, si.x[:2].copy(), np.empty(vals.shape), np.empty(jac.shape))
+        with pytest.raises(mdps.MdpsError, match="jacobian_out"):
+            mdps.mdps_eval_diff_host(s.handle, si.x, np.empty(vals.shape), np.empty(jac.shape)[:-1].copy())
+    with mdps.Solver(3, 7, 2) as sol:
+        with pytest.raises(mdps.MdpsError, match="rhs"):
+            sol.solve(jac, vals[:2].contiguous())
+        with pytest.raises(mdps.MdpsError, match="jacobian"):
+            sol.solve(jac[:2].contiguous(), vals)

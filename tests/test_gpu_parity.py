@@ -14,7 +14,7 @@ import pytest
 import mdinputs
 import oracle
 from tests.exact import greedy, value
-from tests.gpu_util import TOL, check_against_oracle, gpu_eval, sample_entries, structural_support
+from tests.gpu_util import TOL, check_against_oracle, euler_check, gpu_eval, sample_entries, structural_support
 
 pytestmark = pytest.mark.gpu
 LEVELS = (2, 3, 4, 5, 8, 10)
@@ -213,8 +213,10 @@ def test_config_sampled(mdps, name, nv, nj):
 @pytest.mark.parametrize("d", mdinputs.SWEEP_DEGREES)
 def test_sweep_cells(mdps, d):
     """BASELINE config 4: the fixed system at d x L; one sampled Jacobian entry
-    and (small cells) one value per cell; Euler's identity (all monomials have
-    degree 8) on the value row of the smallest cells."""
+    and (small cells) one value per cell against the oracle; EVERY output of
+    every cell through Euler's identity on all 64 rows (all monomials have
+    degree 8: sum_j x_j J_ij = 8 f_i, the residual formed exactly by the
+    oracle, tests/gpu_util.euler_check)."""
     for L in mdinputs.SWEEP_LIMBS:
         si = mdinputs.sweep_cell(d, L)
         # the default (EFT for L = 2 and L = 3 up to d = 31 here, digits
@@ -227,6 +229,7 @@ def test_sweep_cells(mdps, d):
             nv = 1 if d * L <= 63 * 4 else 0
             err, _ = check_against_oracle(si, vals, jac, sample_entries(si, nv, 1, seed=d + L), TOL[L])
             assert err <= TOL[L], (d, L, algo, err)
+            euler_check(si, vals, jac, TOL[L])
 
 
 def test_graph_and_stream_paths(mdps):
