@@ -79,7 +79,17 @@ typedef struct {
                             [batch][N][...], jacobian_out [batch][N][n][...] —
                             in one launch per level (small systems fill the GPU;
                             mdps_newton_step needs batch = 1) */
+    int32_t schedule;    /* MDPS_SCHED_*: how the product and addition jobs are run */
 } mdps_options;
+
+/* Job scheduling (PAPER.md:367-378 job queue, 411-424 stages). */
+#define MDPS_SCHED_AUTO 0    /* default: QUEUE for small systems on the EFT algorithm
+                                (<= MDPS_QUEUE_MAX_PRODUCTS product jobs per call), else LEVELS */
+#define MDPS_SCHED_LEVELS 1  /* one launch per DAG level, then one for the addition jobs */
+#define MDPS_SCHED_QUEUE 2   /* one persistent launch: blocks claim jobs from a device
+                                counter in topological order and wait on per-series ready
+                                flags (EFT algorithm only) */
+#define MDPS_QUEUE_MAX_PRODUCTS 8192
 
 /* Create a system.  exponents: HOST [nnz] aligned with
  * vars, each >= 1.  coefficients: HOST [M][2][limbs][degree+1], the series
@@ -142,6 +152,7 @@ typedef struct {
     int32_t degree;            /* truncation degree d (D = d + 1 coefficients) */
     int32_t limbs;             /* L */
     int32_t batch;             /* points per evaluation (mdps_options.batch) */
+    int32_t schedule;          /* MDPS_SCHED_LEVELS or MDPS_SCHED_QUEUE (as resolved at create) */
 } mdps_stats;
 
 /* Statistics of a system (for the measurement). */

@@ -17,13 +17,14 @@ import numpy as np
 
 __all__ = [
     "MDPS_OK", "MDPS_EINVAL", "MDPS_ENOMEM", "MDPS_ECUDA", "MDPS_ALGO_AUTO", "MDPS_ALGO_EFT",
-    "MDPS_ALGO_DIGITS", "MdpsError", "lib", "library_path", "System",
+    "MDPS_ALGO_DIGITS", "MDPS_SCHED_AUTO", "MDPS_SCHED_LEVELS", "MDPS_SCHED_QUEUE", "MdpsError", "lib", "library_path", "System",
     "mdps_system_create", "mdps_eval_diff", "mdps_eval_diff_host", "mdps_system_destroy",
     "mdps_last_error", "mdps_system_stats", "EXPORTED_SYMBOLS", "Solver",
 ]
 
 MDPS_OK, MDPS_EINVAL, MDPS_ENOMEM, MDPS_ECUDA = 0, -1, -2, -3
 MDPS_ALGO_AUTO, MDPS_ALGO_EFT, MDPS_ALGO_DIGITS = 0, 1, 2
+MDPS_SCHED_AUTO, MDPS_SCHED_LEVELS, MDPS_SCHED_QUEUE = 0, 1, 2
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 library_path = os.path.join(_HERE, "libmdps.so")
@@ -50,7 +51,7 @@ class _Supports(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("real", ctypes.c_int32),
-                ("batch", ctypes.c_int32)]
+                ("batch", ctypes.c_int32), ("schedule", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -59,7 +60,8 @@ class Stats(ctypes.Structure):
                 ("compulsory_bytes", ctypes.c_int64), ("levels", ctypes.c_int32),
                 ("algo", ctypes.c_int32), ("digits", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("workspace_bytes", ctypes.c_size_t), ("n", ctypes.c_int32), ("n_polys", ctypes.c_int32),
-                ("degree", ctypes.c_int32), ("limbs", ctypes.c_int32), ("batch", ctypes.c_int32)]
+                ("degree", ctypes.c_int32), ("limbs", ctypes.c_int32), ("batch", ctypes.c_int32),
+                ("schedule", ctypes.c_int32)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -187,12 +189,12 @@ def _current_device() -> int:
 
 def mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n: int, degree: int,
                        limbs: int, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False,
-                       batch: int = 1) -> int:
+                       batch: int = 1, schedule: int = MDPS_SCHED_AUTO) -> int:
     """Create a system; returns the opaque handle (int).  Host numpy inputs."""
     pp, mp, vv, ee = _i32(poly_ptr), _i32(mono_ptr), _i32(vars_), _i32(exponents)
     coeffs = np.ascontiguousarray(np.asarray(coefficients, dtype=np.float64))
     sup = _Supports(len(pp) - 1, _ptr_i32(pp), _ptr_i32(mp), _ptr_i32(vv))
-    opts = _Options(algo, 1 if use_graph else 0, 1 if real else 0, int(batch))
+    opts = _Options(algo, 1 if use_graph else 0, 1 if real else 0, int(batch), int(schedule))
     h = lib().mdps_system_create_ex(ctypes.byref(sup), _ptr_i32(ee),
                                     coeffs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                     n, degree, limbs, ctypes.byref(opts))
@@ -245,20 +247,21 @@ class System:
     """RAII wrapper: a polynomial system on the device (see libmdps.h)."""
 
     def __init__(self, poly_ptr, mono_ptr, vars_, exponents, coefficients, n, degree, limbs,
-                 algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False, batch: int = 1):
+                 algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False, batch: int = 1,
+                 schedule: int = MDPS_SCHED_AUTO):
         self.n, self.degree, self.limbs = int(n), int(degree), int(limbs)
         self.n_polys = int(len(poly_ptr) - 1)
         self.batch = int(batch)
         self.handle = mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n,
-                                         degree, limbs, algo, use_graph, real, batch)
+                                         degree, limbs, algo, use_graph, real, batch, schedule)
         self.device = _current_device()  # the library allocated on the current device
 
     @classmethod
     def from_inputs(cls, si, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False,
-                    batch: int = 1) -> "System":
+                    batch: int = 1, schedule: int = MDPS_SCHED_AUTO) -> "System":
         """From an mdinputs.SystemInputs-like object (poly_ptr, mono_ptr, vars, exps, coeffs)."""
         return cls(si.poly_ptr, si.mono_ptr, si.vars, si.exps, si.coeffs, si.n, si.degree, si.limbs,
-                   algo, use_graph, real, batch)
+                   algo, use_graph, real, batch, schedule)
 
     @property
     def series_shape(self):
@@ -345,9 +348,10 @@ class Solver:
 
     def newton_step(self, system: "System", x, dx_out=None, norm_out=None, stream=None):
         """x <- x + dx with J dx = -f at x (asynchronous; device tensors)."""
-        ser = 2 * self.limbs * (self.degree + 1)
-        _check(lib().mdps_newton_step(system.handle, self.handle, _dptr(x, self.n * ser, self.device, "x"),
-                                      _dptr(dx_out, self.n * ser, self.device, "dx_out") if dx_out is not None
+        # sizes from the system (a system/solver shape mismatch is the library's to report)
+        nx = system.n * 2 * system.limbs * (system.degree + 1)
+        _check(lib().mdps_newton_step(system.handle, self.handle, _dptr(x, nx, system.device, "x"),
+                                      _dptr(dx_out, nx, system.device, "dx_out") if dx_out is not None
                                       else None,
                                       _dptr(norm_out, 1, self.device, "norm_out") if norm_out is not None else None,
                                       _stream_handle(stream)),
@@ -356,8 +360,8 @@ class Solver:
     def newton(self, system: "System", x, max_iters: int, tol: float, stream=None):
         """Newton's method in place on x; returns (steps, last update norm)."""
         norm = ctypes.c_double(0.0)
-        ser = 2 * self.limbs * (self.degree + 1)
-        rc = lib().mdps_newton(system.handle, self.handle, _dptr(x, self.n * ser, self.device, "x"), int(max_iters), float(tol), ctypes.byref(norm),
+        nx = system.n * 2 * system.limbs * (system.degree + 1)
+        rc = lib().mdps_newton(system.handle, self.handle, _dptr(x, nx, system.device, "x"), int(max_iters), float(tol), ctypes.byref(norm),
                                _stream_handle(stream))
         if rc < 0:
             raise MdpsError(f"mdps_newton failed (rc={rc}): {mdps_last_error()}")

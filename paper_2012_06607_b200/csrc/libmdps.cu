@@ -15,6 +15,7 @@
 #include "conv_dig.cuh"
 #include "kernels_dig.cuh"
 #include "kernels_eft.cuh"
+#include "queue_eft.cuh"
 #include "schedule.hpp"
 
 using namespace mdps;
@@ -219,6 +220,51 @@ struct ConvDig {
     }
 };
 
+// the device-side job queue (queue_eft.cuh): one persistent launch
+struct QueueGeom {
+    int F, threads, blocks, tasks_per_ticket;
+    size_t smem;
+};
+
+template <int L>
+struct QueueEft {
+    static int geom(int D, int njobs, int ntasks, QueueGeom &g) {
+        g.F = queue_lanes(D);
+        g.threads = (2 * ((D + 1) / 2) * g.F + 31) / 32 * 32;
+        g.tasks_per_ticket = std::max(1, g.threads / D);
+        g.smem = (size_t)2 * (2 * L * D) * sizeof(double);
+        auto kern = queue_eft_kernel<L>;
+        if (g.smem > 48 * 1024 &&
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem) != cudaSuccess) {
+            cudaGetLastError();
+            set_err("queue kernel: shared memory does not fit");
+            return MDPS_EINVAL;
+        }
+        int dev = 0, sms = 0, per = 0;
+        CUDA_TRY(cudaGetDevice(&dev), MDPS_ECUDA);
+        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), MDPS_ECUDA);
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, g.threads, g.smem), MDPS_ECUDA);
+        if (per < 1) { set_err("queue kernel does not fit on an SM"); return MDPS_EINVAL; }
+        const long long tickets = (long long)njobs + (ntasks + g.tasks_per_ticket - 1) / g.tasks_per_ticket;
+        g.blocks = (int)std::max(1LL, std::min<long long>(tickets, (long long)sms * per));
+        return MDPS_OK;
+    }
+    static int run(const QueueGeom &g, const double *x_in, double *pool, unsigned *flags, QueueCtl *ctl,
+                   const int *jobs, int njobs, const int *tp, const int *es, const int *ew, int ntasks, int nvals,
+                   int nx, int nready, int D, double *values, double *jac, cudaStream_t st) {
+        queue_eft_kernel<L><<<g.blocks, g.threads, g.smem, st>>>(x_in, pool, flags, ctl, jobs, njobs, tp, es, ew,
+                                                                  ntasks, nvals, g.tasks_per_ticket, nx, nready, D,
+                                                                  g.F, values, jac);
+        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
+        return MDPS_OK;
+    }
+};
+
+template <int L>
+struct QueueGeomFn {
+    static int run(int D, int njobs, int ntasks, QueueGeom &g) { return QueueEft<L>::geom(D, njobs, ntasks, g); }
+};
+
 template <int L>
 struct AccumEft {
     static int run(const double *pool, const int *tp, const int *es, const int *ew, int ntasks, int n, int D,
@@ -249,6 +295,11 @@ struct mdps_system {
     int real = 0;  // mdps_options.real: every series real, one product per term
     int batch = 1; // mdps_options.batch: points per evaluation (n, N are per point)
     int use_graph = 0;
+    int schedule = MDPS_SCHED_LEVELS;  // resolved: LEVELS or QUEUE
+    unsigned *qflags = nullptr;        // QUEUE: per-slot ready flags (epochs)
+    QueueCtl *qctl = nullptr;          // QUEUE: ticket counter and epoch
+    QueueGeom qgeom{};
+    int64_t njobs = 0;
     int64_t nslots = 0, products = 0, add_terms = 0, add_terms_w = 0;  // add_terms_w: weight != 1
     std::vector<int64_t> level_off, level_cnt;  // in jobs
     int ntasks = 0;
@@ -319,6 +370,8 @@ static void free_system(mdps_system *s) {
     cudaFree(s->dev_in);
     cudaFree(s->dev_vals);
     cudaFree(s->dev_jac);
+    cudaFree(s->qflags);
+    cudaFree(s->qctl);
     delete s;
 }
 
@@ -371,6 +424,22 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     if (algo == MDPS_ALGO_AUTO)
         algo = D > 128 || (!real && (limbs == 2 || (limbs == 3 && D <= 32 && S.products >= 4096)))
                    ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
+    const int sched_opt = opt ? opt->schedule : MDPS_SCHED_AUTO;
+    if (sched_opt != MDPS_SCHED_AUTO && sched_opt != MDPS_SCHED_LEVELS && sched_opt != MDPS_SCHED_QUEUE) {
+        set_err("unknown schedule");
+        return nullptr;
+    }
+    if (sched_opt == MDPS_SCHED_QUEUE && algo != MDPS_ALGO_EFT) {
+        set_err("the job queue (MDPS_SCHED_QUEUE) runs the EFT algorithm only");
+        return nullptr;
+    }
+    // AUTO: the queue for small systems on the EFT algorithm, where one level's
+    // jobs cannot fill the GPU and the per-level launch + tail dominate
+    // (measured)
+    const int sched = sched_opt == MDPS_SCHED_QUEUE ||
+                              (sched_opt == MDPS_SCHED_AUTO && algo == MDPS_ALGO_EFT &&
+                               S.products * (opt && opt->batch > 1 ? opt->batch : 1) <= MDPS_QUEUE_MAX_PRODUCTS)
+                          ? MDPS_SCHED_QUEUE : MDPS_SCHED_LEVELS;
     const std::vector<int32_t> limb_slot1(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + S.M));
     const int64_t nlimb1 = S.nlimb;
     if (B > 1 && !replicate_schedule(S, n, B, err)) {
@@ -395,12 +464,25 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->add_terms = (int64_t)S.ent_slot.size();
     for (int32_t w : S.ent_w) s->add_terms_w += w != 1;
     s->ntasks = B * (S.N + S.N * n);
+    s->schedule = sched;
 
     std::vector<int32_t> alljobs;  // (in1, in2, out, code) per job, level by level
     for (auto &lv : S.levels4) {
         s->level_off.push_back((int64_t)alljobs.size() / 4);
         s->level_cnt.push_back((int64_t)lv.size() / 4);
         alljobs.insert(alljobs.end(), lv.begin(), lv.end());
+    }
+    s->njobs = (int64_t)alljobs.size() / 4;
+    if (sched == MDPS_SCHED_QUEUE) {
+        if (s->njobs + (int64_t)s->ntasks >= (int64_t)INT32_MAX / 2) { set_err("queue: too many jobs"); free_system(s); return nullptr; }
+        const int rc = dispatch_L<QueueGeomFn>(limbs, D, (int)s->njobs, s->ntasks, s->qgeom);
+        if (rc != MDPS_OK || !dalloc(s, &s->qflags, (size_t)s->nslots) || !dalloc(s, &s->qctl, 1) ||
+            cudaMemset(s->qflags, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(1, s->nslots)) != cudaSuccess ||
+            cudaMemset(s->qctl, 0, sizeof(QueueCtl)) != cudaSuccess) {
+            if (g_err.empty()) set_err("queue setup failed");
+            free_system(s);
+            return nullptr;
+        }
     }
     const size_t ser = algo == MDPS_ALGO_DIGITS ? dig_slot_stride(s->S, D) : (size_t)2 * limbs * D;  // doubles per slot
     if (!dalloc(s, &s->pool, ser * (size_t)s->nslots) ||
@@ -475,11 +557,26 @@ extern "C" void mdps_system_destroy(mdps_system *s) {
     free_system(s);
 }
 
+template <int L>
+struct QueueRun {
+    static int run(mdps_system *s, const double *in, double *vals, double *jac, cudaStream_t st) {
+        const int nx = s->n * s->batch;
+        return QueueEft<L>::run(s->qgeom, in, s->pool, s->qflags, s->qctl, s->jobs, (int)s->njobs, s->task_ptr,
+                                s->ent_slot, s->ent_w, s->ntasks, s->N * s->batch, nx, nx + s->M, s->D, vals, jac,
+                                st);
+    }
+};
+
 // the launch sequence of one eval (also what the CUDA graph captures)
 static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, cudaStream_t st) {
     const int L = s->L, D = s->D, n = s->n * s->batch;  // input series of all points
     int rc;
     if (s->timing) s->timed_evals++;
+    if (s->schedule == MDPS_SCHED_QUEUE) {
+        // one persistent launch: products and additions, x read in place
+        TimedGroup tg(s, st, 0);
+        return dispatch_L<QueueRun>(L, s, in, vals, jac, st);
+    }
     if (s->algo == MDPS_ALGO_EFT) {
         {
             TimedGroup tg(s, st, 2);
@@ -653,7 +750,8 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     out->levels = (int32_t)s->level_cnt.size();
     out->algo = s->algo;
     out->digits = s->S;
-    out->launches = (int32_t)s->level_cnt.size() + 2;
+    out->launches = s->schedule == MDPS_SCHED_QUEUE ? 1 : (int32_t)s->level_cnt.size() + 2;
+    out->schedule = s->schedule;
     out->workspace_bytes = s->device_bytes;
     out->n = s->n;
     out->n_polys = s->N;
