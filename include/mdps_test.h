@@ -73,6 +73,20 @@ int mdps_system_timing(mdps_system *sys, mdps_timing *out, int32_t reset);
  * Newton-Schulz steps run. */
 int mdps_solver_trace(mdps_solver *solver, int64_t *ns, int32_t max, int32_t *refine_steps);
 
+/* Job-queue diagnostics (MDPS_SCHED_QUEUE systems).  enable = 1 allocates a
+ * per-ticket trace that every later evaluation fills with five globaltimer
+ * stamps (ticket claimed, inputs ready, inputs staged, computed, flag
+ * released; addition tickets fill 0, 1 and 4), enable = 0 frees it, < 0
+ * leaves it as is.  With out != NULL (after an evaluation) copies
+ * min(tickets, max_tickets) x 5 stamps, synchronising the device.  Returns
+ * the ticket count (or the count copied), < 0 on error. */
+int mdps_test_queue_trace(mdps_system *sys, int32_t enable, int64_t *out, int32_t max_tickets);
+
+/* Tuning only: queue-kernel geometry for systems created afterwards — grid
+ * cap (max_blocks > 0; 0 = occupancy x SMs) and lanes per output pair and part
+ * (a power of two; 0 = the default rule).  Returns MDPS_OK or MDPS_EINVAL. */
+int mdps_test_queue_config(int32_t max_blocks, int32_t lanes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,8 @@ EXPORTED_SYMBOLS = (
     "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
     "mdps_fp64_peak", "mdps_test_force_geometry", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
-    "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls",
+    "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls", "mdps_test_queue_trace",
+    "mdps_test_queue_config",
 )
 
 
@@ -127,6 +128,8 @@ def lib() -> ctypes.CDLL:
     L.mdps_solver_trace.argtypes = [vp, P(i64), i32, P(i32)]
     L.mdps_newton_step.argtypes = [vp, vp, vp, vp, vp, vp]
     L.mdps_newton.argtypes = [vp, vp, vp, i32, ctypes.c_double, P(ctypes.c_double), vp]
+    L.mdps_test_queue_trace.argtypes = [vp, i32, P(i64), i32]
+    L.mdps_test_queue_config.argtypes = [i32, i32]
     L.mdps_solver_destroy.argtypes = [vp]
     L.mdps_solver_destroy.restype = None
     _lib = L
@@ -289,6 +292,26 @@ class System:
     def stats(self) -> dict:
         return mdps_system_stats(self.handle)
 
+    def queue_trace(self, enable: Optional[bool] = None, read: bool = False):
+        """Job-queue diagnostics (mdps_test_queue_trace): enable/disable the
+        per-ticket trace; with read=True return [tickets][5] globaltimer ns
+        (claimed, inputs ready, staged, computed, released) of the last evaluation."""
+        L = lib()
+        en = -1 if enable is None else (1 if enable else 0)
+        if not read:
+            n = L.mdps_test_queue_trace(self.handle, en, None, 0)
+            if n < 0:
+                raise MdpsError(mdps_last_error())
+            return n
+        n = L.mdps_test_queue_trace(self.handle, en, None, 0)
+        if n < 0:
+            raise MdpsError(mdps_last_error())
+        buf = (ctypes.c_int64 * (5 * n))()
+        n = L.mdps_test_queue_trace(self.handle, -1, buf, n)
+        if n < 0:
+            raise MdpsError(mdps_last_error())
+        return np.array(buf[:5 * n], dtype=np.int64).reshape(n, 5)
+
     def level_jobs(self):
         buf = (ctypes.c_int64 * 4096)()
         n = lib().mdps_system_level_jobs(self.handle, buf, 4096)
@@ -442,6 +465,11 @@ def test_digits_roundtrip(x, stream=None):
     _check(lib().mdps_test_digits_roundtrip(_dptr(x), _dptr(y), count, D - 1, L, _stream_handle(stream)),
            "mdps_test_digits_roundtrip")
     return y
+
+
+def queue_config(max_blocks: int = 0, lanes: int = 0) -> None:
+    """Tuning only: job-queue grid cap and lanes per output pair for systems created afterwards."""
+    _check(lib().mdps_test_queue_config(max_blocks, lanes), "mdps_test_queue_config")
 
 
 def force_geometry(F: int = 0, P: int = 0) -> None:

@@ -81,6 +81,8 @@ struct DigGeom {
 // amortises the per-output epilogue — unless a measured table entry exists.
 // forced geometry of the product kernel (mdps_test_force_geometry; tuning only)
 static int g_force_F = 0, g_force_P = 0;
+static int g_force_queue_blocks = 0;  // mdps_test_queue_config: grid cap of the queue kernel (0 = occupancy)
+static int g_force_queue_F = 0;       // mdps_test_queue_config: lanes per output pair and part (0 = default)
 
 // Measured best (F, P) of the complex two-pass digit kernel where it beats the
 // model by > 1% (scripts/tune_table.py, every fitting (F, P) timed on the
@@ -229,7 +231,7 @@ struct QueueGeom {
 template <int L>
 struct QueueEft {
     static int geom(int D, int njobs, int ntasks, QueueGeom &g) {
-        g.F = queue_lanes(D);
+        g.F = g_force_queue_F > 0 ? queue_lanes(D, g_force_queue_F) : queue_lanes(D);
         g.threads = (2 * ((D + 1) / 2) * g.F + 31) / 32 * 32;
         g.tasks_per_ticket = std::max(1, g.threads / D);
         g.smem = (size_t)2 * (2 * L * D) * sizeof(double);
@@ -246,15 +248,18 @@ struct QueueEft {
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, g.threads, g.smem), MDPS_ECUDA);
         if (per < 1) { set_err("queue kernel does not fit on an SM"); return MDPS_EINVAL; }
         const long long tickets = (long long)njobs + (ntasks + g.tasks_per_ticket - 1) / g.tasks_per_ticket;
-        g.blocks = (int)std::max(1LL, std::min<long long>(tickets, (long long)sms * per));
+        // at most 4 blocks per SM: more only lengthen the launch and the
+        // ticket traffic (dd: 592 vs 1184 blocks, scripts/queue_tune.py)
+        g.blocks = (int)std::max(1LL, std::min<long long>(tickets, (long long)sms * std::min(per, 4)));
+        if (g_force_queue_blocks > 0) g.blocks = std::min(g.blocks, g_force_queue_blocks);
         return MDPS_OK;
     }
     static int run(const QueueGeom &g, const double *x_in, double *pool, unsigned *flags, QueueCtl *ctl,
                    const int *jobs, int njobs, const int *tp, const int *es, const int *ew, int ntasks, int nvals,
-                   int nx, int nready, int D, double *values, double *jac, cudaStream_t st) {
+                   int nx, int nready, int D, double *values, double *jac, long long *trace, cudaStream_t st) {
         queue_eft_kernel<L><<<g.blocks, g.threads, g.smem, st>>>(x_in, pool, flags, ctl, jobs, njobs, tp, es, ew,
                                                                   ntasks, nvals, g.tasks_per_ticket, nx, nready, D,
-                                                                  g.F, values, jac);
+                                                                  g.F, values, jac, trace);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -299,6 +304,8 @@ struct mdps_system {
     unsigned *qflags = nullptr;        // QUEUE: per-slot ready flags (epochs)
     QueueCtl *qctl = nullptr;          // QUEUE: ticket counter and epoch
     QueueGeom qgeom{};
+    long long *qtrace = nullptr;       // QUEUE diagnostics: [ticket][QUEUE_TRACE_STAMPS] ns (mdps_test_queue_trace)
+    int64_t qtickets = 0;
     int64_t njobs = 0;
     int64_t nslots = 0, products = 0, add_terms = 0, add_terms_w = 0;  // add_terms_w: weight != 1
     std::vector<int64_t> level_off, level_cnt;  // in jobs
@@ -372,6 +379,7 @@ static void free_system(mdps_system *s) {
     cudaFree(s->dev_jac);
     cudaFree(s->qflags);
     cudaFree(s->qctl);
+    cudaFree(s->qtrace);
     delete s;
 }
 
@@ -476,6 +484,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     if (sched == MDPS_SCHED_QUEUE) {
         if (s->njobs + (int64_t)s->ntasks >= (int64_t)INT32_MAX / 2) { set_err("queue: too many jobs"); free_system(s); return nullptr; }
         const int rc = dispatch_L<QueueGeomFn>(limbs, D, (int)s->njobs, s->ntasks, s->qgeom);
+        s->qtickets = s->njobs + (s->ntasks + s->qgeom.tasks_per_ticket - 1) / s->qgeom.tasks_per_ticket;
         if (rc != MDPS_OK || !dalloc(s, &s->qflags, (size_t)s->nslots) || !dalloc(s, &s->qctl, 1) ||
             cudaMemset(s->qflags, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(1, s->nslots)) != cudaSuccess ||
             cudaMemset(s->qctl, 0, sizeof(QueueCtl)) != cudaSuccess) {
@@ -563,7 +572,7 @@ struct QueueRun {
         const int nx = s->n * s->batch;
         return QueueEft<L>::run(s->qgeom, in, s->pool, s->qflags, s->qctl, s->jobs, (int)s->njobs, s->task_ptr,
                                 s->ent_slot, s->ent_w, s->ntasks, s->N * s->batch, nx, nx + s->M, s->D, vals, jac,
-                                st);
+                                s->qtrace, st);
     }
 };
 
@@ -1029,4 +1038,38 @@ extern "C" int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t s
     const double inst = (double)blocks * threads * (double)iters * 16.0 * 8.0;
     *inst_per_s = inst / (ms * 1e-3);
     return MDPS_OK;
+}
+
+// queue diagnostics: enable the per-ticket trace, or read it back after a
+// synchronize; the geometry knobs apply to systems created afterwards
+extern "C" int mdps_test_queue_config(int32_t max_blocks, int32_t lanes) {
+    if (max_blocks < 0 || lanes < 0 || lanes > 32 || (lanes & (lanes - 1))) {
+        set_err("queue config: max_blocks >= 0, lanes a power of two <= 32 (0 = default)");
+        return MDPS_EINVAL;
+    }
+    g_force_queue_blocks = max_blocks;
+    g_force_queue_F = lanes;
+    return MDPS_OK;
+}
+
+extern "C" int mdps_test_queue_trace(mdps_system *s, int32_t enable, int64_t *out, int32_t max_tickets) {
+    if (!s) { set_err("NULL system"); return MDPS_EINVAL; }
+    if (s->schedule != MDPS_SCHED_QUEUE) { set_err("not a queue-scheduled system"); return MDPS_EINVAL; }
+    if (enable > 0 && !s->qtrace) {
+        if (!dalloc(s, &s->qtrace, (size_t)QUEUE_TRACE_STAMPS * s->qtickets)) return MDPS_ENOMEM;
+        CUDA_TRY(cudaMemset(s->qtrace, 0, sizeof(long long) * QUEUE_TRACE_STAMPS * (size_t)s->qtickets), MDPS_ECUDA);
+    }
+    if (enable == 0 && s->qtrace) {
+        cudaDeviceSynchronize();
+        cudaFree(s->qtrace);
+        s->qtrace = nullptr;
+    }
+    if (out && s->qtrace) {
+        const int64_t cnt = std::min<int64_t>(s->qtickets, max_tickets);
+        CUDA_TRY(cudaDeviceSynchronize(), MDPS_ECUDA);
+        CUDA_TRY(cudaMemcpy(out, s->qtrace, sizeof(long long) * QUEUE_TRACE_STAMPS * (size_t)cnt,
+                            cudaMemcpyDeviceToHost), MDPS_ECUDA);
+        return (int)cnt;
+    }
+    return (int)s->qtickets;
 }

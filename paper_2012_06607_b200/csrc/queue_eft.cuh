@@ -30,6 +30,10 @@
 
 namespace mdps {
 
+// diagnostics (mdps_test_queue_trace): globaltimer stamps per ticket — claimed,
+// inputs ready, staged, computed, released (addition tickets: 0, 1, 4)
+constexpr int QUEUE_TRACE_STAMPS = 5;
+
 struct QueueCtl {
     unsigned int counter;  // next ticket (reset to 0 by the last block)
     unsigned int epoch;    // evaluations completed; flags of this launch hold epoch + 1
@@ -45,10 +49,47 @@ __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// wait until series `slot` is final (slots below nready are inputs: always)
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// wait until series `slot` is final (slots below nready are inputs: always).
+// Relaxed polling; the caller issues one acquire fence after its waits.
 __device__ __forceinline__ void queue_wait(const unsigned *flags, int slot, int nready, unsigned cur) {
     if (slot < nready) return;
-    while (ld_acquire_u32(flags + slot) != cur) __nanosleep(32);
+    if (ld_relaxed_u32(flags + slot) == cur) return;
+    unsigned ns = 8;
+    while (ld_relaxed_u32(flags + slot) != cur) {
+        __nanosleep(ns);
+        ns = ns < 128 ? 2 * ns : ns;
+    }
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// wait until the NS series slot[0..NS) are final: the flags are polled
+// together (one L2 round trip per poll, not one per series)
+template <int NS>
+__device__ __forceinline__ void queue_wait_all(const unsigned *flags, const int (&slot)[NS], const bool (&need)[NS],
+                                               unsigned cur) {
+    unsigned ns = 8;
+    for (;;) {
+        bool ok = true;
+#pragma unroll
+        for (int u = 0; u < NS; u++)
+            if (need[u]) ok &= ld_relaxed_u32(flags + slot[u]) == cur;
+        if (ok) return;
+        __nanosleep(ns);
+        ns = ns < 128 ? 2 * ns : ns;
+    }
 }
 
 // B += the bins of another partial sum (level o at level o; guard plainly)
@@ -65,10 +106,11 @@ __device__ __forceinline__ void bins_merge(double (&B)[L + 1], const double (&C)
 }
 
 // threads per job for the queue kernel: 2 parts x T pairs x F lanes, F the
-// largest power of two <= 8 with 2 T F <= 256
-__host__ __device__ inline int queue_lanes(int D) {
+// largest power of two <= fmax with 2 T F <= 256 (default 4: measured on dd,
+// scripts/queue_tune.py — 8 and 16 lanes cost more in merges than they save)
+__host__ __device__ inline int queue_lanes(int D, int fmax = 4) {
     const int T = (D + 1) / 2;
-    int F = 8;
+    int F = fmax;
     while (F > 1 && 2 * T * F > 256) F >>= 1;
     return F;
 }
@@ -81,9 +123,10 @@ __global__ void __launch_bounds__(256) queue_eft_kernel(
     QueueCtl *ctl, const int *__restrict__ jobs, int njobs,  // (in1, in2, out, code), topological
     const int *__restrict__ task_ptr, const int *__restrict__ ent_slot, const int *__restrict__ ent_w,
     int ntasks, int nvals, int tasks_per_ticket, int nx, int nready, int D, int F, double *__restrict__ values,
-    double *__restrict__ jac) {
+    double *__restrict__ jac, long long *__restrict__ trace) {  // trace: NULL, or [ticket][QUEUE_TRACE_STAMPS] ns
     extern __shared__ double sq[];
     __shared__ unsigned s_ticket;
+    constexpr int TS = QUEUE_TRACE_STAMPS;
     const int LD2 = 2 * L * D;
     const int T = (D + 1) / 2;
     const unsigned cur = ctl->epoch + 1u;
@@ -110,15 +153,39 @@ __global__ void __launch_bounds__(256) queue_eft_kernel(
             }
             return;
         }
+        if (trace && threadIdx.x == 0) trace[TS * tk] = (long long)globaltimer_ns();
         if (tk < (unsigned)njobs) {
             // ---- product job z = x * y mod t^D
             const int in1 = __ldg(jobs + 4 * tk), in2 = __ldg(jobs + 4 * tk + 1), out = __ldg(jobs + 4 * tk + 2);
-            queue_wait(flags, in1, nready, cur);
-            queue_wait(flags, in2, nready, cur);
-            const double *s1 = series(in1), *s2 = series(in2);
-            for (int idx = threadIdx.x; idx < 2 * LD2; idx += blockDim.x)
-                sq[idx] = idx < LD2 ? __ldcg(s1 + idx) : __ldcg(s2 + idx - LD2);
+            // one thread waits for both inputs (acquire), the barrier passes
+            // the ordering on to the block; the loads bypass L1
+            if (threadIdx.x == 0) {
+                const int sl[2] = {in1, in2};
+                const bool nd[2] = {in1 >= nready, in2 >= nready};
+                if (nd[0] || nd[1]) {
+                    queue_wait_all<2>(flags, sl, nd, cur);
+                    fence_acquire_gpu();
+                }
+                if (trace) trace[TS * tk + 1] = (long long)globaltimer_ns();
+            }
             __syncthreads();
+            const double *s1 = series(in1), *s2 = series(in2);
+            // staging: up to 4 loads per thread in flight before the stores
+            for (int base = threadIdx.x; base < 2 * LD2; base += 4 * blockDim.x) {
+                double v[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int idx = base + u * blockDim.x;
+                    v[u] = idx < LD2 ? __ldcg(s1 + idx) : (idx < 2 * LD2 ? __ldcg(s2 + idx - LD2) : 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int idx = base + u * blockDim.x;
+                    if (idx < 2 * LD2) sq[idx] = v[u];
+                }
+            }
+            __syncthreads();
+            if (trace && threadIdx.x == 0) trace[TS * tk + 2] = (long long)globaltimer_ns();
             const double *sx = sq, *sy = sq + LD2;
             double B1[L + 1], B2[L + 1];
             md_zero(B1);
@@ -169,35 +236,71 @@ __global__ void __launch_bounds__(256) queue_eft_kernel(
                 md_renorm(B2, r);
 #pragma unroll
                 for (int p = 0; p < L; p++) z[(part * L + p) * D + (D - 1 - t)] = r[p];
-                __threadfence();
             }
+            // the block's stores, then one gpu-scope fence and the release of
+            // the output's flag by thread 0 (the barrier orders the stores first)
             __syncthreads();
-            if (threadIdx.x == 0) st_release_u32(flags + out, cur);
+            if (threadIdx.x == 0) {
+                if (trace) trace[TS * tk + 3] = (long long)globaltimer_ns();
+                __threadfence();
+                st_release_u32(flags + out, cur);
+                if (trace) trace[TS * tk + 4] = (long long)globaltimer_ns();
+            }
         } else {
             // ---- addition jobs: values and Jacobian entries
             const int a0 = (int)(tk - (unsigned)njobs) * tasks_per_ticket;
+            // every thread waits for the entries of its own batch as it goes
+            // (sums start on the entries that are final), an acquire load
+            // after each wait; the loads bypass L1
+            if (trace && threadIdx.x == 0) trace[TS * tk + 1] = (long long)globaltimer_ns();
             for (int e = threadIdx.x; e < tasks_per_ticket * D; e += blockDim.x) {
                 const int task = a0 + e / D, k = e - (e / D) * D;
                 if (task >= ntasks) break;
                 double Br[L + 1], Bi[L + 1];
                 md_zero(Br);
                 md_zero(Bi);
-                for (int q = __ldg(task_ptr + task); q < __ldg(task_ptr + task + 1); q++) {
-                    const int slot = __ldg(ent_slot + q), w = __ldg(ent_w + q);
-                    queue_wait(flags, slot, nready, cur);
-                    const double *s = series(slot);
-                    double ar[L], ai[L];
+                // entries in batches of QB: the loads of a batch are in flight
+                // together (a serial load per entry costs an L2 round trip
+                // each), then summed in entry order (the same bins as one by one)
+                constexpr int QB = L <= 2 ? 8 : (L <= 5 ? 4 : 2);
+                const int q1 = __ldg(task_ptr + task + 1);
+                for (int qb = __ldg(task_ptr + task); qb < q1; qb += QB) {
+                    double ar[QB][L], ai[QB][L];
+                    int w[QB];
+                    int slots[QB];
 #pragma unroll
-                    for (int p = 0; p < L; p++) {
-                        ar[p] = __ldcg(s + p * D + k);
-                        ai[p] = __ldcg(s + (L + p) * D + k);
+                    for (int u = 0; u < QB; u++) slots[u] = qb + u < q1 ? __ldg(ent_slot + qb + u) : 0;
+                    bool need[QB], any = false;
+#pragma unroll
+                    for (int u = 0; u < QB; u++) {
+                        need[u] = qb + u < q1 && slots[u] >= nready;
+                        any |= need[u];
                     }
-                    if (w == 1) {
-                        bins_add<L>(Br, ar);
-                        bins_add<L>(Bi, ai);
-                    } else {
-                        bins_add_scaled<L>(Br, ar, (double)w);
-                        bins_add_scaled<L>(Bi, ai, (double)w);
+                    if (any) {
+                        queue_wait_all<QB>(flags, slots, need, cur);
+                        fence_acquire_gpu();
+                    }
+#pragma unroll
+                    for (int u = 0; u < QB; u++) {
+                        const bool in = qb + u < q1;
+                        const int slot = slots[u];
+                        w[u] = in ? __ldg(ent_w + qb + u) : 0;
+                        const double *sp = series(slot);
+#pragma unroll
+                        for (int p = 0; p < L; p++) {
+                            ar[u][p] = in ? __ldcg(sp + p * D + k) : 0.0;
+                            ai[u][p] = in ? __ldcg(sp + (L + p) * D + k) : 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < QB; u++) {
+                        if (w[u] == 1) {
+                            bins_add<L>(Br, ar[u]);
+                            bins_add<L>(Bi, ai[u]);
+                        } else if (w[u] != 0) {
+                            bins_add_scaled<L>(Br, ar[u], (double)w[u]);
+                            bins_add_scaled<L>(Bi, ai[u], (double)w[u]);
+                        }
                     }
                 }
                 double zr[L], zi[L];
@@ -209,6 +312,10 @@ __global__ void __launch_bounds__(256) queue_eft_kernel(
                     o[p * D + k] = zr[p];
                     o[(L + p) * D + k] = zi[p];
                 }
+            }
+            if (trace) {
+                __syncthreads();
+                if (threadIdx.x == 0) trace[TS * tk + 4] = (long long)globaltimer_ns();
             }
         }
     }
