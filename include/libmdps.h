@@ -208,6 +208,17 @@ int mdps_solve(mdps_solver *solver, const double *jacobian, const double *rhs, d
  * singular = 1 if some pivot column of A_0 was zero. */
 int mdps_solver_status(mdps_solver *solver, int32_t *pivots, int32_t *singular);
 
+/* After synchronising the last solve's stream: its outcome flags.
+ * MDPS_SOLVE_SINGULAR: a zero pivot column of A_0 (as mdps_solver_status).
+ * MDPS_SOLVE_NOT_CONVERGED: the md refinement of A_0's inverse (Newton-Schulz
+ * from the double-precision Gauss-Jordan seed) missed ||I - W A_0||^2 <
+ * 2^-(53 L + 16) after its step limit — A_0 is too ill-conditioned for a
+ * double seed (kappa >~ 1e16; the paper's md LU, has no
+ * such limit).  dx_out is unspecified when either flag is set. */
+#define MDPS_SOLVE_SINGULAR 1
+#define MDPS_SOLVE_NOT_CONVERGED 2
+int mdps_solver_flags(mdps_solver *solver, int32_t *flags);
+
 typedef struct {
     int64_t complex_fma;       /* complex md multiply-adds per solve (LU, inverse, substitution) */
     int64_t fp64_ops;          /* algorithmic FP64 instructions per solve */

@@ -25,6 +25,7 @@ __all__ = [
 MDPS_OK, MDPS_EINVAL, MDPS_ENOMEM, MDPS_ECUDA = 0, -1, -2, -3
 MDPS_ALGO_AUTO, MDPS_ALGO_EFT, MDPS_ALGO_DIGITS = 0, 1, 2
 MDPS_SCHED_AUTO, MDPS_SCHED_LEVELS, MDPS_SCHED_QUEUE = 0, 1, 2
+MDPS_SOLVE_SINGULAR, MDPS_SOLVE_NOT_CONVERGED = 1, 2
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 library_path = os.path.join(_HERE, "libmdps.so")
@@ -37,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "mdps_fp64_peak", "mdps_test_force_geometry", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
     "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls", "mdps_test_queue_trace",
-    "mdps_test_queue_config",
+    "mdps_test_queue_config", "mdps_solver_flags",
 )
 
 
@@ -124,6 +125,7 @@ def lib() -> ctypes.CDLL:
     L.mdps_solver_create_ls.argtypes = [i32, i32, i32, i32]
     L.mdps_solve.argtypes = [vp, vp, vp, vp, vp]
     L.mdps_solver_status.argtypes = [vp, P(i32), P(i32)]
+    L.mdps_solver_flags.argtypes = [vp, P(i32)]
     L.mdps_solver_stats.argtypes = [vp, P(SolverInfo)]
     L.mdps_solver_trace.argtypes = [vp, P(i64), i32, P(i32)]
     L.mdps_newton_step.argtypes = [vp, vp, vp, vp, vp, vp]
@@ -396,6 +398,13 @@ class Solver:
         sing = ctypes.c_int32(0)
         _check(lib().mdps_solver_status(self.handle, _ptr_i32(piv), ctypes.byref(sing)), "mdps_solver_status")
         return piv, bool(sing.value)
+
+    def flags(self) -> int:
+        """Outcome flags of the last solve (synchronises): MDPS_SOLVE_SINGULAR,
+        MDPS_SOLVE_NOT_CONVERGED."""
+        f = ctypes.c_int32(0)
+        _check(lib().mdps_solver_flags(self.handle, ctypes.byref(f)), "mdps_solver_flags")
+        return f.value
 
     def trace(self):
         """(barrier completion times in ns relative to the kernel start, refine steps)."""

@@ -60,7 +60,7 @@ struct Ctl {              // device control block (memset to 0 before every solv
     unsigned int count;   // grid barrier
     unsigned int gen;
     int emax;             // max radix exponent of the entries of E = I - A_0 W (+ bias), 0 = none
-    int status;           // bit 0: singular A_0
+    int status;           // bit 0: singular A_0; bit 1: the refinement missed its bound (MDPS_SOLVE_NOT_CONVERGED)
     int refine_steps;     // Newton-Schulz steps run
     int ntrace;           // entries of the phase trace written
     unsigned int rdy;     // substitution loop: right-hand-side entries final (cumulative)
@@ -785,7 +785,12 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
         // ||E|| < R^emax / 2; the step leaves an error ~||E||^2: stop once that
         // is below 2^-(53 L + 16)
         const int eraw = *(volatile int *)&ctl->emax;
-        const bool last = eraw == 0 || 2 * (BETA * (eraw - EMAX_BIAS) - 1) < -(53 * L + 16) || it + 1 == MAX_REFINE;
+        const bool conv = eraw == 0 || 2 * (BETA * (eraw - EMAX_BIAS) - 1) < -(53 * L + 16);
+        const bool last = conv || it + 1 == MAX_REFINE;
+        // MAX_REFINE steps without reaching the bound: ||I - W A_0|| was not
+        // < 1 at the double-precision seed (A_0 too ill-conditioned for the
+        // double Gauss-Jordan, kappa >~ 1e16): reported, dx unspecified
+        if (!conv && last && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&ctl->status, 2);
         {
             const ColSplit cs = col_split(RL, n);
             const int G = pick_group(cs.r1 - cs.r0, n, blockDim.x);
@@ -1341,6 +1346,18 @@ int mdps_solve_internal(mdps_solver *s, const double *J, const double *b, double
 
 extern "C" int mdps_solve(mdps_solver *s, const double *J, const double *b, double *dx, mdps_stream_t stream) {
     return mdps_solve_internal(s, J, b, dx, 0, (cudaStream_t)stream);
+}
+
+extern "C" int mdps_solver_flags(mdps_solver *s, int32_t *flags) {
+    if (!s || !flags) {
+        mdps_internal_set_error("mdps_solver_flags: NULL argument");
+        return MDPS_EINVAL;
+    }
+    TS_TRY(cudaStreamSynchronize(s->last), MDPS_ECUDA);
+    ts::Ctl c;
+    TS_TRY(cudaMemcpy(&c, s->ctl, sizeof c, cudaMemcpyDeviceToHost), MDPS_ECUDA);
+    *flags = c.status & (MDPS_SOLVE_SINGULAR | MDPS_SOLVE_NOT_CONVERGED);
+    return MDPS_OK;
 }
 
 extern "C" int mdps_solver_status(mdps_solver *s, int32_t *pivots, int32_t *singular) {

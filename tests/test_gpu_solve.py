@@ -157,3 +157,61 @@ def test_least_squares_config_shape(mdps):
         dx = dx.cpu().numpy()
     want = oracle.toeplitz_lstsq(t.jac, t.rhs, nthreads=NTHREADS)
     assert oracle.series_err(dx, want).max() <= TOL[8]
+
+
+def _conditioned_toeplitz(kappa_exp, seed, L, n=4, degree=3):
+    """A_0 = H1 diag(2, 1, .., 1, 10^-kappa_exp) H2 with rational Householder
+    reflections H (exactly orthogonal), rounded to L limbs: kappa(A_0) ~
+    2 10^kappa_exp; A_1.. and b from the seeded unit-circle generator."""
+    import random
+    from fractions import Fraction as Fr
+    from tests.exact import greedy
+
+    def householder(v):
+        vv = sum(x * x for x in v)
+        return [[(1 if i == j else 0) - 2 * v[i] * v[j] / vv for j in range(n)] for i in range(n)]
+
+    def mm(A, B):
+        return [[sum(A[i][k] * B[k][j] for k in range(n)) for j in range(n)] for i in range(n)]
+
+    rng = random.Random(seed)
+    H1 = householder([Fr(rng.randint(1, 9)) for _ in range(n)])
+    H2 = householder([Fr(rng.randint(-9, 9) or 1) for _ in range(n)])
+    d = [[Fr(0)] * n for _ in range(n)]
+    for i in range(n):
+        d[i][i] = Fr(1)
+    d[0][0], d[n - 1][n - 1] = Fr(2), Fr(1, 10 ** kappa_exp)
+    A0 = mm(mm(H1, d), H2)
+    t = mdinputs.random_toeplitz(300 + seed, n, degree, L)
+    jac = t.jac.copy()
+    for p in range(n):
+        for q in range(n):
+            jac[p, q, 0, :, 0] = greedy(A0[p][q], L)
+            jac[p, q, 1, :, 0] = 0.0
+    return t, jac
+
+
+@pytest.mark.parametrize("L", (2, 8))
+@pytest.mark.parametrize("seed", (0, 1, 2))
+def test_ill_conditioned_flags(mdps, L, seed):
+    """kappa(A_0) ~ 1e12: the refinement converges (no flag) and dx matches
+    the oracle's md LU within kappa x the md unit; kappa ~ 1e17: the double
+    Gauss-Jordan seed has ||I - W A_0|| > 1, Newton-Schulz cannot converge,
+    and the solve reports MDPS_SOLVE_NOT_CONVERGED (the
+    paper's md LU has no such limit, so the limit is reported, not silent)."""
+    import torch
+    for kexp, must_flag in ((12, False), (17, True)):
+        t, jac = _conditioned_toeplitz(kexp, seed, L)
+        with mdps.Solver(t.n, t.degree, t.limbs) as s:
+            dx = s.solve(cuda(jac), cuda(t.rhs))
+            torch.cuda.synchronize()
+            flags = s.flags()
+            _, sing = s.status()
+        assert not sing
+        if must_flag:
+            assert flags & mdps.MDPS_SOLVE_NOT_CONVERGED, (kexp, seed, flags)
+        else:
+            assert flags == 0, (kexp, seed, flags)
+            want, _ = oracle.toeplitz_solve(jac, t.rhs, nthreads=NTHREADS)
+            err = oracle.series_err(dx.cpu().numpy() if hasattr(dx, "cpu") else dx, want)
+            assert err.max() <= 2.0 * 10.0 ** kexp * 4096 * 2.0 ** (-53 * L), err.max()
