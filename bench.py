@@ -350,6 +350,8 @@ def main():
     ap.add_argument("--algo", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workspace-mb", type=int, default=0,
+                    help="bound on the system's pool memory (mdps_options.workspace_mb; 0 = default)")
     ap.add_argument("--no-next", action="store_true", help="skip the solver / Newton-step measurements")
     ap.add_argument("--shard", default="replicas", choices=["replicas", "rows"],
                     help="N > 1: independent replicas (weak scaling, default) or one system's rows sharded (strong)")
@@ -389,7 +391,7 @@ def main():
         full_products = sum(costs)
     n_rows = len(si.poly_ptr) - 1
     peaks = load_peaks()
-    sys_ = mdps.System.from_inputs(si, algo=args.algo)
+    sys_ = mdps.System.from_inputs(si, algo=args.algo, workspace_mb=args.workspace_mb)
     st = sys_.stats()
     stream = torch.cuda.current_stream()
     x = torch.from_numpy(si.x).cuda()
@@ -513,7 +515,9 @@ def main():
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": bench_config(si_full, args.config, world, sharded),
             "schedule": {"algo": {1: "eft", 2: "digits"}[st["algo"]], "digits": st["digits"],
-                         "products_per_step": products_per_step, "levels": st["levels"]},
+                         "products_per_step": products_per_step, "levels": st["levels"],
+                         "order": {1: "levels", 2: "queue"}[st["schedule"]], "chunks": st["chunks"],
+                         "workspace_bytes": st["workspace_bytes"], "pool_bytes": st["pool_bytes"]},
             "fp64_ops_per_s": fp64_per_s,
             "fp64_ops_per_step": st["fp64_ops_total"],
             "roofline": roofline,

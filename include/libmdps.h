@@ -80,7 +80,14 @@ typedef struct {
                             in one launch per level (small systems fill the GPU;
                             mdps_newton_step needs batch = 1) */
     int32_t schedule;    /* MDPS_SCHED_*: how the product and addition jobs are run */
+    int32_t workspace_mb; /* LEVELS schedule: bound on the pool memory, MiB (0 = default,
+                            MDPS_DEFAULT_WORKSPACE_MB).  Pool slots are reused by
+                            liveness; when that is not enough the rows are split into
+                            chunks evaluated one after the other (each its levels, then
+                            its addition jobs), as few as fit (<= 64) */
 } mdps_options;
+
+#define MDPS_DEFAULT_WORKSPACE_MB 0   /* 0: no bound beyond liveness reuse */
 
 /* Job scheduling (PAPER.md:367-378 job queue, 411-424 stages). */
 #define MDPS_SCHED_AUTO 0    /* default: QUEUE for small systems on the EFT algorithm
@@ -153,6 +160,8 @@ typedef struct {
     int32_t limbs;             /* L */
     int32_t batch;             /* points per evaluation (mdps_options.batch) */
     int32_t schedule;          /* MDPS_SCHED_LEVELS or MDPS_SCHED_QUEUE (as resolved at create) */
+    int32_t chunks;            /* row chunks evaluated one after the other (LEVELS; 1 = none) */
+    int64_t pool_bytes;        /* of workspace_bytes: the slot pools (digits + limbs, or limbs) */
 } mdps_stats;
 
 /* Statistics of a system (for the measurement). */

@@ -87,6 +87,18 @@ int mdps_test_queue_trace(mdps_system *sys, int32_t enable, int64_t *out, int32_
  * (a power of two; 0 = the default rule).  Returns MDPS_OK or MDPS_EINVAL. */
 int mdps_test_queue_config(int32_t max_blocks, int32_t lanes);
 
+/* Host-only (no GPU): build the job schedule of a system, check it (every
+ * slot in range, every input written by an earlier launch, no slot read and
+ * written in one launch, no live slot overwritten — schedule.hpp
+ * check_schedule), plan its memory (liveness reuse, `chunks` row chunks) and
+ * check the plan.  out[0] pool bytes without reuse, out[1] with the plan,
+ * out[2] chunks used, out[3] launches per evaluation.  corrupt in {1,2,3}
+ * damages the plan first (same-launch read/write, overwrite of a live slot,
+ * slot out of range): then MDPS_EINVAL means the check caught it, 1 that it
+ * did not. */
+int mdps_test_plan(const mdps_supports *supports, const int32_t *exponents, int32_t n, int32_t degree,
+                   int32_t limbs, int32_t eft, int32_t batch, int32_t chunks, int32_t corrupt, int64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "mdps_fp64_peak", "mdps_test_force_geometry", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
     "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls", "mdps_test_queue_trace",
-    "mdps_test_queue_config", "mdps_solver_flags",
+    "mdps_test_queue_config", "mdps_solver_flags", "mdps_test_plan",
 )
 
 
@@ -53,7 +53,7 @@ class _Supports(ctypes.Structure):
 
 class _Options(ctypes.Structure):
     _fields_ = [("algo", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("real", ctypes.c_int32),
-                ("batch", ctypes.c_int32), ("schedule", ctypes.c_int32)]
+                ("batch", ctypes.c_int32), ("schedule", ctypes.c_int32), ("workspace_mb", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -63,7 +63,7 @@ class Stats(ctypes.Structure):
                 ("algo", ctypes.c_int32), ("digits", ctypes.c_int32), ("launches", ctypes.c_int32),
                 ("workspace_bytes", ctypes.c_size_t), ("n", ctypes.c_int32), ("n_polys", ctypes.c_int32),
                 ("degree", ctypes.c_int32), ("limbs", ctypes.c_int32), ("batch", ctypes.c_int32),
-                ("schedule", ctypes.c_int32)]
+                ("schedule", ctypes.c_int32), ("chunks", ctypes.c_int32), ("pool_bytes", ctypes.c_int64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -132,6 +132,7 @@ def lib() -> ctypes.CDLL:
     L.mdps_newton.argtypes = [vp, vp, vp, i32, ctypes.c_double, P(ctypes.c_double), vp]
     L.mdps_test_queue_trace.argtypes = [vp, i32, P(i64), i32]
     L.mdps_test_queue_config.argtypes = [i32, i32]
+    L.mdps_test_plan.argtypes = [P(_Supports), P(i32), i32, i32, i32, i32, i32, i32, i32, P(i64)]
     L.mdps_solver_destroy.argtypes = [vp]
     L.mdps_solver_destroy.restype = None
     _lib = L
@@ -194,12 +195,12 @@ def _current_device() -> int:
 
 def mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n: int, degree: int,
                        limbs: int, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False,
-                       batch: int = 1, schedule: int = MDPS_SCHED_AUTO) -> int:
+                       batch: int = 1, schedule: int = MDPS_SCHED_AUTO, workspace_mb: int = 0) -> int:
     """Create a system; returns the opaque handle (int).  Host numpy inputs."""
     pp, mp, vv, ee = _i32(poly_ptr), _i32(mono_ptr), _i32(vars_), _i32(exponents)
     coeffs = np.ascontiguousarray(np.asarray(coefficients, dtype=np.float64))
     sup = _Supports(len(pp) - 1, _ptr_i32(pp), _ptr_i32(mp), _ptr_i32(vv))
-    opts = _Options(algo, 1 if use_graph else 0, 1 if real else 0, int(batch), int(schedule))
+    opts = _Options(algo, 1 if use_graph else 0, 1 if real else 0, int(batch), int(schedule), int(workspace_mb))
     h = lib().mdps_system_create_ex(ctypes.byref(sup), _ptr_i32(ee),
                                     coeffs.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
                                     n, degree, limbs, ctypes.byref(opts))
@@ -253,20 +254,20 @@ class System:
 
     def __init__(self, poly_ptr, mono_ptr, vars_, exponents, coefficients, n, degree, limbs,
                  algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False, batch: int = 1,
-                 schedule: int = MDPS_SCHED_AUTO):
+                 schedule: int = MDPS_SCHED_AUTO, workspace_mb: int = 0):
         self.n, self.degree, self.limbs = int(n), int(degree), int(limbs)
         self.n_polys = int(len(poly_ptr) - 1)
         self.batch = int(batch)
         self.handle = mdps_system_create(poly_ptr, mono_ptr, vars_, exponents, coefficients, n,
-                                         degree, limbs, algo, use_graph, real, batch, schedule)
+                                         degree, limbs, algo, use_graph, real, batch, schedule, workspace_mb)
         self.device = _current_device()  # the library allocated on the current device
 
     @classmethod
     def from_inputs(cls, si, algo: int = MDPS_ALGO_AUTO, use_graph: bool = False, real: bool = False,
-                    batch: int = 1, schedule: int = MDPS_SCHED_AUTO) -> "System":
+                    batch: int = 1, schedule: int = MDPS_SCHED_AUTO, workspace_mb: int = 0) -> "System":
         """From an mdinputs.SystemInputs-like object (poly_ptr, mono_ptr, vars, exps, coeffs)."""
         return cls(si.poly_ptr, si.mono_ptr, si.vars, si.exps, si.coeffs, si.n, si.degree, si.limbs,
-                   algo, use_graph, real, batch, schedule)
+                   algo, use_graph, real, batch, schedule, workspace_mb)
 
     @property
     def series_shape(self):
@@ -474,6 +475,17 @@ def test_digits_roundtrip(x, stream=None):
     _check(lib().mdps_test_digits_roundtrip(_dptr(x), _dptr(y), count, D - 1, L, _stream_handle(stream)),
            "mdps_test_digits_roundtrip")
     return y
+
+
+def test_plan(si, eft: bool, batch: int = 1, chunks: int = 1, corrupt: int = 0):
+    """Host-only schedule + memory-plan check (mdps_test_plan): returns
+    (rc, {unplanned_bytes, planned_bytes, chunks, launches}, message)."""
+    pp, mp, vv, ee = _i32(si.poly_ptr), _i32(si.mono_ptr), _i32(si.vars), _i32(si.exps)
+    sup = _Supports(len(pp) - 1, _ptr_i32(pp), _ptr_i32(mp), _ptr_i32(vv))
+    out = (ctypes.c_int64 * 4)()
+    rc = lib().mdps_test_plan(ctypes.byref(sup), _ptr_i32(ee), si.n, si.degree, si.limbs, 1 if eft else 0, batch,
+                              chunks, corrupt, out)
+    return rc, dict(unplanned_bytes=out[0], planned_bytes=out[1], chunks=out[2], launches=out[3]), mdps_last_error()
 
 
 def queue_config(max_blocks: int = 0, lanes: int = 0) -> None:

@@ -95,18 +95,18 @@ __global__ void __launch_bounds__(128) conv_eft_kernel(double *__restrict__ pool
     }
 }
 
-// tasks [0, n) write values_out, [n, n + n*n) write jacobian_out (row-major)
+// tasks [task0, task0 + ntasks) of [0, n) values_out, [n, n + n*n) jacobian_out (row-major)
 template <int L>
 __global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict__ pool,
                                                        const int *__restrict__ task_ptr,
                                                        const int *__restrict__ ent_slot,
-                                                       const int *__restrict__ ent_w, int ntasks,
+                                                       const int *__restrict__ ent_w, int task0, int ntasks,
                                                        int n, int D, double *__restrict__ values,
                                                        double *__restrict__ jac) {
     const int LD2 = 2 * L * D;
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (g >= (long long)ntasks * D) return;
-    const int task = (int)(g / D), k = (int)(g - (long long)task * D);
+    const int task = task0 + (int)(g / D), k = (int)(g % D);
     double Br[L + 1], Bi[L + 1];
     md_zero(Br);
     md_zero(Bi);

@@ -272,11 +272,13 @@ struct QueueGeomFn {
 
 template <int L>
 struct AccumEft {
-    static int run(const double *pool, const int *tp, const int *es, const int *ew, int ntasks, int n, int D,
-                   double *values, double *jac, cudaStream_t st) {
+    // addition jobs [task0, task0 + ntasks)
+    static int run(const double *pool, const int *tp, const int *es, const int *ew, int task0, int ntasks, int n,
+                   int D, double *values, double *jac, cudaStream_t st) {
+        if (ntasks <= 0) return MDPS_OK;
         const long long total = (long long)ntasks * D;
         const int blocks = (int)((total + 127) / 128);
-        accum_eft_kernel<L><<<blocks, 128, 0, st>>>(pool, tp, es, ew, ntasks, n, D, values, jac);
+        accum_eft_kernel<L><<<blocks, 128, 0, st>>>(pool, tp, es, ew, task0, ntasks, n, D, values, jac);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -308,7 +310,15 @@ struct mdps_system {
     int64_t qtickets = 0;
     int64_t njobs = 0;
     int64_t nslots = 0, products = 0, add_terms = 0, add_terms_w = 0;  // add_terms_w: weight != 1
-    std::vector<int64_t> level_off, level_cnt;  // in jobs
+    // LEVELS: row chunks run one after the other, each its levels then its
+    // addition-job ranges (schedule.hpp plan_memory); one chunk normally
+    struct ChunkRun {
+        std::vector<int64_t> lv_off, lv_cnt;  // in jobs
+        int32_t task0[2], ntask[2];
+    };
+    std::vector<ChunkRun> chunks;
+    int64_t pool_bytes = 0;
+    std::vector<int64_t> level_cnt;  // jobs per DAG level (diagnostics)
     int ntasks = 0;
     // device
     double *pool = nullptr;  // EFT: limb planes [slot][2][L][D]; DIGITS: digit planes [slot][2][S][D]
@@ -316,7 +326,6 @@ struct mdps_system {
     int *jobs = nullptr;     // all levels, (in1, in2, out) triples
     int *task_ptr = nullptr, *ent_slot = nullptr, *ent_w = nullptr;
     double *lpool = nullptr;  // DIGITS: limb planes of the series the addition jobs sum [lslot][2][L][D]
-    int *ent_lslot = nullptr; // DIGITS: addition terms indexed into lpool
     std::vector<std::pair<int32_t, int32_t>> x_lslots;  // (x index, lslot) of inputs summed directly
     double *host_in = nullptr;  // staging for the _host variant (device buffers)
     double *dev_in = nullptr, *dev_vals = nullptr, *dev_jac = nullptr;
@@ -373,7 +382,6 @@ static void free_system(mdps_system *s) {
     cudaFree(s->ent_slot);
     cudaFree(s->ent_w);
     cudaFree(s->lpool);
-    cudaFree(s->ent_lslot);
     cudaFree(s->dev_in);
     cudaFree(s->dev_vals);
     cudaFree(s->dev_jac);
@@ -448,9 +456,28 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
                               (sched_opt == MDPS_SCHED_AUTO && algo == MDPS_ALGO_EFT &&
                                S.products * (opt && opt->batch > 1 ? opt->batch : 1) <= MDPS_QUEUE_MAX_PRODUCTS)
                           ? MDPS_SCHED_QUEUE : MDPS_SCHED_LEVELS;
-    const std::vector<int32_t> limb_slot1(S.limb_slot.begin(), S.limb_slot.begin() + (size_t)(n + S.M));
-    const int64_t nlimb1 = S.nlimb;
     if (B > 1 && !replicate_schedule(S, n, B, err)) {
+        set_err(err);
+        return nullptr;
+    }
+    const bool eft = algo == MDPS_ALGO_EFT;
+    const int Sd = eft ? 0 : digits_for(limbs);
+    if (sched == MDPS_SCHED_LEVELS) {
+        // memory plan: liveness reuse; then as few row chunks as keep the
+        // pools within the budget (none by default)
+        const int64_t budget = (opt && opt->workspace_mb > 0) ? (int64_t)opt->workspace_mb << 20
+                               : (MDPS_DEFAULT_WORKSPACE_MB > 0 ? (int64_t)MDPS_DEFAULT_WORKSPACE_MB << 20 : 0);
+        if (opt && opt->workspace_mb < 0) { set_err("workspace_mb must be >= 0"); return nullptr; }
+        for (int C = 1;; C++) {
+            if (!plan_memory(S, n, C, eft, err)) {
+                set_err(err);
+                return nullptr;
+            }
+            if (budget == 0 || plan_bytes(S, Sd, limbs, D, eft) <= budget || C >= 64 || (int)S.chunks.size() < C ||
+                B > 1)
+                break;
+        }
+    } else if (!check_schedule(S, n, eft, err)) {
         set_err(err);
         return nullptr;
     }
@@ -463,23 +490,37 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->L = limbs;
     s->M = S.M;
     s->algo = algo;
-    s->S = algo == MDPS_ALGO_DIGITS ? digits_for(limbs) : 0;
+    s->S = Sd;
     s->use_graph = opt ? opt->use_graph : 0;
     s->real = real;
     s->batch = B;
-    s->nslots = S.nslots;
+    s->nslots = S.planned ? S.dig_slots : S.nslots;
     s->products = S.products;
     s->add_terms = (int64_t)S.ent_slot.size();
     for (int32_t w : S.ent_w) s->add_terms_w += w != 1;
     s->ntasks = B * (S.N + S.N * n);
     s->schedule = sched;
+    const int64_t nlimb = S.planned ? S.plan_nlimb : S.nlimb;
 
-    std::vector<int32_t> alljobs;  // (in1, in2, out, code) per job, level by level
-    for (auto &lv : S.levels4) {
-        s->level_off.push_back((int64_t)alljobs.size() / 4);
-        s->level_cnt.push_back((int64_t)lv.size() / 4);
-        alljobs.insert(alljobs.end(), lv.begin(), lv.end());
+    std::vector<int32_t> alljobs;  // (in1, in2, out, code) per job, launch by launch
+    if (S.planned) {
+        for (auto &ch : S.chunks) {
+            mdps_system::ChunkRun cr;
+            for (auto &lv : ch.levels4) {
+                cr.lv_off.push_back((int64_t)alljobs.size() / 4);
+                cr.lv_cnt.push_back((int64_t)lv.size() / 4);
+                alljobs.insert(alljobs.end(), lv.begin(), lv.end());
+            }
+            for (int r = 0; r < 2; r++) {
+                cr.task0[r] = ch.task0[r];
+                cr.ntask[r] = ch.ntask[r];
+            }
+            s->chunks.push_back(std::move(cr));
+        }
+    } else {
+        for (auto &lv : S.levels4) alljobs.insert(alljobs.end(), lv.begin(), lv.end());
     }
+    for (auto &lv : S.levels4) s->level_cnt.push_back((int64_t)lv.size() / 4);  // per DAG level (diagnostics)
     s->njobs = (int64_t)alljobs.size() / 4;
     if (sched == MDPS_SCHED_QUEUE) {
         if (s->njobs + (int64_t)s->ntasks >= (int64_t)INT32_MAX / 2) { set_err("queue: too many jobs"); free_system(s); return nullptr; }
@@ -494,12 +535,17 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
         }
     }
     const size_t ser = algo == MDPS_ALGO_DIGITS ? dig_slot_stride(s->S, D) : (size_t)2 * limbs * D;  // doubles per slot
+    const size_t before_pools = s->device_bytes;
     if (!dalloc(s, &s->pool, ser * (size_t)s->nslots) ||
         (algo == MDPS_ALGO_DIGITS && !dalloc(s, &s->epool, (size_t)2 * D * s->nslots)) ||
-        !dalloc(s, &s->jobs, alljobs.size()) || !dalloc(s, &s->task_ptr, S.task_ptr.size()) ||
-        !dalloc(s, &s->ent_slot, S.ent_slot.size()) || !dalloc(s, &s->ent_w, S.ent_w.size()) ||
-        (algo == MDPS_ALGO_DIGITS && (!dalloc(s, &s->lpool, (size_t)2 * limbs * D * S.nlimb) ||
-                                      !dalloc(s, &s->ent_lslot, S.ent_lslot.size())))) {
+        (algo == MDPS_ALGO_DIGITS && !dalloc(s, &s->lpool, (size_t)2 * limbs * D * nlimb))) {
+        free_system(s);
+        return nullptr;
+    }
+    s->pool_bytes = (int64_t)(s->device_bytes - before_pools);
+    const std::vector<int32_t> &ents = S.planned ? S.plan_ent : (eft ? S.ent_slot : S.ent_lslot);
+    if (!dalloc(s, &s->jobs, alljobs.size()) || !dalloc(s, &s->task_ptr, S.task_ptr.size()) ||
+        !dalloc(s, &s->ent_slot, ents.size()) || !dalloc(s, &s->ent_w, S.ent_w.size())) {
         free_system(s);
         return nullptr;
     }
@@ -509,25 +555,19 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     const size_t limb_ser = (size_t)2 * limbs * D;
     bool ok = up(s->jobs, alljobs.data(), alljobs.size() * 4) &&
               up(s->task_ptr, S.task_ptr.data(), S.task_ptr.size() * 4) &&
-              up(s->ent_slot, S.ent_slot.data(), S.ent_slot.size() * 4) &&
+              up(s->ent_slot, ents.data(), ents.size() * 4) &&
               up(s->ent_w, S.ent_w.data(), S.ent_w.size() * 4);
     if (ok && algo == MDPS_ALGO_DIGITS) {
-        ok = up(s->ent_lslot, S.ent_lslot.data(), S.ent_lslot.size() * 4);
         // summed coefficient series (constant terms, m = 1 without common
         // factor) are copied once into the limb pool; summed inputs x_j (none
         // with the current DAG) are copied at every eval
-        // (one copy per point of a batch, each point with its own limb-pool block)
-        for (int64_t slot = 0; ok && slot < (int64_t)n + S.M; slot++) {
-            const int32_t ls1 = limb_slot1[(size_t)slot];
-            if (ls1 < 0) continue;
-            for (int b = 0; ok && b < B; b++) {
-                const int32_t ls = (int32_t)(ls1 + (int64_t)b * nlimb1);
-                if (slot < n)
-                    s->x_lslots.emplace_back((int32_t)((int64_t)b * n + slot), ls);
-                else
-                    ok = up(s->lpool + (size_t)ls * limb_ser, coefficients + (size_t)(slot - n) * limb_ser,
-                            limb_ser * 8);
-            }
+        const int64_t nx = (int64_t)B * n;
+        for (auto &fl : S.fixed_limb) {
+            if (fl.first < nx)
+                s->x_lslots.emplace_back(fl.first, fl.second);
+            else
+                ok = ok && up(s->lpool + (size_t)fl.second * limb_ser, coefficients + (size_t)(fl.first - nx) * limb_ser,
+                              limb_ser * 8);
         }
     }
     if (ok && S.M > 0) {
@@ -586,43 +626,40 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
         TimedGroup tg(s, st, 0);
         return dispatch_L<QueueRun>(L, s, in, vals, jac, st);
     }
-    if (s->algo == MDPS_ALGO_EFT) {
-        {
-            TimedGroup tg(s, st, 2);
+    const bool eft = s->algo == MDPS_ALGO_EFT;
+    {
+        TimedGroup tg(s, st, 2);
+        if (eft) {
             CUDA_TRY(cudaMemcpyAsync(s->pool, in, (size_t)n * 2 * L * D * 8, cudaMemcpyDeviceToDevice, st),
                      MDPS_ECUDA);
+        } else {
+            rc = dispatch_L<ToDigits>(L, in, n, D, s->pool, s->epool, 0, st);
+            if (rc) return rc;
+            for (auto &xl : s->x_lslots)
+                CUDA_TRY(cudaMemcpyAsync(s->lpool + (size_t)xl.second * 2 * L * D, in + (size_t)xl.first * 2 * L * D,
+                                         (size_t)2 * L * D * 8, cudaMemcpyDeviceToDevice, st),
+                         MDPS_ECUDA);
         }
-        for (size_t lv = 0; lv < s->level_cnt.size(); lv++) {
+    }
+    // chunk by chunk (normally one): its product levels, then its addition
+    // jobs, which read the limb pool (EFT: the one pool) the products wrote
+    for (const auto &ch : s->chunks) {
+        for (size_t lv = 0; lv < ch.lv_cnt.size(); lv++) {
             TimedGroup tg(s, st, 0);
-            rc = dispatch_L<ConvEft>(L, s->pool, (const int *)(s->jobs + 4 * s->level_off[lv]),
-                                     (int)s->level_cnt[lv], D, st);
+            const int *jb = (const int *)(s->jobs + 4 * ch.lv_off[lv]);
+            rc = eft ? dispatch_L<ConvEft>(L, s->pool, jb, (int)ch.lv_cnt[lv], D, st)
+                     : dispatch_L<ConvDig>(L, s->pool, s->epool, s->lpool, jb, (int)ch.lv_cnt[lv], D, s->real, st);
             if (rc) return rc;
         }
         TimedGroup tg(s, st, 1);
-        return dispatch_L<AccumEft>(L, (const double *)s->pool, (const int *)s->task_ptr,
-                                    (const int *)s->ent_slot, (const int *)s->ent_w, s->ntasks, s->N * s->batch, D, vals,
-                                    jac, st);
+        for (int r = 0; r < 2; r++) {
+            rc = dispatch_L<AccumEft>(L, (const double *)(eft ? s->pool : s->lpool), (const int *)s->task_ptr,
+                                      (const int *)s->ent_slot, (const int *)s->ent_w, ch.task0[r], ch.ntask[r],
+                                      s->N * s->batch, D, vals, jac, st);
+            if (rc) return rc;
+        }
     }
-    {
-        TimedGroup tg(s, st, 2);
-        rc = dispatch_L<ToDigits>(L, in, n, D, s->pool, s->epool, 0, st);
-        if (rc) return rc;
-        for (auto &xl : s->x_lslots)
-            CUDA_TRY(cudaMemcpyAsync(s->lpool + (size_t)xl.second * 2 * L * D, in + (size_t)xl.first * 2 * L * D,
-                                     (size_t)2 * L * D * 8, cudaMemcpyDeviceToDevice, st),
-                     MDPS_ECUDA);
-    }
-    for (size_t lv = 0; lv < s->level_cnt.size(); lv++) {
-        TimedGroup tg(s, st, 0);
-        rc = dispatch_L<ConvDig>(L, s->pool, s->epool, s->lpool, (const int *)(s->jobs + 4 * s->level_off[lv]),
-                                 (int)s->level_cnt[lv], D, s->real, st);
-        if (rc) return rc;
-    }
-    // the addition jobs read the limb pool (the product jobs wrote limbs for
-    // exactly the series they sum)
-    TimedGroup tg(s, st, 1);
-    return dispatch_L<AccumEft>(L, (const double *)s->lpool, (const int *)s->task_ptr, (const int *)s->ent_lslot,
-                                (const int *)s->ent_w, s->ntasks, s->N * s->batch, D, vals, jac, st);
+    return MDPS_OK;
 }
 
 extern "C" int mdps_system_set_timing(mdps_system *s, int32_t enable) {
@@ -759,8 +796,15 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     out->levels = (int32_t)s->level_cnt.size();
     out->algo = s->algo;
     out->digits = s->S;
-    out->launches = s->schedule == MDPS_SCHED_QUEUE ? 1 : (int32_t)s->level_cnt.size() + 2;
+    int32_t launches = 1;  // QUEUE: one persistent launch
+    if (s->schedule != MDPS_SCHED_QUEUE) {
+        launches = 1;  // input conversion / copy
+        for (const auto &ch : s->chunks) launches += (int32_t)ch.lv_cnt.size() + (ch.ntask[0] > 0) + (ch.ntask[1] > 0);
+    }
+    out->launches = launches;
     out->schedule = s->schedule;
+    out->chunks = (int32_t)std::max<size_t>(1, s->chunks.size());
+    out->pool_bytes = s->pool_bytes;
     out->workspace_bytes = s->device_bytes;
     out->n = s->n;
     out->n_polys = s->N;
@@ -1072,4 +1116,82 @@ extern "C" int mdps_test_queue_trace(mdps_system *s, int32_t enable, int64_t *ou
         return (int)cnt;
     }
     return (int)s->qtickets;
+}
+
+// host-only check of the job schedule and its memory plan (no GPU needed):
+// out[0] pool bytes without reuse, out[1] with the plan, out[2] chunks,
+// out[3] launches per evaluation.  corrupt > 0 damages the plan first (1: a
+// job writes a slot another job of its launch reads; 2: a job overwrites a
+// slot that a later launch still reads; 3: an input slot out of range) —
+// the check must then fail (its own test).
+extern "C" int mdps_test_plan(const mdps_supports *sup, const int32_t *exponents, int32_t n, int32_t degree,
+                              int32_t limbs, int32_t eft, int32_t batch, int32_t chunks, int32_t corrupt,
+                              int64_t *out) {
+    if (!sup || !out || n < 1 || degree < 0 || !valid_limbs(limbs) || batch < 1 || chunks < 1) {
+        set_err("invalid argument");
+        return MDPS_EINVAL;
+    }
+    Schedule S;
+    std::string err;
+    if (!build_schedule(sup->n_polys, sup->poly_ptr, sup->mono_ptr, sup->vars, exponents, n, S, err) ||
+        (batch > 1 && !replicate_schedule(S, n, batch, err))) {
+        set_err(err);
+        return MDPS_EINVAL;
+    }
+    const int D = degree + 1, Sd = eft ? 0 : digits_for(limbs);
+    out[0] = plan_bytes(S, Sd, limbs, D, eft != 0);
+    if (!check_schedule(S, n, eft != 0, err) || !plan_memory(S, n, chunks, eft != 0, err)) {
+        set_err(err);
+        return MDPS_EINVAL;
+    }
+    out[1] = plan_bytes(S, Sd, limbs, D, eft != 0);
+    out[2] = (int64_t)S.chunks.size();
+    int64_t launches = 1;
+    for (auto &ch : S.chunks) launches += (int64_t)ch.levels4.size() + (ch.ntask[0] > 0) + (ch.ntask[1] > 0);
+    out[3] = launches;
+    if (corrupt > 0) {
+        const int64_t nfix = (int64_t)S.batch * n + S.M;
+        bool done = false;
+        for (auto &ch : S.chunks) {
+            for (size_t lv = 0; lv < ch.levels4.size() && !done; lv++) {
+                auto &v = ch.levels4[lv];
+                if (corrupt == 1) {  // the last job writes the first dynamic input read in this launch
+                    for (size_t q = 0; q < v.size() && !done; q += 4)
+                        for (int k = 0; k < 2 && !done; k++)
+                            if (v[q + k] >= nfix && v.size() >= 8) {
+                                v[v.size() - 4 + 2] = v[q + k];
+                                v[v.size() - 4 + 3] |= 1;
+                                done = true;
+                            }
+                } else if (corrupt == 2 && lv + 2 < ch.levels4.size()) {
+                    // a job of launch lv+1 overwrites an input that launch lv+2 reads and lv+1 does not write
+                    auto &w = ch.levels4[lv + 2];
+                    for (size_t q = 0; q < w.size() && !done; q += 4)
+                        if (w[q] >= nfix) {
+                            auto &u = ch.levels4[lv + 1];
+                            bool produced_here = false;
+                            for (size_t r = 0; r < u.size(); r += 4) produced_here |= u[r + 2] == w[q];
+                            if (produced_here) continue;
+                            u[2] = w[q];
+                            u[3] |= 1;
+                            done = true;
+                        }
+                } else if (corrupt == 3) {
+                    v[0] = (int32_t)(S.dig_slots + 5);
+                    done = true;
+                }
+            }
+        }
+        if (!done) {
+            set_err("nothing to corrupt");
+            return MDPS_EINVAL;
+        }
+        if (!check_schedule(S, n, eft != 0, err)) {
+            set_err(err);
+            return MDPS_EINVAL;  // detected
+        }
+        set_err("corruption not detected");
+        return 1;
+    }
+    return MDPS_OK;
 }

@@ -13,6 +13,7 @@ namespace {
 struct Builder {
     Schedule &S;
     std::vector<int32_t> level;  // per slot
+    int32_t row = 0;             // the polynomial whose monomial is being built
     explicit Builder(Schedule &s) : S(s) {}
 
     int32_t job(int32_t a, int32_t b) {
@@ -24,6 +25,7 @@ struct Builder {
         v.push_back(a);
         v.push_back(b);
         v.push_back(out);
+        S.job_row.push_back(row);
         S.products++;
         return out;
     }
@@ -63,7 +65,9 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
 
     std::vector<std::pair<int32_t, int32_t>> mono;
     std::vector<int32_t> f, Bk;
+    S.job_row.clear();
     for (int i = 0; i < n_polys; i++) {
+        B.row = i;
         for (int r = poly_ptr[i]; r < poly_ptr[i + 1]; r++) {
             mono.clear();
             for (int t = mono_ptr[r]; t < mono_ptr[r + 1]; t++) {
@@ -232,6 +236,312 @@ bool replicate_schedule(Schedule &S, int32_t n, int32_t B, std::string &err) {
     S.nlimb = (int64_t)B * nl;
     S.products *= B;
     S.batch = B;
+    return true;
+}
+
+}  // namespace mdps
+
+namespace mdps {
+
+namespace {
+
+// slots by liveness: acquire() the lowest-numbered free slot... a LIFO free
+// list keeps recently used (L2-warm) slots in use
+struct SlotPool {
+    int64_t base, next;
+    std::vector<int32_t> free_;
+    explicit SlotPool(int64_t b) : base(b), next(b) {}
+    int32_t acquire() {
+        if (!free_.empty()) {
+            const int32_t s = free_.back();
+            free_.pop_back();
+            return s;
+        }
+        return (int32_t)next++;
+    }
+    void release(int32_t s) { free_.push_back(s); }
+};
+
+}  // namespace
+
+bool plan_memory(Schedule &S, int32_t n, int32_t chunks, bool eft, std::string &err) {
+    const int64_t B = S.batch, nx = B * n, nfix = nx + S.M;
+    const int64_t ndyn = S.nslots - nfix;
+    if (chunks < 1) chunks = 1;
+    if (B > 1) chunks = 1;  // rows of a batch are per point: one chunk
+    if (chunks > S.N) chunks = S.N;
+    // ---- rows -> chunks, contiguous, balanced by product count
+    std::vector<int32_t> chunk_of_row((size_t)S.N, 0);
+    std::vector<int32_t> row_lo((size_t)chunks + 1, S.N);
+    row_lo[0] = 0;
+    if (chunks > 1) {
+        if ((int64_t)S.job_row.size() != ndyn) { err = "plan_memory: no row map"; return false; }
+        std::vector<int64_t> cost((size_t)S.N, 0);
+        for (int32_t r : S.job_row) cost[(size_t)r]++;
+        int64_t total = 0;
+        for (int64_t c : cost) total += c;
+        int64_t acc = 0;
+        int c = 0;
+        for (int32_t r = 0; r < S.N; r++) {
+            // start chunk c+1 once this chunk holds its share
+            if (c + 1 < chunks && acc >= total * (c + 1) / chunks && r > row_lo[(size_t)c]) row_lo[(size_t)++c] = r;
+            chunk_of_row[(size_t)r] = c;
+            acc += cost[(size_t)r];
+        }
+        chunks = c + 1;
+        row_lo.resize((size_t)chunks + 1);
+        row_lo[(size_t)chunks] = S.N;
+    }
+    // ---- launch order: chunk-major, level-minor (empty levels skipped), then
+    // the chunk's addition jobs
+    S.chunks.assign((size_t)chunks, Schedule::Chunk());
+    const int nlev = (int)S.levels4.size();
+    std::vector<std::vector<std::vector<int32_t>>> cl((size_t)chunks, std::vector<std::vector<int32_t>>((size_t)nlev));
+    for (int lv = 0; lv < nlev; lv++) {
+        const auto &v = S.levels4[(size_t)lv];
+        for (size_t q = 0; q < v.size(); q += 4) {
+            const int32_t out = v[q + 2];
+            const int c = chunks > 1 ? chunk_of_row[(size_t)S.job_row[(size_t)(out - nfix)]] : 0;
+            auto &d = cl[(size_t)c][(size_t)lv];
+            d.insert(d.end(), v.begin() + (long)q, v.begin() + (long)q + 4);
+        }
+    }
+    // launch index of every dynamic slot's producer, last product read, and
+    // the chunk's addition launch (summed series)
+    std::vector<int64_t> t_prod((size_t)ndyn, -1), t_read((size_t)ndyn, -1), t_sum((size_t)ndyn, -1);
+    std::vector<int64_t> t_accum((size_t)chunks, 0);
+    int64_t t = 0;
+    for (int c = 0; c < chunks; c++) {
+        for (int lv = 0; lv < nlev; lv++) {
+            const auto &v = cl[(size_t)c][(size_t)lv];
+            if (v.empty()) continue;
+            for (size_t q = 0; q < v.size(); q += 4) {
+                for (int k = 0; k < 2; k++)
+                    if (v[q + k] >= nfix) t_read[(size_t)(v[q + k] - nfix)] = t;
+                t_prod[(size_t)(v[q + 2] - nfix)] = t;
+            }
+            t++;
+        }
+        t_accum[(size_t)c] = t++;
+    }
+    const int64_t nlaunch = t;
+    // summed series: read by the addition launch of the chunk of their row
+    // (entries of task i, N + i n + j belong to row i)
+    const int64_t N = S.N;
+    auto task_row = [&](int64_t task) -> int64_t {
+        const int64_t per = N + N * n;  // tasks per point
+        const int64_t tt = task % per;
+        return tt < N ? tt : (tt - N) / n;
+    };
+    for (int64_t task = 0; task + 1 < (int64_t)S.task_ptr.size(); task++) {
+        const int c = chunks > 1 ? chunk_of_row[(size_t)task_row(task)] : 0;
+        for (int32_t e = S.task_ptr[(size_t)task]; e < S.task_ptr[(size_t)task + 1]; e++) {
+            const int32_t sl = S.ent_slot[(size_t)e];
+            if (sl >= nfix) t_sum[(size_t)(sl - nfix)] = t_accum[(size_t)c];
+        }
+    }
+    // ---- slot assignment in launch order; a slot whose last use is launch t
+    // is released before launch t + 1
+    std::vector<std::vector<int32_t>> rel_d((size_t)nlaunch + 1), rel_l((size_t)nlaunch + 1);
+    std::vector<int32_t> dslot((size_t)ndyn, -1), lslot((size_t)ndyn, -1);
+    // fixed limb slots: summed x / coefficient series, first
+    S.fixed_limb.clear();
+    int64_t nfixed_l = 0;
+    if (!eft) {
+        std::vector<int32_t> fl((size_t)nfix, -1);
+        for (int32_t sl : S.ent_slot)
+            if (sl < nfix && fl[(size_t)sl] < 0) fl[(size_t)sl] = 0;
+        for (int64_t sl = 0; sl < nfix; sl++)
+            if (fl[(size_t)sl] == 0) S.fixed_limb.emplace_back((int32_t)sl, (int32_t)nfixed_l++);
+    }
+    SlotPool pd(nfix), pl(nfixed_l);
+    t = 0;
+    for (int c = 0; c < chunks; c++) {
+        for (int lv = 0; lv < nlev; lv++) {
+            auto &v = cl[(size_t)c][(size_t)lv];
+            if (v.empty()) continue;
+            for (int32_t r : rel_d[(size_t)t]) pd.release(r);
+            for (int32_t r : rel_l[(size_t)t]) pl.release(r);
+            for (size_t q = 0; q < v.size(); q += 4) {
+                const int64_t o = v[q + 2] - nfix;
+                const bool input = t_read[(size_t)o] >= 0, summed = t_sum[(size_t)o] >= 0;
+                if (eft) {
+                    const int64_t last = std::max(t_read[(size_t)o], t_sum[(size_t)o]);
+                    if (last < 0) { err = "plan_memory: a product nobody reads"; return false; }
+                    dslot[(size_t)o] = pd.acquire();
+                    rel_d[(size_t)last + 1].push_back(dslot[(size_t)o]);
+                } else {
+                    if (input) {
+                        dslot[(size_t)o] = pd.acquire();
+                        rel_d[(size_t)t_read[(size_t)o] + 1].push_back(dslot[(size_t)o]);
+                    }
+                    if (summed) {
+                        lslot[(size_t)o] = pl.acquire();
+                        rel_l[(size_t)t_sum[(size_t)o] + 1].push_back(lslot[(size_t)o]);
+                    }
+                    if (!input && !summed) { err = "plan_memory: a product nobody reads"; return false; }
+                }
+            }
+            t++;
+        }
+        for (int32_t r : rel_d[(size_t)t]) pd.release(r);
+        for (int32_t r : rel_l[(size_t)t]) pl.release(r);
+        t++;
+    }
+    if (pd.next > INT32_MAX / 4 || (pl.next << 2) > INT32_MAX) { err = "plan_memory: slots overflow int32"; return false; }
+    S.dig_slots = pd.next;
+    S.plan_nlimb = pl.next;
+    // ---- rewrite the jobs and the addition entries
+    auto map_in = [&](int32_t s) -> int32_t { return s < nfix ? s : dslot[(size_t)(s - nfix)]; };
+    for (int c = 0; c < chunks; c++) {
+        auto &ch = S.chunks[(size_t)c];
+        for (int lv = 0; lv < nlev; lv++) {
+            auto &v = cl[(size_t)c][(size_t)lv];
+            if (v.empty()) continue;
+            std::vector<int32_t> w, o3;
+            w.reserve(v.size());
+            o3.reserve(v.size() / 4 * 3);
+            for (size_t q = 0; q < v.size(); q += 4) {
+                const int64_t o = v[q + 2] - nfix;
+                o3.push_back(v[q]);
+                o3.push_back(v[q + 1]);
+                o3.push_back(v[q + 2]);
+                w.push_back(map_in(v[q]));
+                w.push_back(map_in(v[q + 1]));
+                if (eft) {
+                    w.push_back(dslot[(size_t)o]);
+                    w.push_back(0);
+                } else {
+                    w.push_back(dslot[(size_t)o] >= 0 ? dslot[(size_t)o] : 0);
+                    w.push_back((lslot[(size_t)o] >= 0 ? ((lslot[(size_t)o] << 2) | 2) : 0) | (dslot[(size_t)o] >= 0 ? 1 : 0));
+                }
+            }
+            ch.levels4.push_back(std::move(w));
+            ch.orig3.push_back(std::move(o3));
+        }
+        if (chunks > 1) {
+            const int32_t r0 = row_lo[(size_t)c], r1 = row_lo[(size_t)c + 1];
+            ch.task0[0] = r0;
+            ch.ntask[0] = r1 - r0;
+            ch.task0[1] = (int32_t)(N + (int64_t)r0 * n);
+            ch.ntask[1] = (int32_t)((int64_t)(r1 - r0) * n);
+        } else {
+            ch.task0[0] = 0;
+            ch.ntask[0] = (int32_t)(S.task_ptr.size() - 1);
+        }
+    }
+    std::vector<int32_t> fixl((size_t)nfix, -1);
+    for (auto &fl : S.fixed_limb) fixl[(size_t)fl.first] = fl.second;
+    S.plan_ent.resize(S.ent_slot.size());
+    for (size_t e = 0; e < S.ent_slot.size(); e++) {
+        const int32_t sl = S.ent_slot[e];
+        if (eft) S.plan_ent[e] = map_in(sl);
+        else S.plan_ent[e] = sl < nfix ? fixl[(size_t)sl] : lslot[(size_t)(sl - nfix)];
+    }
+    S.planned = true;
+    return check_schedule(S, n, eft, err);
+}
+
+int64_t plan_bytes(const Schedule &S, int S_digits, int L, int D, bool eft) {
+    const int64_t limb = (int64_t)2 * L * D * 8;
+    if (eft) return (S.planned ? S.dig_slots : S.nslots) * limb;
+    const int64_t dig = (int64_t)2 * S_digits * D * 8 + (int64_t)2 * D * 4;
+    return (S.planned ? S.dig_slots : S.nslots) * dig + (S.planned ? S.plan_nlimb : S.nlimb) * limb;
+}
+
+bool check_schedule(const Schedule &S, int32_t n, bool eft, std::string &err) {
+    const int64_t nfix = (int64_t)S.batch * n + S.M;
+    auto fail = [&](const std::string &m) {
+        err = "schedule check: " + m;
+        return false;
+    };
+    if (!S.planned) {
+        // every dynamic slot written exactly once, at a level above its inputs'
+        std::vector<int32_t> lev((size_t)S.nslots, -1);
+        for (int64_t s = 0; s < nfix; s++) lev[(size_t)s] = 0;
+        for (size_t lv = 0; lv < S.levels4.size(); lv++) {
+            const auto &v = S.levels4[lv];
+            for (size_t q = 0; q < v.size(); q += 4) {
+                for (int k = 0; k < 3; k++)
+                    if (v[q + k] < 0 || v[q + k] >= S.nslots) return fail("slot out of range");
+                if (lev[(size_t)v[q + 2]] >= 0) return fail("a slot written twice");
+                for (int k = 0; k < 2; k++)
+                    if (lev[(size_t)v[q + k]] < 0 || lev[(size_t)v[q + k]] > (int)lv)
+                        return fail("an input not written by an earlier level");
+            }
+            for (size_t q = 0; q < v.size(); q += 4) lev[(size_t)v[q + 2]] = (int32_t)lv + 1;
+        }
+        for (int32_t sl : S.ent_slot)
+            if (sl < 0 || sl >= S.nslots || lev[(size_t)sl] < 0) return fail("a summed series never written");
+        return true;
+    }
+    // planned: replay the launches; per pool slot the original series it holds
+    const int64_t npool = S.dig_slots;
+    std::vector<int32_t> holds((size_t)npool, -1), holds_l((size_t)S.plan_nlimb, -1);
+    std::vector<int64_t> wrote_at((size_t)npool, -1), wrote_at_l((size_t)S.plan_nlimb, -1);
+    for (int64_t s = 0; s < nfix && s < npool; s++) holds[(size_t)s] = (int32_t)s;
+    for (auto &fl : S.fixed_limb) {
+        if (fl.second < 0 || fl.second >= S.plan_nlimb) return fail("fixed limb slot out of range");
+        holds_l[(size_t)fl.second] = fl.first;
+    }
+    int64_t t = 0;
+    for (const auto &ch : S.chunks) {
+        for (size_t lv = 0; lv < ch.levels4.size(); lv++) {
+            const auto &v = ch.levels4[lv];
+            const auto &o = ch.orig3[lv];
+            if (o.size() / 3 != v.size() / 4) return fail("planned/original job count");
+            for (size_t j = 0; j < v.size() / 4; j++)  // reads: the intended series, written by an earlier launch
+                for (int k = 0; k < 2; k++) {
+                    const int32_t p = v[4 * j + k];
+                    if (p < 0 || p >= npool) return fail("input slot out of range");
+                    if (holds[(size_t)p] != o[3 * j + k]) return fail("an input overwritten or never written");
+                }
+            for (size_t j = 0; j < v.size() / 4; j++) {  // writes: no slot twice per launch, none read in it
+                const int32_t p = v[4 * j + 2], code = v[4 * j + 3];
+                const bool wd = eft || (code & 1), wl = !eft && (code & 2);
+                if (wd) {
+                    if (p < nfix || p >= npool) return fail("output slot out of range");
+                    if (wrote_at[(size_t)p] == t) return fail("a slot written twice in one launch");
+                    holds[(size_t)p] = o[3 * j + 2];
+                    wrote_at[(size_t)p] = t;
+                }
+                if (wl) {
+                    const int32_t ls = code >> 2;
+                    if (ls < 0 || ls >= S.plan_nlimb) return fail("limb slot out of range");
+                    if (wrote_at_l[(size_t)ls] == t) return fail("a limb slot written twice in one launch");
+                    holds_l[(size_t)ls] = o[3 * j + 2];
+                    wrote_at_l[(size_t)ls] = t;
+                }
+            }
+            for (size_t j = 0; j < v.size() / 4; j++)  // no input slot of this launch also written in it
+                for (int k = 0; k < 2; k++)
+                    if (wrote_at[(size_t)v[4 * j + k]] == t) return fail("a slot read and overwritten in one launch");
+            t++;
+        }
+        // the chunk's addition jobs read the series they sum
+        for (int r = 0; r < 2; r++)
+            for (int32_t task = ch.task0[r]; task < ch.task0[r] + ch.ntask[r]; task++)
+                for (int32_t e = S.task_ptr[(size_t)task]; e < S.task_ptr[(size_t)task + 1]; e++) {
+                    const int32_t p = S.plan_ent[(size_t)e];
+                    if (eft) {
+                        if (p < 0 || p >= npool || holds[(size_t)p] != S.ent_slot[(size_t)e])
+                            return fail("a summed series overwritten or never written");
+                    } else if (p < 0 || p >= S.plan_nlimb || holds_l[(size_t)p] != S.ent_slot[(size_t)e]) {
+                        return fail("a summed series overwritten or never written");
+                    }
+                }
+        t++;
+    }
+    // every addition job covered by exactly one chunk range
+    std::vector<uint8_t> cov(S.task_ptr.size() - 1, 0);
+    for (const auto &ch : S.chunks)
+        for (int r = 0; r < 2; r++)
+            for (int32_t task = ch.task0[r]; task < ch.task0[r] + ch.ntask[r]; task++) {
+                if (task < 0 || task >= (int32_t)cov.size() || cov[(size_t)task]) return fail("addition ranges");
+                cov[(size_t)task] = 1;
+            }
+    for (uint8_t c : cov)
+        if (!c) return fail("an addition job in no chunk");
     return true;
 }
 

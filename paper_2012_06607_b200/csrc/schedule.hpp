@@ -44,6 +44,21 @@ struct Schedule {
     int batch = 1;
     std::vector<int32_t> limb_slot1;
     int64_t nlimb1 = 0;
+    // row (polynomial) of every product job's output, slot - n - M (batch 1)
+    std::vector<int32_t> job_row;
+    // memory plan (plan_memory): chunks of rows run one after the other, each
+    // its levels then its addition jobs; slots reused by liveness
+    struct Chunk {
+        std::vector<std::vector<int32_t>> levels4;  // non-empty levels, (in1, in2, out, code) per job
+        std::vector<std::vector<int32_t>> orig3;    // the same jobs' unplanned (in1, in2, out) (checks)
+        int32_t task0[2] = {0, 0}, ntask[2] = {0, 0};  // addition-job ranges (values, Jacobian rows)
+    };
+    std::vector<Chunk> chunks;
+    bool planned = false;
+    std::vector<std::pair<int32_t, int32_t>> fixed_limb;  // (slot < nx + M, limb slot) of summed inputs
+    std::vector<int32_t> plan_ent;  // per addition entry: its planned slot (EFT pool) or limb slot (digits)
+    int64_t dig_slots = 0;          // digit pool (or EFT pool) slots after planning
+    int64_t plan_nlimb = 0;         // limb pool slots after planning (digits)
 };
 
 // Validates the inputs (libmdps.h) and builds the schedule.  Pool slots:
@@ -58,5 +73,28 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
 // addition jobs are the B N values then the B N n Jacobian entries, each
 // point with its own limb-pool block.  The kernels are unchanged.
 bool replicate_schedule(Schedule &S, int32_t n, int32_t B, std::string &err);
+
+// Memory plan for the leveled launch order: the rows are split
+// into `chunks` contiguous groups balanced by product count (batch 1 only),
+// run one after the other (each: its levels, then its addition jobs), and
+// every product output gets a pool slot only for its live range — from the
+// launch that writes it to the last launch that reads it (a product input:
+// digit slot; a summed series: limb slot, read by its chunk's addition jobs).
+// A slot freed after launch t is reused from launch t + 1 on (launches are
+// stream-ordered, so no two launches overlap).  eft: one pool of limb series
+// for both roles.  Rewrites the job tuples and the addition entries.
+bool plan_memory(Schedule &S, int32_t n, int32_t chunks, bool eft, std::string &err);
+
+// Bytes of the plan's pools: digits (2 S D doubles + 2 D ints per slot) and
+// limbs (2 L D doubles per slot), or one limb pool for eft.
+int64_t plan_bytes(const Schedule &S, int S_digits, int L, int D, bool eft);
+
+// Checks a schedule (planned or not): every slot index in range; every job
+// output written exactly once per evaluation (unplanned) or, planned, no
+// slot read after it was overwritten and no slot written while a launch
+// still reads it; every input of a launch written by an EARLIER launch (or a
+// fixed input); every summed series written before its addition jobs.  The
+// race-freedom and bounds invariants of the kernels' reads and writes.
+bool check_schedule(const Schedule &S, int32_t n, bool eft, std::string &err);
 
 }  // namespace mdps
