@@ -465,9 +465,13 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     if (sched == MDPS_SCHED_LEVELS) {
         // memory plan: liveness reuse; then as few row chunks as keep the
         // pools within the budget (none by default)
-        const int64_t budget = (opt && opt->workspace_mb > 0) ? (int64_t)opt->workspace_mb << 20
-                               : (MDPS_DEFAULT_WORKSPACE_MB > 0 ? (int64_t)MDPS_DEFAULT_WORKSPACE_MB << 20 : 0);
         if (opt && opt->workspace_mb < 0) { set_err("workspace_mb must be >= 0"); return nullptr; }
+        int64_t budget = (opt && opt->workspace_mb > 0) ? (int64_t)opt->workspace_mb << 20 : 0;
+        if (budget == 0) {  // default: a quarter of the device memory free now
+            size_t fr = 0, tot = 0;
+            if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = (int64_t)(fr / 4);
+            cudaGetLastError();
+        }
         for (int C = 1;; C++) {
             if (!plan_memory(S, n, C, eft, err)) {
                 set_err(err);
