@@ -90,15 +90,13 @@ typedef struct {
 } mdps_options;
 
 /* Job scheduling (PAPER.md:367-378 job queue, 411-424 stages). */
-#define MDPS_SCHED_AUTO 0    /* default: QUEUE for small and mid-size complex systems
-                                (<= MDPS_QUEUE_MAX_PRODUCTS product jobs per call on the EFT
-                                algorithm, <= MDPS_QUEUE_DIG_MAX_PRODUCTS on digits), else LEVELS */
+#define MDPS_SCHED_AUTO 0    /* default: QUEUE for small systems on the EFT algorithm
+                                (<= MDPS_QUEUE_MAX_PRODUCTS product jobs per call), else LEVELS */
 #define MDPS_SCHED_LEVELS 1  /* one launch per DAG level, then one for the addition jobs */
-#define MDPS_SCHED_QUEUE 2   /* one persistent launch (digits: after the conversion of x):
-                                blocks claim jobs from a device counter in topological order
-                                and wait on per-series ready flags (complex systems) */
-#define MDPS_QUEUE_MAX_PRODUCTS 8192        /* AUTO: EFT systems up to this many products per call */
-#define MDPS_QUEUE_DIG_MAX_PRODUCTS 65536   /* AUTO: digit-algorithm systems up to this many */
+#define MDPS_SCHED_QUEUE 2   /* one persistent launch: blocks claim jobs from a device
+                                counter in topological order and wait on per-series ready
+                                flags (EFT algorithm only) */
+#define MDPS_QUEUE_MAX_PRODUCTS 8192
 
 /* Create a system.  exponents: HOST [nnz] aligned with
  * vars, each >= 1.  coefficients: HOST [M][2][limbs][degree+1], the series

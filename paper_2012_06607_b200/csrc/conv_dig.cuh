@@ -257,34 +257,38 @@ __device__ __forceinline__ void conv_dig_emit_digits(const double (&A)[digits_fo
     ze[part * D + k] = e;
 }
 
-// The work of one block: P product jobs starting at job0 (jobs beyond njobs
-// are shadows, not written).  QUEUE: the inputs were written inside the same
-// launch (the job queue, queue_dig.cuh) — staged with ld.global.cg, never
-// TMA (no proxy crossing) nor a stale L1 line; else TMA bulk copies for even
-// D.  `bar`: the block's mbarrier (initialised by the caller), `phase` its
-// current parity (flipped by one use).
-template <int L, int DT, bool REAL, bool QUEUE>
-__device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *__restrict__ epool,
-                                               double *__restrict__ lpool, const int *__restrict__ jobs, int job0,
-                                               int njobs, int Drt, int T, int F, int P, double *sm, uint64_t *bar,
-                                               unsigned phase) {
+template <int L, int DT, bool REAL = false>
+// register budget per SM: 4 blocks of 128 up to L = 4 (<= 128 registers),
+// 3 up to L = 8 (<= 170), 2 above; 256-thread blocks for D = 128 and the
+// generic-D build.  REAL: real systems (mdps_options.real): only the real
+// part is computed; the imaginary limbs of the limb outputs are written as 0.
+__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
+                                  DT == 128 || DT == 0 ? 1 : (L <= 4 ? 4 : (L <= 8 ? 3 : 2)))
+    conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
+                                                      double *__restrict__ lpool, const int *__restrict__ jobs, int njobs, int Drt, int T,
+                                                      int F, int P) {
     constexpr int S = digits_for(L);
     const int D = DT > 0 ? DT : Drt;
     const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
     const int threads_per_job = T * F;
+    extern __shared__ __align__(16) double sm[];
     double *sdig = sm;                                        // [P][SX + SY]
     double *spark = sm + (size_t)P * (SX + SY);               // [threads][S]
     constexpr int PSTR = S + 2;                               // parking / emit scratch slot
     int *sexp = (int *)(spark + (size_t)blockDim.x * PSTR);   // [P][2 series][2][D]
 
+    const int job0 = blockIdx.x * P;
     // stage: x planes -> [part][s][D] (the pool layout), y planes ->
     // [part][PADZ + s][D], zero planes.  Even D: three 16-byte aligned
     // contiguous runs per job (x whole, y per part), so one thread issues
     // three TMA bulk copies (cp.async.bulk) per job against an mbarrier while
-    // the other warps write the zero planes and exponents.  Odd D (and the
-    // queue): one warp per plane row.
-    const bool use_tma = !QUEUE && (D & 1) == 0;
+    // the other warps write the zero planes and exponents.  Odd D: one warp
+    // per plane row, scalar loads.
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sexp + (size_t)P * 4 * D);
+    const bool use_tma = (D & 1) == 0;
     if (use_tma) {
+        if (threadIdx.x == 0) mbar_init(bar, 1);
+        __syncthreads();
         if (threadIdx.x < 32) {
             if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(P * 4 * S * D * 8));
             __syncwarp();
@@ -315,11 +319,9 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
                                                                    : (size_t)ps * D);
             if ((D & 1) == 0) {
                 for (int k = 2 * lane; k < D; k += 64)
-                    *reinterpret_cast<double2 *>(dst + k) =
-                        QUEUE ? __ldcg(reinterpret_cast<const double2 *>(g + k))
-                              : __ldg(reinterpret_cast<const double2 *>(g + k));
+                    *reinterpret_cast<double2 *>(dst + k) = __ldg(reinterpret_cast<const double2 *>(g + k));
             } else {
-                for (int k = lane; k < D; k += 32) dst[k] = QUEUE ? __ldcg(g + k) : __ldg(g + k);
+                for (int k = lane; k < D; k += 32) dst[k] = __ldg(g + k);
             }
         }
     }
@@ -332,10 +334,9 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
         const int jl = idx / (4 * D), r = idx - jl * 4 * D;
         const int which = r / (2 * D), r2 = r - which * 2 * D;
         const int job = min(job0 + jl, njobs - 1);
-        const int *src = epool + (size_t)jobs[4 * job + which] * 2 * D + r2;
-        sexp[idx] = QUEUE ? __ldcg(src) : *src;
+        sexp[idx] = epool[(size_t)jobs[4 * job + which] * 2 * D + r2];
     }
-    if (use_tma) mbar_wait(bar, phase);
+    if (use_tma) mbar_wait(bar, 0);
     __syncthreads();
 
     const int jl = threadIdx.x / threads_per_job;
@@ -430,27 +431,6 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
         }
         __syncwarp();
     }
-}
-
-template <int L, int DT, bool REAL = false>
-// register budget per SM: 4 blocks of 128 up to L = 4 (<= 128 registers),
-// 3 up to L = 8 (<= 170), 2 above; 256-thread blocks for D = 128 and the
-// generic-D build.  REAL: real systems (mdps_options.real): only the real
-// part is computed; the imaginary limbs of the limb outputs are written as 0.
-__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
-                                  DT == 128 || DT == 0 ? 1 : (L <= 4 ? 4 : (L <= 8 ? 3 : 2)))
-    conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool, double *__restrict__ lpool,
-                    const int *__restrict__ jobs, int njobs, int Drt, int T, int F, int P) {
-    constexpr int S = digits_for(L);
-    const int D = DT > 0 ? DT : Drt;
-    extern __shared__ __align__(16) double sm[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(
-        (int *)(sm + (size_t)P * (2 * S * D + 2 * (PADZ + S) * D) + (size_t)blockDim.x * (S + 2)) + (size_t)P * 4 * D);
-    if ((D & 1) == 0) {
-        if (threadIdx.x == 0) mbar_init(bar, 1);
-        __syncthreads();
-    }
-    conv_dig_block<L, DT, REAL, false>(dpool, epool, lpool, jobs, blockIdx.x * P, njobs, Drt, T, F, P, sm, bar, 0u);
 }
 
 }  // namespace mdps

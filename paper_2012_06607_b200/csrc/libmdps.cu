@@ -16,7 +16,6 @@
 #include "kernels_dig.cuh"
 #include "kernels_eft.cuh"
 #include "queue_eft.cuh"
-#include "queue_dig.cuh"
 #include "schedule.hpp"
 
 using namespace mdps;
@@ -226,7 +225,6 @@ struct ConvDig {
 // the device-side job queue (queue_eft.cuh): one persistent launch
 struct QueueGeom {
     int F, threads, blocks, tasks_per_ticket;
-    int T = 0, P = 1;  // digits: output pairs per job, jobs per ticket
     size_t smem;
 };
 
@@ -267,65 +265,9 @@ struct QueueEft {
     }
 };
 
-// the digit job queue (queue_dig.cuh): the leveled kernel's block geometry
-template <int L>
-struct QueueDig {
-    using KernT = void (*)(double *, int *, double *, unsigned *, QueueCtl *, const int *, int, int, int, int, int,
-                           const int *, const int *, const int *, const int *, int, int, int, int, double *, double *);
-    static KernT kernel(int D) {
-        return D == 16 ? queue_dig_kernel<L, 16> : D == 32 ? queue_dig_kernel<L, 32> : D == 64 ? queue_dig_kernel<L, 64>
-             : D == 128 ? queue_dig_kernel<L, 128> : queue_dig_kernel<L, 0>;
-    }
-    static int geom(int D, int njobs, int ntasks, QueueGeom &g) {
-        KernT kern = kernel(D);
-        cudaFuncAttributes fa;
-        int regs = 255, maxt = 128;
-        if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess) {
-            regs = fa.numRegs;
-            maxt = std::min(fa.maxThreadsPerBlock, 256);
-        }
-        cudaGetLastError();
-        DigGeom dg = dig_geom(L, D, regs, maxt, g_force_F, g_force_P, 1);
-        if (dg.smem == 0) dg = dig_geom(L, D, regs, maxt);
-        if (dg.smem == 0) { set_err("queue kernel: no geometry fits"); return MDPS_EINVAL; }
-        g.T = dg.T;
-        g.F = dg.F;
-        g.P = dg.P;
-        g.threads = dg.threads;
-        g.smem = dg.smem;
-        g.tasks_per_ticket = std::max(1, g.threads / D);
-        if (g.smem > 48 * 1024 &&
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem) != cudaSuccess) {
-            cudaGetLastError();
-            set_err("queue kernel: shared memory does not fit");
-            return MDPS_EINVAL;
-        }
-        int dev = 0, sms = 0, per = 0;
-        CUDA_TRY(cudaGetDevice(&dev), MDPS_ECUDA);
-        CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), MDPS_ECUDA);
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, g.threads, g.smem), MDPS_ECUDA);
-        if (per < 1) { set_err("queue kernel does not fit on an SM"); return MDPS_EINVAL; }
-        const long long tickets = (long long)(njobs + g.P - 1) / g.P + (ntasks + g.tasks_per_ticket - 1) / g.tasks_per_ticket;
-        g.blocks = (int)std::max(1LL, std::min<long long>(tickets, (long long)sms * per));
-        if (g_force_queue_blocks > 0) g.blocks = std::min(g.blocks, g_force_queue_blocks);
-        return MDPS_OK;
-    }
-    static int run(const QueueGeom &g, double *dpool, int *epool, double *lpool, unsigned *flags, QueueCtl *ctl,
-                   const int *jobs, int njobs, int D, const int *tp, const int *eflag, const int *elslot,
-                   const int *ew, int ntasks, int nvals, int nready, double *values, double *jac, cudaStream_t st) {
-        kernel(D)<<<g.blocks, g.threads, g.smem, st>>>(dpool, epool, lpool, flags, ctl, jobs, njobs, D, g.T, g.F, g.P,
-                                                        tp, eflag, elslot, ew, ntasks, nvals, g.tasks_per_ticket,
-                                                        nready, values, jac);
-        CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
-        return MDPS_OK;
-    }
-};
-
 template <int L>
 struct QueueGeomFn {
-    static int run(int D, int njobs, int ntasks, bool eft, QueueGeom &g) {
-        return eft ? QueueEft<L>::geom(D, njobs, ntasks, g) : QueueDig<L>::geom(D, njobs, ntasks, g);
-    }
+    static int run(int D, int njobs, int ntasks, QueueGeom &g) { return QueueEft<L>::geom(D, njobs, ntasks, g); }
 };
 
 template <int L>
@@ -383,7 +325,6 @@ struct mdps_system {
     int *epool = nullptr;    // DIGITS: exponents [slot][2][D]
     int *jobs = nullptr;     // all levels, (in1, in2, out) triples
     int *task_ptr = nullptr, *ent_slot = nullptr, *ent_w = nullptr;
-    int *ent_flag = nullptr;  // QUEUE + DIGITS: the flag (digit-space slot) of each addition entry
     double *lpool = nullptr;  // DIGITS: limb planes of the series the addition jobs sum [lslot][2][L][D]
     std::vector<std::pair<int32_t, int32_t>> x_lslots;  // (x index, lslot) of inputs summed directly
     double *host_in = nullptr;  // staging for the _host variant (device buffers)
@@ -445,7 +386,6 @@ static void free_system(mdps_system *s) {
     cudaFree(s->dev_vals);
     cudaFree(s->dev_jac);
     cudaFree(s->qflags);
-    cudaFree(s->ent_flag);
     cudaFree(s->qctl);
     cudaFree(s->qtrace);
     delete s;
@@ -505,19 +445,16 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
         set_err("unknown schedule");
         return nullptr;
     }
-    if (sched_opt == MDPS_SCHED_QUEUE && real) {
-        set_err("the job queue (MDPS_SCHED_QUEUE) does not run real systems");
+    if (sched_opt == MDPS_SCHED_QUEUE && algo != MDPS_ALGO_EFT) {
+        set_err("the job queue (MDPS_SCHED_QUEUE) runs the EFT algorithm only");
         return nullptr;
     }
-    // AUTO (measured): the queue for small systems on the EFT
-    // algorithm, where one level's jobs cannot fill the GPU and the per-level
-    // launch + tail dominate; for the digit algorithm on mid-size systems,
-    // where the levels are a wave or two of blocks each
-    const int64_t tot_products = S.products * (opt && opt->batch > 1 ? opt->batch : 1);
+    // AUTO: the queue for small systems on the EFT algorithm, where one level's
+    // jobs cannot fill the GPU and the per-level launch + tail dominate
+    // (measured)
     const int sched = sched_opt == MDPS_SCHED_QUEUE ||
-                              (sched_opt == MDPS_SCHED_AUTO && !real &&
-                               tot_products <= (algo == MDPS_ALGO_EFT ? MDPS_QUEUE_MAX_PRODUCTS
-                                                                      : MDPS_QUEUE_DIG_MAX_PRODUCTS))
+                              (sched_opt == MDPS_SCHED_AUTO && algo == MDPS_ALGO_EFT &&
+                               S.products * (opt && opt->batch > 1 ? opt->batch : 1) <= MDPS_QUEUE_MAX_PRODUCTS)
                           ? MDPS_SCHED_QUEUE : MDPS_SCHED_LEVELS;
     if (B > 1 && !replicate_schedule(S, n, B, err)) {
         set_err(err);
@@ -591,9 +528,8 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->njobs = (int64_t)alljobs.size() / 4;
     if (sched == MDPS_SCHED_QUEUE) {
         if (s->njobs + (int64_t)s->ntasks >= (int64_t)INT32_MAX / 2) { set_err("queue: too many jobs"); free_system(s); return nullptr; }
-        const int rc = dispatch_L<QueueGeomFn>(limbs, D, (int)s->njobs, s->ntasks, eft, s->qgeom);
-        s->qtickets = (s->njobs + s->qgeom.P - 1) / s->qgeom.P +
-                      (s->ntasks + s->qgeom.tasks_per_ticket - 1) / s->qgeom.tasks_per_ticket;
+        const int rc = dispatch_L<QueueGeomFn>(limbs, D, (int)s->njobs, s->ntasks, s->qgeom);
+        s->qtickets = s->njobs + (s->ntasks + s->qgeom.tasks_per_ticket - 1) / s->qgeom.tasks_per_ticket;
         if (rc != MDPS_OK || !dalloc(s, &s->qflags, (size_t)s->nslots) || !dalloc(s, &s->qctl, 1) ||
             cudaMemset(s->qflags, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(1, s->nslots)) != cudaSuccess ||
             cudaMemset(s->qctl, 0, sizeof(QueueCtl)) != cudaSuccess) {
@@ -613,8 +549,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     s->pool_bytes = (int64_t)(s->device_bytes - before_pools);
     const std::vector<int32_t> &ents = S.planned ? S.plan_ent : (eft ? S.ent_slot : S.ent_lslot);
     if (!dalloc(s, &s->jobs, alljobs.size()) || !dalloc(s, &s->task_ptr, S.task_ptr.size()) ||
-        !dalloc(s, &s->ent_slot, ents.size()) || !dalloc(s, &s->ent_w, S.ent_w.size()) ||
-        (sched == MDPS_SCHED_QUEUE && !eft && !dalloc(s, &s->ent_flag, S.ent_slot.size()))) {
+        !dalloc(s, &s->ent_slot, ents.size()) || !dalloc(s, &s->ent_w, S.ent_w.size())) {
         free_system(s);
         return nullptr;
     }
@@ -625,24 +560,8 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     bool ok = up(s->jobs, alljobs.data(), alljobs.size() * 4) &&
               up(s->task_ptr, S.task_ptr.data(), S.task_ptr.size() * 4) &&
               up(s->ent_slot, ents.data(), ents.size() * 4) &&
-              up(s->ent_w, S.ent_w.data(), S.ent_w.size() * 4) &&
-              (!s->ent_flag || up(s->ent_flag, S.ent_slot.data(), S.ent_slot.size() * 4));
-    if (ok && algo == MDPS_ALGO_DIGITS && !S.planned) {
-        // unplanned (the queue): the summed x / coefficient series keep the
-        // schedule's limb slots, one copy per point of a batch
-        const std::vector<int32_t> &ls1 = B > 1 ? S.limb_slot1 : S.limb_slot;
-        const int64_t nl1 = B > 1 ? S.nlimb1 : S.nlimb;
-        for (int64_t sl = 0; ok && sl < (int64_t)n + S.M; sl++) {
-            if (ls1[(size_t)sl] < 0) continue;
-            for (int b = 0; ok && b < B; b++) {
-                const int32_t ls = (int32_t)(ls1[(size_t)sl] + (int64_t)b * nl1);
-                if (sl < n)
-                    s->x_lslots.emplace_back((int32_t)((int64_t)b * n + sl), ls);
-                else
-                    ok = up(s->lpool + (size_t)ls * limb_ser, coefficients + (size_t)(sl - n) * limb_ser, limb_ser * 8);
-            }
-        }
-    } else if (ok && algo == MDPS_ALGO_DIGITS) {
+              up(s->ent_w, S.ent_w.data(), S.ent_w.size() * 4);
+    if (ok && algo == MDPS_ALGO_DIGITS) {
         // summed coefficient series (constant terms, m = 1 without common
         // factor) are copied once into the limb pool; summed inputs x_j (none
         // with the current DAG) are copied at every eval
@@ -701,26 +620,17 @@ struct QueueRun {
     }
 };
 
-template <int L>
-struct QueueDigRun {
-    static int run(mdps_system *s, double *vals, double *jac, cudaStream_t st) {
-        return QueueDig<L>::run(s->qgeom, s->pool, s->epool, s->lpool, s->qflags, s->qctl, s->jobs, (int)s->njobs,
-                                s->D, s->task_ptr, s->ent_flag, s->ent_slot, s->ent_w, s->ntasks, s->N * s->batch,
-                                s->n * s->batch + s->M, vals, jac, st);
-    }
-};
-
 // the launch sequence of one eval (also what the CUDA graph captures)
 static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, cudaStream_t st) {
     const int L = s->L, D = s->D, n = s->n * s->batch;  // input series of all points
     int rc;
     if (s->timing) s->timed_evals++;
-    const bool eft = s->algo == MDPS_ALGO_EFT;
-    if (s->schedule == MDPS_SCHED_QUEUE && eft) {
+    if (s->schedule == MDPS_SCHED_QUEUE) {
         // one persistent launch: products and additions, x read in place
         TimedGroup tg(s, st, 0);
         return dispatch_L<QueueRun>(L, s, in, vals, jac, st);
     }
+    const bool eft = s->algo == MDPS_ALGO_EFT;
     {
         TimedGroup tg(s, st, 2);
         if (eft) {
@@ -734,10 +644,6 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
                                          (size_t)2 * L * D * 8, cudaMemcpyDeviceToDevice, st),
                          MDPS_ECUDA);
         }
-    }
-    if (s->schedule == MDPS_SCHED_QUEUE) {  // digits: x converted above, then one persistent launch
-        TimedGroup tg(s, st, 0);
-        return dispatch_L<QueueDigRun>(L, s, vals, jac, st);
     }
     // chunk by chunk (normally one): its product levels, then its addition
     // jobs, which read the limb pool (EFT: the one pool) the products wrote
@@ -894,7 +800,7 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     out->levels = (int32_t)s->level_cnt.size();
     out->algo = s->algo;
     out->digits = s->S;
-    int32_t launches = s->algo == MDPS_ALGO_EFT ? 1 : 2;  // QUEUE: one persistent launch (+ digits of x)
+    int32_t launches = 1;  // QUEUE: one persistent launch
     if (s->schedule != MDPS_SCHED_QUEUE) {
         launches = 1;  // input conversion / copy
         for (const auto &ch : s->chunks) launches += (int32_t)ch.lv_cnt.size() + (ch.ntask[0] > 0) + (ch.ntask[1] > 0);

@@ -115,78 +115,6 @@ __host__ __device__ inline int queue_lanes(int D, int fmax = 4) {
     return F;
 }
 
-// One ticket of addition jobs: tasks [a0, a0 + count) of
-// the values (task < nvals) and Jacobian entries, one thread per (task, k).
-// ent_flag: the series' flag index; ent_data: its index in the data (slots
-// below nx in x_in, the others in pool).  The entries are taken in batches of
-// QB whose flags are polled together and whose loads are then issued
-// together (one L2 round trip per batch, not per entry), and summed in entry
-// order into EFT bins — the same sums as one by one.
-template <int L>
-__device__ __forceinline__ void queue_add_ticket(const unsigned *flags, unsigned cur, int nready,
-                                                 const int *__restrict__ task_ptr, const int *__restrict__ ent_flag,
-                                                 const int *__restrict__ ent_data, const int *__restrict__ ent_w, int a0,
-                                                 int count, int ntasks, int nvals, int D,
-                                                 const double *__restrict__ x_in, int nx, const double *pool,
-                                                 double *__restrict__ values, double *__restrict__ jac) {
-    const int LD2 = 2 * L * D;
-    for (int e = threadIdx.x; e < count * D; e += blockDim.x) {
-        const int task = a0 + e / D, k = e - (e / D) * D;
-        if (task >= ntasks) break;
-        double Br[L + 1], Bi[L + 1];
-        md_zero(Br);
-        md_zero(Bi);
-        constexpr int QB = L <= 2 ? 8 : (L <= 5 ? 4 : 2);
-        const int q1 = __ldg(task_ptr + task + 1);
-        for (int qb = __ldg(task_ptr + task); qb < q1; qb += QB) {
-            double ar[QB][L], ai[QB][L];
-            int w[QB], fl[QB];
-            bool need[QB], any = false;
-#pragma unroll
-            for (int u = 0; u < QB; u++) {
-                fl[u] = qb + u < q1 ? __ldg(ent_flag + qb + u) : 0;
-                need[u] = qb + u < q1 && fl[u] >= nready;
-                any |= need[u];
-            }
-            if (any) {
-                queue_wait_all<QB>(flags, fl, need, cur);
-                fence_acquire_gpu();
-            }
-#pragma unroll
-            for (int u = 0; u < QB; u++) {
-                const bool in = qb + u < q1;
-                const int slot = in ? __ldg(ent_data + qb + u) : 0;
-                w[u] = in ? __ldg(ent_w + qb + u) : 0;
-                const double *sp = slot < nx ? x_in + (size_t)slot * LD2 : pool + (size_t)slot * LD2;
-#pragma unroll
-                for (int p = 0; p < L; p++) {
-                    ar[u][p] = in ? __ldcg(sp + p * D + k) : 0.0;
-                    ai[u][p] = in ? __ldcg(sp + (L + p) * D + k) : 0.0;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < QB; u++) {
-                if (w[u] == 1) {
-                    bins_add<L>(Br, ar[u]);
-                    bins_add<L>(Bi, ai[u]);
-                } else if (w[u] != 0) {
-                    bins_add_scaled<L>(Br, ar[u], (double)w[u]);
-                    bins_add_scaled<L>(Bi, ai[u], (double)w[u]);
-                }
-            }
-        }
-        double zr[L], zi[L];
-        md_renorm(Br, zr);
-        md_renorm(Bi, zi);
-        double *o = task < nvals ? values + (size_t)task * LD2 : jac + (size_t)(task - nvals) * LD2;
-#pragma unroll
-        for (int p = 0; p < L; p++) {
-            o[p * D + k] = zr[p];
-            o[(L + p) * D + k] = zi[p];
-        }
-    }
-}
-
 template <int L>
 __global__ void __launch_bounds__(256) queue_eft_kernel(
     const double *__restrict__ x_in,  // [nx][2][L][D]: the evaluation's input series (slots 0..nx-1)
@@ -325,8 +253,66 @@ __global__ void __launch_bounds__(256) queue_eft_kernel(
             // (sums start on the entries that are final), an acquire load
             // after each wait; the loads bypass L1
             if (trace && threadIdx.x == 0) trace[TS * tk + 1] = (long long)globaltimer_ns();
-            queue_add_ticket<L>(flags, cur, nready, task_ptr, ent_slot, ent_slot, ent_w, a0, tasks_per_ticket, ntasks,
-                                nvals, D, x_in, nx, pool, values, jac);
+            for (int e = threadIdx.x; e < tasks_per_ticket * D; e += blockDim.x) {
+                const int task = a0 + e / D, k = e - (e / D) * D;
+                if (task >= ntasks) break;
+                double Br[L + 1], Bi[L + 1];
+                md_zero(Br);
+                md_zero(Bi);
+                // entries in batches of QB: the loads of a batch are in flight
+                // together (a serial load per entry costs an L2 round trip
+                // each), then summed in entry order (the same bins as one by one)
+                constexpr int QB = L <= 2 ? 8 : (L <= 5 ? 4 : 2);
+                const int q1 = __ldg(task_ptr + task + 1);
+                for (int qb = __ldg(task_ptr + task); qb < q1; qb += QB) {
+                    double ar[QB][L], ai[QB][L];
+                    int w[QB];
+                    int slots[QB];
+#pragma unroll
+                    for (int u = 0; u < QB; u++) slots[u] = qb + u < q1 ? __ldg(ent_slot + qb + u) : 0;
+                    bool need[QB], any = false;
+#pragma unroll
+                    for (int u = 0; u < QB; u++) {
+                        need[u] = qb + u < q1 && slots[u] >= nready;
+                        any |= need[u];
+                    }
+                    if (any) {
+                        queue_wait_all<QB>(flags, slots, need, cur);
+                        fence_acquire_gpu();
+                    }
+#pragma unroll
+                    for (int u = 0; u < QB; u++) {
+                        const bool in = qb + u < q1;
+                        const int slot = slots[u];
+                        w[u] = in ? __ldg(ent_w + qb + u) : 0;
+                        const double *sp = series(slot);
+#pragma unroll
+                        for (int p = 0; p < L; p++) {
+                            ar[u][p] = in ? __ldcg(sp + p * D + k) : 0.0;
+                            ai[u][p] = in ? __ldcg(sp + (L + p) * D + k) : 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < QB; u++) {
+                        if (w[u] == 1) {
+                            bins_add<L>(Br, ar[u]);
+                            bins_add<L>(Bi, ai[u]);
+                        } else if (w[u] != 0) {
+                            bins_add_scaled<L>(Br, ar[u], (double)w[u]);
+                            bins_add_scaled<L>(Bi, ai[u], (double)w[u]);
+                        }
+                    }
+                }
+                double zr[L], zi[L];
+                md_renorm(Br, zr);
+                md_renorm(Bi, zi);
+                double *o = task < nvals ? values + (size_t)task * LD2 : jac + (size_t)(task - nvals) * LD2;
+#pragma unroll
+                for (int p = 0; p < L; p++) {
+                    o[p * D + k] = zr[p];
+                    o[(L + p) * D + k] = zi[p];
+                }
+            }
             if (trace) {
                 __syncthreads();
                 if (threadIdx.x == 0) trace[TS * tk + 4] = (long long)globaltimer_ns();
