@@ -42,6 +42,24 @@ CONFIG_TEXT = {
 METRIC = "series products/s (mdps_eval_diff)"
 TOL = {2: 1e-29, 3: 1e-45, 4: 1e-61, 5: 1e-77, 8: 1e-124, 10: 1e-156}
 
+# PAPER.md:109-147 (Table 1): hardware double operations per md add and per
+# md mul (the +, -, * columns summed; no division on this path)
+TABLE1_ADD = {2: 8 + 12, 3: 13 + 22, 4: 35 + 54, 5: 44 + 78, 8: 95 + 174, 10: 139 + 258}
+TABLE1_MUL = {2: 5 + 9 + 9, 3: 83 + 84 + 42, 4: 99 + 164 + 73, 5: 162 + 283 + 109, 8: 529 + 954 + 259,
+              10: 952 + 1743 + 394}
+
+
+def table1_ops_per_product(D: int, L: int) -> int:
+    """The paper's cost of one truncated complex series product in hardware
+    double operations: D(D+1)/2 complex md multiplications (4 md mul + 2 md
+    add each, DESIGN R5) and D(D-1)/2 complex md additions (2 md add each),
+    PAPER.md:233-239, priced with Table 1.  A reported
+    context figure ("paper-equivalent" FP64 ops), not the kernel's own
+    instruction count: the digit kernel does far fewer."""
+    cmul = D * (D + 1) // 2
+    cadd = D * (D - 1) // 2
+    return cmul * (4 * TABLE1_MUL[L] + 2 * TABLE1_ADD[L]) + cadd * 2 * TABLE1_ADD[L]
+
 
 def load_peaks():
     try:
@@ -520,6 +538,12 @@ def main():
                          "workspace_bytes": st["workspace_bytes"], "pool_bytes": st["pool_bytes"]},
             "fp64_ops_per_s": fp64_per_s,
             "fp64_ops_per_step": st["fp64_ops_total"],
+            "paper_equivalent": {
+                "table1_fp64_ops_per_product": table1_ops_per_product(si.D, si.limbs),
+                "table1_fp64_ops_per_s": value * table1_ops_per_product(si.D, si.limbs),
+                "kernel_fp64_instr_per_product": st["fp64_ops_conv"] / max(1, products_per_step),
+                "source": "PAPER.md:109-147 Table 1 (md add/mul in hardware double ops) x the product's "
+                          "D(D+1)/2 complex md mul + D(D-1)/2 complex md add (PAPER.md:233-239); context only"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -57,3 +57,22 @@ def test_gpu_arm_line():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     n = d["next_rows"]
     assert n["toeplitz_solve"]["ms"] > 0 and n["newton_step"]["ms"] > 0
+
+
+def test_table1_equivalent_ops():
+    """The paper-equivalent op count of one series product (PAPER.md:109-147
+    Table 1 x the 2D(D+1) md mul + 2D^2 md add of SURVEY §8(a) a7) against
+    SURVEY §8(a)'s per-config figures and BASELINE.md's totals."""
+    # SURVEY §8(a) a7: Table-1 ops per product dd 22,752; qd 891,904; od 16.70 M; deca 28.95 M
+    assert bench.table1_ops_per_product(16, 2) == 22752
+    assert bench.table1_ops_per_product(32, 4) == 891904
+    assert round(bench.table1_ops_per_product(64, 8) / 1e6, 2) == 16.70
+    assert round(bench.table1_ops_per_product(64, 10) / 1e6, 2) == 28.95
+    # BASELINE.md: md add / mul totals per limb count (dd 20 / 23 ... deca 397 / 3,089)
+    assert [bench.TABLE1_ADD[L] for L in (2, 3, 4, 5, 8, 10)] == [20, 35, 89, 122, 269, 397]
+    assert [bench.TABLE1_MUL[L] for L in (2, 3, 4, 5, 8, 10)] == [23, 209, 336, 554, 1742, 3089]
+    # 2D(D+1) real md mul + 2D^2 real md add (SURVEY §8(a) a7), any D
+    for D in (1, 9, 33, 128):
+        for L in (2, 3, 4, 5, 8, 10):
+            assert bench.table1_ops_per_product(D, L) == 2 * D * (D + 1) * bench.TABLE1_MUL[L] + \
+                2 * D * D * bench.TABLE1_ADD[L]
