@@ -116,7 +116,7 @@ def lib() -> ctypes.CDLL:
     L.mdps_test_norm2sq.argtypes = [vp, i32, i32, vp, vp]
     L.mdps_test_digits_roundtrip.argtypes = [vp, vp, i32, i32, i32, vp]
     L.mdps_fp64_peak.argtypes = [i64, P(ctypes.c_double), vp]
-    L.mdps_test_force_geometry.argtypes = [i32, i32]
+    L.mdps_test_force_geometry.argtypes = [i32, i32, i32]
     L.mdps_system_set_timing.argtypes = [vp, i32]
     L.mdps_system_timing.argtypes = [vp, P(Timing), i32]
     L.mdps_solver_create.restype = vp
@@ -493,9 +493,9 @@ def queue_config(max_blocks: int = 0, lanes: int = 0) -> None:
     _check(lib().mdps_test_queue_config(max_blocks, lanes), "mdps_test_queue_config")
 
 
-def force_geometry(F: int = 0, P: int = 0) -> None:
-    """Tuning only: force the digit product kernel's (F, P); 0, 0 = the model."""
-    _check(lib().mdps_test_force_geometry(F, P), "mdps_test_force_geometry")
+def force_geometry(F: int = 0, P: int = 0, NP: int = 0) -> None:
+    """Tuning only: force the digit product kernel's (F, P, NP); 0, 0, 0 = the default."""
+    _check(lib().mdps_test_force_geometry(F, P, NP), "mdps_test_force_geometry")
 
 
 def fp64_peak(iters: int = 20000, stream=None) -> float:

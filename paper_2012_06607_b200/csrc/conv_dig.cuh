@@ -2,11 +2,15 @@
 // z = x * y mod t^D for every job of one DAG level.
 //
 // See kernels_dig.cuh for the digit representation.  Mapping:
-//  * P jobs per block; per job T = ceil(D/2) output pairs x F splits.  Thread
-//    (t, f) owns outputs k1 = t and k2 = D-1-t — the folded triangle has
-//    exactly D+1 terms per pair, so no lane idles — and the fold iterations
-//    j = f, f+F, ... (the F lanes of a pair are adjacent lanes of one warp).
-//  * Two passes (real part, imaginary part): each keeps S digit accumulators
+//  * P jobs per block; per job T = ceil(D/2) output pairs x F splits x NP
+//    part lanes.  Thread (part lane, t, f) owns outputs k1 = t and k2 = D-1-t
+//    — the folded triangle has exactly D+1 terms per pair, so no lane idles —
+//    and the fold iterations j = f, f+F, ... (the F lanes of a pair are
+//    adjacent lanes of one warp).
+//  * Two passes (real part, imaginary part), one after the other on the same
+//    thread (NP = 1) or one per part lane (NP = 2: twice the threads per job,
+//    half its latency, no extra reduction — the parts are separate outputs;
+//    for small levels and short bodies).  Each pass keeps S digit accumulators
 //    and the 2S digits of the operand x_i in registers and streams the 2S
 //    digits of y_{k-i} from shared memory: per digit pair one DFMA.
 //  * Alignment: a term whose exponent is delta digits below the accumulator
@@ -15,9 +19,11 @@
 //    checked warp-uniformly) every load is base + compile-time offset; larger
 //    shifts take a select-based path.  A term with a zero operand part is
 //    read at delta = 0 (its product is zero anyway).
-//  * Partials: the k1 partial is parked in shared memory when a lane crosses
-//    the fold (lanes cross at different iterations); the k2 partials are
-//    added with warp shuffles.  All additions are exact (integer digits).
+//  * Partials: a copy of the k1 partial is parked in shared memory when a
+//    lane crosses the fold (lanes cross at different iterations) and the k2
+//    terms go on top of it; k2 = A - park after the loop.  The F lanes'
+//    partials are added with warp shuffles.  All additions are exact
+//    (integer digits).
 //  * Shared memory per job: x planes [2][S][D] (the pool's own layout, one
 //    TMA bulk copy), y planes [2][PADZ+S][D] (PADZ zero planes in front of
 //    each part, one bulk copy per part), exponents [2][2][D]; per thread a
@@ -123,18 +129,21 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     // per digit row, inside the body) rather than to the S held x digits
     auto neg = [&](double w) { return __longlong_as_double(__double_as_longlong(w) ^ sgn); };
     for (int j = f; j <= D; j += F) {
-        if (j > t && !switched) {  // k1 partial complete: park it (raw), start k2
-            // no carry here: lanes of a warp cross the fold at different
-            // iterations, so anything done here runs divergently.  The raw
-            // partial is below 2^53 (< NORM terms since the last carry) and
-            // is carried after the loop, by all lanes at once.  cnt is not
-            // reset, so the periodic carries stay warp-uniform too.
+        // k1 partial complete: park a copy (raw) and keep accumulating — the
+        // k2 terms go on top of it, and k2 = A - park after the loop (exact:
+        // integer digits).  Not zeroing A keeps the in-loop work at S/2
+        // stores, which the compiler predicates onto every term (a lane
+        // crosses the fold once, at a lane-dependent iteration); zeroing
+        // cost S more predicated moves per term (measured at qd: the park
+        // was ~14% of the kernel's instructions).  No carry here: anything
+        // done at the crossing runs divergently.  The raw partial is below
+        // 2^53 (< NORM terms since the last carry) and is carried after the
+        // loop, by all lanes at once; cnt is not reset, so the periodic
+        // carries of A stay warp-uniform.
+        if (j > t && !switched) {
             switched = true;
 #pragma unroll
-            for (int s = 0; s < S; s++) {
-                park[s] = A[s];
-                A[s] = 0.0;
-            }
+            for (int s = 0; s < S; s++) park[s] = A[s];
         }
         // the next term (this term again on the last iteration: harmless)
         const int jn = j + F <= D ? j + F : j;
@@ -194,11 +203,10 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     carry_pass(A);
     if (!switched) {  // no k2 iterations on this lane: everything belongs to k1
 #pragma unroll
-        for (int s = 0; s < S; s++) {
-            park[s] = A[s];
-            A[s] = 0.0;
-        }
+        for (int s = 0; s < S; s++) park[s] = A[s];
     }
+    // on return: park = the k1 partial (|digit| < 2^53), A = the k1 + k2
+    // partials (carried, |digit| <= R/2 + 2^31)
 }
 
 template <int L>
@@ -264,13 +272,13 @@ template <int L, int DT, bool REAL = false>
 // part is computed; the imaginary limbs of the limb outputs are written as 0.
 __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
                                   DT == 128 || DT == 0 ? 1 : (L <= 4 ? 4 : (L <= 8 ? 3 : 2)))
-    conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool,
-                                                      double *__restrict__ lpool, const int *__restrict__ jobs, int njobs, int Drt, int T,
-                                                      int F, int P) {
+    conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool, double *__restrict__ lpool,
+                    const int *__restrict__ jobs, int njobs, int Drt, int T, int F, int P, int NPrt) {
     constexpr int S = digits_for(L);
     const int D = DT > 0 ? DT : Drt;
     const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
-    const int threads_per_job = T * F;
+    const int NP = REAL ? 1 : NPrt;  // part lanes per output pair (1 or 2)
+    const int threads_per_job = T * F * NP;
     extern __shared__ __align__(16) double sm[];
     double *sdig = sm;                                        // [P][SX + SY]
     double *spark = sm + (size_t)P * (SX + SY);               // [threads][S]
@@ -340,7 +348,9 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
     __syncthreads();
 
     const int jl = threadIdx.x / threads_per_job;
-    const int r = threadIdx.x - jl * threads_per_job;
+    const int r0 = threadIdx.x - jl * threads_per_job;
+    const int pl = NP == 2 ? r0 / (T * F) : 0;  // part lane (NP = 2: this thread's part)
+    const int r = r0 - pl * T * F;
     const int t = r / F, f = r - t * F;
     const int jlc = min(jl, P - 1);  // padding lanes (blockDim rounded to whole warps) shadow the last job
     const double *sx = sdig + (size_t)jlc * (SX + SY), *sy = sx + SX;
@@ -398,21 +408,25 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
             }
     }
 #pragma unroll 1
-    for (int part = 0; part < (REAL ? 1 : 2); part++) {
+    for (int part = pl; part < (REAL ? 1 : (NP == 2 ? pl + 1 : 2)); part++) {
         double A[S];
         const int e1 = part ? ea1i : ea1r, e2 = part ? ea2i : ea2r;
         conv_dig_pass<L, DT, REAL>(sx, sy, ex, ey, D, part, t, f, F, e1, e2, A, park);
+        // k1: every lane carries its parked (raw) partial — warp-uniform work,
+        // no lane sums alone — and takes it off A, which leaves the k2 partial
+        // (|digit| <= R + 2^32: exact)
+        double B[S];
+#pragma unroll
+        for (int s = 0; s < S; s++) B[s] = park[s];
+        carry_pass(B);
+#pragma unroll
+        for (int s = 0; s < S; s++) A[s] = __dsub_rn(A[s], B[s]);
         // k2: sum the F lanes' partials (exact) with shuffles; every lane has it
         for (int off = F >> 1; off > 0; off >>= 1) {
 #pragma unroll
             for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
         }
-        // k1: every lane carries its parked (raw) partial, then the same
-        // shuffle reduction — warp-uniform work, no lane sums alone
-        double B[S];
-#pragma unroll
-        for (int s = 0; s < S; s++) B[s] = park[s];
-        carry_pass(B);
+        // k1: the same shuffle reduction
         for (int off = F >> 1; off > 0; off >>= 1) {
 #pragma unroll
             for (int s = 0; s < S; s++) B[s] = __dadd_rn(B[s], __shfl_xor_sync(0xffffffffu, B[s], off));

@@ -13,6 +13,14 @@ import mdinputs  # noqa: E402
 import paper_2012_06607_b200 as mdps  # noqa: E402
 
 
+def digits_for(L):
+    """digits per part of the digit algorithm (kernels_dig.cuh digits_for)"""
+    S = 2
+    while (S - 2) * 23 < 53 * L + 8:
+        S += 1
+    return S
+
+
 def measure(si, algo=0, steps=5, warmup=3):
     s = mdps.System.from_inputs(si, algo=algo)
     st = s.stats()
@@ -43,7 +51,11 @@ def measure(si, algo=0, steps=5, warmup=3):
             "products_per_s": st["products"] * steps / (ms * 1e-3),
             "fp64_instr_per_s": st["fp64_ops_total"] * steps / (ms * 1e-3),
             "conv_ms": tim["conv_ms"] / steps, "accum_ms": tim["accum_ms"] / steps,
-            "conv_frac_of_fp64_peak": ach / peak, "launches": st["launches"]}
+            "conv_frac_of_fp64_peak": ach / peak, "launches": st["launches"],
+            # one work count for every cell, whatever algorithm ran: the digit
+            # method's D(D+1) S(S+1) DFMAs per complex product
+            "frac_on_digit_count": st["products"] * si.D * (si.D + 1) * digits_for(si.limbs) *
+            (digits_for(si.limbs) + 1) * steps / (tim["conv_ms"] * 1e-3) / peak}
 
 
 if __name__ == "__main__":

@@ -1,4 +1,4 @@
-"""Product-kernel launch geometry per (L, D): time every (F, P) that fits on
+"""Product-kernel launch geometry per (L, D): time every (F, P, NP) that fits on
 the sweep cells and the configs, in one process per cell list
 (mdps_test_force_geometry), and print the measured best next to the model's
 choice.  Digits algorithm, complex systems; CUDA events around the product
@@ -15,7 +15,8 @@ import paper_2012_06607_b200 as mdps  # noqa: E402
 
 CELLS = sys.argv[1].split(",") if len(sys.argv) > 1 else (
     ["qd", "od", "deca"] + [f"sweep_d{d}_L{L}" for d in (15, 31, 63, 127) for L in (2, 3, 4, 5, 8, 10)])
-GEOMS = [(0, 0)] + [(f, p) for f in (1, 2, 4, 8) for p in (1, 2, 4, 8)]
+NPS = (1,) if os.environ.get("TUNE_REAL") == "1" else (1, 2)
+GEOMS = [(0, 0, 0)] + [(f, p, q) for q in NPS for f in (1, 2, 4, 8) for p in (1, 2, 4, 8)]
 
 
 def workload(c):
@@ -51,16 +52,16 @@ for c in CELLS:
         j = torch.empty((si.n, si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
         reps = 3 if si.limbs * si.D <= 64 * 8 else 2
         res = {}
-        for f, p in GEOMS:
+        for f, p, q in GEOMS:
             try:
-                mdps.force_geometry(f, p)
-                res[f"{f},{p}"] = conv_ms(s, x, v, j, flush, reps)
+                mdps.force_geometry(f, p, q)
+                res[f"{f},{p},{q}"] = conv_ms(s, x, v, j, flush, reps)
             except Exception:
                 pass
-        mdps.force_geometry(0, 0)
-    best = min((k for k in res if k != "0,0"), key=lambda k: res[k])
-    row = {"cell": c, "real": REAL, "L": si.limbs, "D": si.D, "model_ms": res.get("0,0"), "best": best, "best_ms": res[best],
-           "gain": res.get("0,0", 0) / res[best], "all": res}
+        mdps.force_geometry(0, 0, 0)
+    best = min((k for k in res if k != "0,0,0"), key=lambda k: res[k])
+    row = {"cell": c, "real": REAL, "L": si.limbs, "D": si.D, "default_ms": res.get("0,0,0"), "best": best,
+           "best_ms": res[best], "gain": res.get("0,0,0", 0) / res[best], "all": res}
     out.append(row)
     print(json.dumps(row), flush=True)
 json.dump(out, open(os.environ.get("TUNE_OUT", "gpurun_out/tune_table.json"), "w"), indent=1)

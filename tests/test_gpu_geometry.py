@@ -1,8 +1,10 @@
 """The digit product kernel under every launch geometry that fits
-(mdps_test_force_geometry: F lanes per output pair x P jobs per block),
+(mdps_test_force_geometry: F lanes per output pair x P jobs per block x NP
+part lanes),
 including F > D + 1 (lanes without terms), odd D (the generic-D build, scalar
 staging) and several jobs per block: every geometry matches the oracle within
-the tolerance, and the tuned defaults are among them."""
+the tolerance, the tuned defaults are among them, and NP = 2 gives bitwise the
+outputs of NP = 1 at the same (F, P)."""
 import numpy as np
 import pytest
 
@@ -12,7 +14,7 @@ from tests.gpu_util import TOL
 
 pytestmark = pytest.mark.gpu
 
-GEOMS = [(f, p) for f in (1, 2, 4, 8) for p in (1, 2, 4)]
+GEOMS = [(f, p, q) for q in (1, 2) for f in (1, 2, 4, 8) for p in (1, 2, 4)]
 
 
 @pytest.mark.parametrize("L,degree", [(2, 6), (4, 15), (8, 31), (10, 15), (3, 63)])
@@ -23,20 +25,26 @@ def test_every_fitting_geometry_matches_the_oracle(L, degree):
                                 limbs=L)
     ov, oj, _ = oracle.eval_diff(si)
     ran = 0
+    seen = {}
     try:
         with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS) as s:
             x = torch.from_numpy(si.x).cuda()
-            for f, p in GEOMS:
-                mdps.force_geometry(f, p)
+            for f, p, q in GEOMS:
+                mdps.force_geometry(f, p, q)
                 try:
                     v, j = s.eval_diff(x)
                 except mdps.MdpsError:
                     continue  # does not fit this kernel's thread / shared-memory limits
                 torch.cuda.synchronize()
                 v, j = v.cpu().numpy(), j.cpu().numpy()
-                assert oracle.series_err(v, ov).max() <= TOL[L], (f, p)
-                assert oracle.series_err(j, oj).max() <= TOL[L], (f, p)
+                assert oracle.series_err(v, ov).max() <= TOL[L], (f, p, q)
+                assert oracle.series_err(j, oj).max() <= TOL[L], (f, p, q)
+                # one thread per part (NP = 2) runs the same per-part sums as
+                # both passes on one thread: bitwise the same outputs
+                if (f, p) in seen:
+                    assert np.array_equal(v, seen[(f, p)][0]) and np.array_equal(j, seen[(f, p)][1]), (f, p, q)
+                seen[(f, p)] = (v, j)
                 ran += 1
     finally:
-        mdps.force_geometry(0, 0)
-    assert ran >= 4
+        mdps.force_geometry(0, 0, 0)
+    assert ran >= 8
