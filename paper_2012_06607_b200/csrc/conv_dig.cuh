@@ -91,7 +91,6 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     const int w1part = part, w2part = 1 - part;
     const long long sgn = part == 0 ? (long long)0x8000000000000000ULL : 0LL;
     md_zero(A);
-    int cnt = 0;
     bool switched = false;
     // Software pipeline, one term ahead.  Everything the next term needs
     // (its x digits, its y offset kk and its alignment shifts d1, d2, read
@@ -100,11 +99,16 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     // after digit row l the operand digit u = S-1-l has had its last use, so
     // its register takes the next term's digit u (no extra registers).  The
     // per-term preamble shrinks to the warp vote on the fast path.
-    auto term_index = [&](int j) { return j <= t ? j : j - t - 1; };
+    // fold iteration j -> term (i, kk = k - i): j <= t is term i = j of k1 = t,
+    // j > t is term i = D - j of k2 = D-1-t (descending), so the x index is
+    // j or D - j — the same for every pair of the warp at a given j (a
+    // shared-memory broadcast) — and kk = t - j or j - t - 1 is consecutive
+    // over the warp's pairs (one contiguous window), for both outputs
+    auto term_index = [&](int j) { return j <= t ? j : D - j; };
     auto term_meta = [&](int j, int &kk, int &d1, int &d2) {
         const bool first = j <= t;
         const int i = term_index(j);
-        kk = (first ? t : D - 1 - t) - i;
+        kk = first ? t - j : j - t - 1;
         const int eacc = first ? eacc1 : eacc2;
         const int exr = ex[i], exi = REAL ? ZERO_E : ex[D + i];
         const int ey1 = ey[w1part * D + kk], ey2 = REAL ? 0 : ey[w2part * D + kk];
@@ -128,7 +132,13 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     // part 0's sign (-Ui*Wi) is applied to the streamed y digit w2 (one flip
     // per digit row, inside the body) rather than to the S held x digits
     auto neg = [&](double w) { return __longlong_as_double(__double_as_longlong(w) ^ sgn); };
-    for (int j = f; j <= D; j += F) {
+    // blocks of at most NORM terms, each closed by a carry pass: one loop
+    // test per term (no per-term counter test and branch), and the carries
+    // stay warp-uniform (every lane's block ends at the same iteration count
+    // but for a shorter last one)
+    for (int j = f; j <= D;) {
+    const int jstop = min(D, j + (NORM - 1) * F);
+    for (; j <= jstop; j += F) {
         // k1 partial complete: park a copy (raw) and keep accumulating — the
         // k2 terms go on top of it, and k2 = A - park after the loop (exact:
         // integer digits).  Not zeroing A keeps the in-loop work at S/2
@@ -138,8 +148,7 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
         // was ~14% of the kernel's instructions).  No carry here: anything
         // done at the crossing runs divergently.  The raw partial is below
         // 2^53 (< NORM terms since the last carry) and is carried after the
-        // loop, by all lanes at once; cnt is not reset, so the periodic
-        // carries of A stay warp-uniform.
+        // loop, by all lanes at once; the block carries of A go on.
         if (j > t && !switched) {
             switched = true;
 #pragma unroll
@@ -195,12 +204,9 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
         kk = kkn;
         d1 = d1n;
         d2 = d2n;
-        if (++cnt == NORM) {
-            carry_pass(A);
-            cnt = 0;
-        }
     }
     carry_pass(A);
+    }
     if (!switched) {  // no k2 iterations on this lane: everything belongs to k1
 #pragma unroll
         for (int s = 0; s < S; s++) park[s] = A[s];
@@ -359,18 +365,32 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
     // exponent pre-pass (split over the F lanes, max-reduced by shuffles):
     // anchors e_acc of (k1, k2) x (re, im) over ALL terms of each output
     int ea1r = ZERO_E, ea1i = ZERO_E, ea2r = ZERO_E, ea2i = ZERO_E;
-    for (int j = f; j <= D; j += F) {
-        const bool first = j <= t;
-        const int i = first ? j : j - t - 1;
-        const int kk = (first ? t : D - 1 - t) - i;
-        const int xr = ex[i], xi = REAL ? ZERO_E : ex[D + i], yr = ey[kk], yi = REAL ? ZERO_E : ey[D + kk];
-        const int er = max(xr + yr, xi + yi), ei = max(xr + yi, xi + yr);
-        if (first) {
-            ea1r = max(ea1r, er);
-            ea1i = max(ea1i, ei);
-        } else {
-            ea2r = max(ea2r, er);
-            ea2i = max(ea2i, ei);
+    if (NP == 2) {  // one part per thread: only its own anchors
+        const int *ey1 = ey + pl * D, *ey2 = ey + (1 - pl) * D;
+        for (int j = f; j <= D; j += F) {
+            const bool first = j <= t;
+            const int i = first ? j : D - j;  // the pass's term order (conv_dig_pass)
+            const int kk = first ? t - j : j - t - 1;
+            const int e = max(ex[i] + ey1[kk], ex[D + i] + ey2[kk]);
+            if (first) ea1r = max(ea1r, e);
+            else ea2r = max(ea2r, e);
+        }
+        ea1i = ea1r;
+        ea2i = ea2r;
+    } else {
+        for (int j = f; j <= D; j += F) {
+            const bool first = j <= t;
+            const int i = first ? j : D - j;  // the pass's term order (conv_dig_pass)
+            const int kk = first ? t - j : j - t - 1;
+            const int xr = ex[i], xi = REAL ? ZERO_E : ex[D + i], yr = ey[kk], yi = REAL ? ZERO_E : ey[D + kk];
+            const int er = max(xr + yr, xi + yi), ei = max(xr + yi, xi + yr);
+            if (first) {
+                ea1r = max(ea1r, er);
+                ea1i = max(ea1i, ei);
+            } else {
+                ea2r = max(ea2r, er);
+                ea2i = max(ea2i, ei);
+            }
         }
     }
     for (int off = F >> 1; off > 0; off >>= 1) {

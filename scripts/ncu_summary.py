@@ -20,13 +20,19 @@ KEYS = {
     "smsp__sass_thread_inst_executed_op_dadd_pred_on.sum": "dadd_thread_inst",
     "smsp__sass_thread_inst_executed_op_dmul_pred_on.sum": "dmul_thread_inst",
     "smsp__sass_inst_executed_op_shared_ld.sum": "lds_inst",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_wavefronts_pct",
+    "smsp__sass_inst_executed_op_dfma.sum": "dfma_warp_inst",
     "launch__grid_size": "grid",
     "launch__block_size": "block",
 }
 
 
 def summarise(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    """path: an .ncu-rep (read with ncu -i) or its raw page already exported as CSV"""
+    if path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
