@@ -60,9 +60,8 @@ typedef struct {
 } mdps_supports;
 
 /* Convolution algorithm for the product jobs. */
-#define MDPS_ALGO_AUTO 0     /* default: digits, except EFT above degree 127, for limbs = 2 and,
-                                on systems of >= 4096 product jobs, for limbs = 3 up to degree
-                                31 (faster there, measured) */
+#define MDPS_ALGO_AUTO 0     /* default: digits, except EFT above degree 127 and for limbs = 2
+                                (faster there, measured) */
 #define MDPS_ALGO_EFT 1      /* limb planes: TwoProd + TwoSum level bins */
 #define MDPS_ALGO_DIGITS 2   /* 23-bit digit planes, exact FP64 FMA products */
 

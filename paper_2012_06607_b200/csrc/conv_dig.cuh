@@ -1,33 +1,41 @@
 // conv_dig.cuh — the product-job kernel on digit planes (MDPS_ALGO_DIGITS):
 // z = x * y mod t^D for every job of one DAG level.
 //
-// See kernels_dig.cuh for the digit representation.  Mapping:
-//  * P jobs per block; per job T = ceil(D/2) output pairs x F splits x NP
-//    part lanes.  Thread (part lane, t, f) owns outputs k1 = t and k2 = D-1-t
-//    — the folded triangle has exactly D+1 terms per pair, so no lane idles —
-//    and the fold iterations j = f, f+F, ... (the F lanes of a pair are
-//    adjacent lanes of one warp).
-//  * Two passes (real part, imaginary part), one after the other on the same
-//    thread (NP = 1) or one per part lane (NP = 2: twice the threads per job,
-//    half its latency, no extra reduction — the parts are separate outputs;
-//    for small levels and short bodies).  Each pass keeps S digit accumulators
-//    and the 2S digits of the operand x_i in registers and streams the 2S
-//    digits of y_{k-i} from shared memory: per digit pair one DFMA.
-//  * Alignment: a term whose exponent is delta digits below the accumulator
-//    anchor reads y's digit plane l - delta.  Shared memory holds PADZ zero
-//    planes in front of y's planes, so for delta <= PADZ (the common case,
-//    checked warp-uniformly) every load is base + compile-time offset; larger
-//    shifts take a select-based path.  A term with a zero operand part is
-//    read at delta = 0 (its product is zero anyway).
+// See kernels_dig.cuh for the digit representation (pool slot: digits
+// [S][D][2] — digit, coefficient, part — and one exponent per complex
+// coefficient, both parts on one grid).  Mapping:
+//  * P jobs per block; per job T = ceil(D/2) output pairs x F splits, and
+//    per part one lane set (NP = 2 part lanes for complex systems, one for
+//    real ones).  The block's threads are [part][job][pair t][lane f] with
+//    each part's set padded to whole warps, so a warp computes ONE part and
+//    runs that part's code copy (no per-row selects or sign flips).  Thread
+//    (part, t, f) owns outputs k1 = t and k2 = D-1-t — the folded triangle
+//    has exactly D+1 terms per pair, so no lane idles — and the fold
+//    iterations j = f, f+F, ... (the F lanes of a pair are adjacent lanes).
+//  * Per term x_i y_{k-i} the S (re, im) digit pairs of x_i are held in
+//    registers (one 16-byte load each) and y's digit rows stream from shared
+//    memory, one 16-byte (re, im) pair per row feeding both real products of
+//    the part: re += xr yr - xi yi, im += xr yi + xi yr.  Per digit pair one
+//    DFMA (exact: integer digits).
+//  * Alignment: a term whose exponent (one per complex coefficient) is delta
+//    digits below the accumulator anchor reads y's digit row l - delta.
+//    Shared memory holds PADZ zero rows in front of y's rows, so for delta
+//    <= PADZ (the common case, checked warp-uniformly) every load is base +
+//    compile-time offset; larger shifts take a select-based path.  A term
+//    with a zero operand is read at delta = 0 (its product is zero anyway).
 //  * Partials: a copy of the k1 partial is parked in shared memory when a
 //    lane crosses the fold (lanes cross at different iterations) and the k2
 //    terms go on top of it; k2 = A - park after the loop.  The F lanes'
 //    partials are added with warp shuffles.  All additions are exact
 //    (integer digits).
-//  * Shared memory per job: x planes [2][S][D] (the pool's own layout, one
-//    TMA bulk copy), y planes [2][PADZ+S][D] (PADZ zero planes in front of
-//    each part, one bulk copy per part), exponents [2][2][D]; per thread a
-//    parking slot of S doubles.
+//  * Output digits: the two parts of a coefficient share the exponent of
+//    the larger: each part lane finds its leading digit, the part lanes
+//    exchange it through shared memory (one block barrier), and both store
+//    on the common grid.
+//  * Shared memory per job: x [S][D][2] (the pool's own layout, one TMA bulk
+//    copy), y [PADZ + S][D][2] (PADZ zero rows in front, one bulk copy),
+//    exponents [2][D]; per thread a parking slot of S + 2 doubles; the
+//    leading-digit exchange [2][P][D][2] ints.
 #pragma once
 #include "kernels_dig.cuh"
 
@@ -38,7 +46,7 @@ constexpr int PADZ = 4;
 __host__ __device__ inline size_t conv_dig_smem(int S, int D, int P, int threads) {
     const size_t per_job = (size_t)2 * S * D + (size_t)2 * (PADZ + S) * D;  // doubles
     return (size_t)P * per_job * sizeof(double) + (size_t)threads * (S + 2) * sizeof(double) +
-           (size_t)P * 4 * D * sizeof(int) + 16;  // + mbarrier
+           (size_t)P * 2 * D * sizeof(int) + (size_t)2 * P * D * 2 * sizeof(int) + 16;  // + mbarrier
 }
 
 // ---- TMA bulk copies (cp.async.bulk) with an mbarrier, single CTA ----------
@@ -74,30 +82,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
         : "memory");
 }
 
-// one product pass over this thread's fold iterations.  REAL: real series
-// (imaginary parts zero and never read): one product per term.
-template <int L, int DT, bool REAL = false>
+// one product pass over this thread's fold iterations for part PART (0: re,
+// 1: im).  REAL: real series (imaginary digits zero and never read): one
+// product per term.
+template <int L, int DT, int PART, bool REAL = false>
 __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, const double *__restrict__ sy,
                                               const int *__restrict__ ex, const int *__restrict__ ey, int Drt,
-                                              int part, int t, int f, int F, int eacc1, int eacc2,
-                                              double (&A)[digits_for(L)], double *park) {
+                                              int t, int f, int F, int eacc1, int eacc2, double (&A)[digits_for(L)],
+                                              double *park) {
     constexpr int S = digits_for(L);
     constexpr int NORM = norm_every(S);
     const int D = DT > 0 ? DT : Drt;
-    constexpr int P2 = PADZ + S;
-    // part 0 (re): Ur*Wr - Ui*Wi ;  part 1 (im): Ur*Wi + Ui*Wr.  One code
-    // copy serves both passes (instruction-cache footprint): the part only
-    // selects the y planes and the sign applied to Wi (a sign-bit flip).
-    const int w1part = part, w2part = 1 - part;
-    const long long sgn = part == 0 ? (long long)0x8000000000000000ULL : 0LL;
+    const int D2 = 2 * D;  // doubles per digit row
     md_zero(A);
     bool switched = false;
     // Software pipeline, one term ahead.  Everything the next term needs
-    // (its x digits, its y offset kk and its alignment shifts d1, d2, read
-    // from the exponents) is prepared INSIDE the current term's body, where
-    // the integer work and the shared-memory latency hide behind the DFMAs:
+    // (its x digits, its y offset kk and its alignment shift d, read from
+    // the exponents) is prepared INSIDE the current term's body, where the
+    // integer work and the shared-memory latency hide behind the DFMAs:
     // after digit row l the operand digit u = S-1-l has had its last use, so
-    // its register takes the next term's digit u (no extra registers).  The
+    // its registers take the next term's digit u (no extra registers).  The
     // per-term preamble shrinks to the warp vote on the fast path.
     // fold iteration j -> term (i, kk = k - i): j <= t is term i = j of k1 = t,
     // j > t is term i = D - j of k2 = D-1-t (descending), so the x index is
@@ -105,33 +109,46 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     // shared-memory broadcast) — and kk = t - j or j - t - 1 is consecutive
     // over the warp's pairs (one contiguous window), for both outputs
     auto term_index = [&](int j) { return j <= t ? j : D - j; };
-    auto term_meta = [&](int j, int &kk, int &d1, int &d2) {
+    auto term_meta = [&](int j, int &kk, int &d) {
         const bool first = j <= t;
         const int i = term_index(j);
         kk = first ? t - j : j - t - 1;
-        const int eacc = first ? eacc1 : eacc2;
-        const int exr = ex[i], exi = REAL ? ZERO_E : ex[D + i];
-        const int ey1 = ey[w1part * D + kk], ey2 = REAL ? 0 : ey[w2part * D + kk];
-        d1 = eacc - exr - ey1;
-        d2 = eacc - exi - ey2;
-        if (exr + ey1 <= ZERO_E / 2) d1 = 0;  // zero product: any plane will do
-        if (REAL || exi + ey2 <= ZERO_E / 2) d2 = 0;
+        const int e = ex[i] + ey[kk];
+        d = e <= ZERO_E / 2 ? 0 : (first ? eacc1 : eacc2) - e;  // zero product: any row will do
     };
     double Ur[S], Ui[S];
-    int kk, d1, d2;
+    auto load_x = [&](const double *ux, int u) {
+        if (REAL) {
+            Ur[u] = ux[u * D2];
+        } else {
+            const double2 v = *reinterpret_cast<const double2 *>(ux + u * D2);
+            Ur[u] = v.x;
+            Ui[u] = v.y;
+        }
+    };
+    int kk, d;
     {
         const int j0 = min(f, D);  // a lane with f > D has no terms (clamped reads only)
-        term_meta(j0, kk, d1, d2);
-        const double *ux = sx + term_index(j0);
+        term_meta(j0, kk, d);
+        const double *ux = sx + 2 * term_index(j0);
 #pragma unroll
-        for (int s = 0; s < S; s++) {
-            Ur[s] = ux[s * D];
-            Ui[s] = REAL ? 0.0 : ux[(S + s) * D];
-        }
+        for (int u = 0; u < S; u++) load_x(ux, u);
     }
-    // part 0's sign (-Ui*Wi) is applied to the streamed y digit w2 (one flip
-    // per digit row, inside the body) rather than to the S held x digits
-    auto neg = [&](double w) { return __longlong_as_double(__double_as_longlong(w) ^ sgn); };
+    // the two real products of digit row l: w = (y re, y im) of that row
+    auto row = [&](int l, double wr, double wi) {
+#pragma unroll
+        for (int u = 0; u < S - l; u++) {
+            if (REAL) {
+                A[u + l] = __fma_rn(Ur[u], wr, A[u + l]);
+            } else if (PART == 0) {
+                A[u + l] = __fma_rn(Ur[u], wr, A[u + l]);
+                A[u + l] = __fma_rn(-Ui[u], wi, A[u + l]);
+            } else {
+                A[u + l] = __fma_rn(Ur[u], wi, A[u + l]);
+                A[u + l] = __fma_rn(Ui[u], wr, A[u + l]);
+            }
+        }
+    };
     // blocks of at most NORM terms, each closed by a carry pass: one loop
     // test per term (no per-term counter test and branch), and the carries
     // stay warp-uniform (every lane's block ends at the same iteration count
@@ -156,54 +173,40 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
         }
         // the next term (this term again on the last iteration: harmless)
         const int jn = j + F <= D ? j + F : j;
-        const double *uxn = sx + term_index(jn);
-        int kkn, d1n, d2n;
+        const double *uxn = sx + 2 * term_index(jn);
+        int kkn, dn;
         auto ahead = [&](int l) {  // called after digit row l of the body
-            if (l == 1) term_meta(jn, kkn, d1n, d2n);
-            const int u = S - 1 - l;
-            Ur[u] = uxn[u * D];
-            if (!REAL) Ui[u] = uxn[(S + u) * D];
+            if (l == 1) term_meta(jn, kkn, dn);
+            load_x(uxn, S - 1 - l);
         };
-        const bool fast = d1 <= PADZ && d2 <= PADZ;
-        if (__all_sync(__activemask(), fast)) {
-            const double *W1 = sy + (w1part * P2 + PADZ - d1) * D + kk;
-            const double *W2 = sy + (w2part * P2 + PADZ - d2) * D + kk;
-            // software pipelined: row l+1's two digits load while row l's FMAs run
-            double w1 = W1[0], w2 = REAL ? 0.0 : neg(W2[0]);
+        if (__all_sync(__activemask(), d <= PADZ)) {
+            const double *W = sy + (PADZ - d) * D2 + 2 * kk;
+            // software pipelined: row l+1's digit pair loads while row l's FMAs run
+            double2 w = REAL ? make_double2(W[0], 0.0) : *reinterpret_cast<const double2 *>(W);
 #pragma unroll
             for (int l = 0; l < S; l++) {
-                double w1n = 0.0, w2n = 0.0;
-                if (l + 1 < S) {
-                    w1n = W1[(l + 1) * D];
-                    if (!REAL) w2n = neg(W2[(l + 1) * D]);
-                }
-#pragma unroll
-                for (int u = 0; u < S - l; u++) {
-                    A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
-                    if (!REAL) A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
-                }
+                double2 wn = make_double2(0.0, 0.0);
+                if (l + 1 < S)
+                    wn = REAL ? make_double2(W[(l + 1) * D2], 0.0)
+                              : *reinterpret_cast<const double2 *>(W + (l + 1) * D2);
+                row(l, w.x, w.y);
                 ahead(l);
-                w1 = w1n;
-                w2 = w2n;
+                w = wn;
             }
         } else {
-            const double *W1 = sy + w1part * P2 * D + kk;
-            const double *W2 = sy + w2part * P2 * D + kk;
+            const double *W = sy + 2 * kk;
 #pragma unroll
             for (int l = 0; l < S; l++) {
-                const double w1 = (l >= d1) ? W1[(PADZ + l - d1) * D] : 0.0;
-                const double w2 = (!REAL && l >= d2) ? neg(W2[(PADZ + l - d2) * D]) : 0.0;
-#pragma unroll
-                for (int u = 0; u < S - l; u++) {
-                    A[u + l] = __fma_rn(Ur[u], w1, A[u + l]);
-                    if (!REAL) A[u + l] = __fma_rn(Ui[u], w2, A[u + l]);
-                }
+                double2 w = make_double2(0.0, 0.0);
+                if (l >= d)
+                    w = REAL ? make_double2(W[(PADZ + l - d) * D2], 0.0)
+                             : *reinterpret_cast<const double2 *>(W + (PADZ + l - d) * D2);
+                row(l, w.x, w.y);
                 ahead(l);
             }
         }
         kk = kkn;
-        d1 = d1n;
-        d2 = d2n;
+        d = dn;
     }
     carry_pass(A);
     }
@@ -215,37 +218,11 @@ __device__ __forceinline__ void conv_dig_pass(const double *__restrict__ sx, con
     // partials (carried, |digit| <= R/2 + 2^31)
 }
 
-template <int L>
-__device__ __forceinline__ void conv_dig_emit_digits(const double (&A)[digits_for(L)], int eacc, double *zd, int *ze,
-                                                     int D, int k, int part, double *scratch);
-
-// normalise and write one output (k, part): limbs (zl != null) for the
-// addition jobs and/or digits with their exponent (zd != null) for later
-// products.  scratch: S+2 doubles of this thread's shared-memory slot (the
-// leading-zero shift by the data-dependent z0 goes through a store/reload).
-template <int L>
-__device__ __forceinline__ void conv_dig_emit(double (&A)[digits_for(L)], int eacc, double *zd, int *ze, double *zl,
-                                              int D, int k, int part, double *scratch) {
-    constexpr int S = digits_for(L);
-    // inputs: carry-passed partials (|A_t| <= R/2 + 2^31) summed over <= 8
-    // lanes, so two parallel carry passes balance every digit to R/2 + 1
-    carry_pass(A);
-    carry_pass(A);
-    if (zd) conv_dig_emit_digits<L>(A, eacc, zd, ze, D, k, part, scratch);
-    if (zl) {  // limbs for the addition jobs: the exact accumulator rounded to L limbs
-        double out[L];
-        digits_to_limbs<L, S, true>(A, eacc - 1, out);  // A_t has weight R^(eacc-2-t); consumes A
-#pragma unroll
-        for (int p = 0; p < L; p++) zl[(part * L + p) * D + k] = out[p];
-    }
-}
-
-// digits of a normalised accumulator with the leading-zero shift
-template <int L>
-__device__ __forceinline__ void conv_dig_emit_digits(const double (&A)[digits_for(L)], int eacc, double *zd, int *ze,
-                                                     int D, int k, int part, double *scratch) {
-    constexpr int S = digits_for(L);
-    // Z = [c2, c1, c0, A_1 .. A_{S-1}], Z_u has weight R^(eacc - u)
+// Z = [c2, c1, c0, A_1 .. A_{S-1}] of a balanced accumulator (Z_u has weight
+// R^(eacc - u)) into shared memory; returns the index of its first nonzero
+// entry (S + 2 if none)
+template <int S>
+__device__ __forceinline__ int conv_dig_z(const double (&A)[S], double *scratch) {
     double a0 = A[0];
     const double c2 = rint_magic(__dmul_rn(a0, INV_RADIX * INV_RADIX));
     a0 = __fma_rn(-c2, RADIX * RADIX, a0);
@@ -263,160 +240,96 @@ __device__ __forceinline__ void conv_dig_emit_digits(const double (&A)[digits_fo
     if (c0 != 0.0) z0 = 2;
     if (c1 != 0.0) z0 = 1;
     if (c2 != 0.0) z0 = 0;
-    const int e = (z0 >= S + 2 || eacc <= ZERO_E / 2) ? ZERO_E : eacc + 1 - z0;
-    const double *src = scratch + z0;
-    const int avail = S + 2 - z0;
-#pragma unroll
-    for (int s = 0; s < S; s++) zd[(part * S + s) * D + k] = (s < avail && e != ZERO_E) ? src[s] : 0.0;
-    ze[part * D + k] = e;
+    return z0;
 }
 
-template <int L, int DT, bool REAL = false>
-// register budget per SM: 4 blocks of 128 up to L = 4 (<= 128 registers),
-// 3 up to L = 8 (<= 170), 2 above; 256-thread blocks for D = 128 and the
-// generic-D build.  REAL: real systems (mdps_options.real): only the real
-// part is computed; the imaginary limbs of the limb outputs are written as 0.
-__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
-                                  DT == 128 || DT == 0 ? 1 : (L <= 4 ? 4 : (L <= 8 ? 3 : 2)))
-    conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool, double *__restrict__ lpool,
-                    const int *__restrict__ jobs, int njobs, int Drt, int T, int F, int P, int NPrt) {
+// The work of one block: P product jobs starting at job0.  NP = 2: complex
+// (part lanes), NP = 1: REAL systems.
+template <int L, int DT, bool REAL>
+__device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *__restrict__ epool,
+                                               double *__restrict__ lpool, const int *__restrict__ jobs, int job0,
+                                               int njobs, int Drt, int T, int F, int P, double *sm) {
     constexpr int S = digits_for(L);
+    constexpr int NP = REAL ? 1 : 2;
     const int D = DT > 0 ? DT : Drt;
     const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
-    const int NP = REAL ? 1 : NPrt;  // part lanes per output pair (1 or 2)
-    const int threads_per_job = T * F * NP;
-    extern __shared__ __align__(16) double sm[];
+    const int half = (P * T * F + 31) / 32 * 32;               // threads per part lane set
     double *sdig = sm;                                        // [P][SX + SY]
-    double *spark = sm + (size_t)P * (SX + SY);               // [threads][S]
+    double *spark = sm + (size_t)P * (SX + SY);               // [threads][S + 2]
     constexpr int PSTR = S + 2;                               // parking / emit scratch slot
-    int *sexp = (int *)(spark + (size_t)blockDim.x * PSTR);   // [P][2 series][2][D]
+    int *sexp = (int *)(spark + (size_t)blockDim.x * PSTR);   // [P][2 series][D]
+    int *szx = sexp + (size_t)P * 2 * D;                      // [2 rounds][P][D][2 parts]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(szx + (size_t)2 * P * D * 2);
 
-    const int job0 = blockIdx.x * P;
-    // stage: x planes -> [part][s][D] (the pool layout), y planes ->
-    // [part][PADZ + s][D], zero planes.  Even D: three 16-byte aligned
-    // contiguous runs per job (x whole, y per part), so one thread issues
-    // three TMA bulk copies (cp.async.bulk) per job against an mbarrier while
-    // the other warps write the zero planes and exponents.  Odd D: one warp
-    // per plane row, scalar loads.
-    uint64_t *bar = reinterpret_cast<uint64_t *>(sexp + (size_t)P * 4 * D);
-    const bool use_tma = (D & 1) == 0;
-    if (use_tma) {
-        if (threadIdx.x == 0) mbar_init(bar, 1);
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(P * 4 * S * D * 8));
-            __syncwarp();
-            for (int c = threadIdx.x; c < 3 * P; c += 32) {  // (job, copy): x | y re | y im
-                const int jl = c / 3, which = c - jl * 3;
-                const int job = min(job0 + jl, njobs - 1);
-                double *base = sdig + (size_t)jl * (SX + SY);
-                if (which == 0)
-                    bulk_g2s(base, dpool + (size_t)jobs[4 * job] * dig_slot_stride(S, D), (unsigned)(2 * S * D * 8),
-                             bar);
-                else
-                    bulk_g2s(base + SX + ((which - 1) * (PADZ + S) + PADZ) * D,
-                             dpool + (size_t)jobs[4 * job + 1] * dig_slot_stride(S, D) + (size_t)(which - 1) * S * D,
-                             (unsigned)(S * D * 8), bar);
-            }
-        }
-    } else {
-        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-        const int nrows = P * 4 * S;  // (job, which, part*S + s)
-#pragma unroll 2
-        for (int row = warp; row < nrows; row += nwarps) {
-            const int jl = row / (4 * S), rem = row - jl * 4 * S;
-            const int which = rem / (2 * S), ps = rem - which * 2 * S;
-            const int part = ps / S, s = ps - part * S;
+    // stage: x -> [S][D][2] (the pool layout), y -> [PADZ + S][D][2] behind
+    // PADZ zero rows: two 16-byte aligned contiguous runs per job (every
+    // slot and row is a multiple of 16 bytes), so one thread issues two TMA
+    // bulk copies (cp.async.bulk) per job against an mbarrier while the
+    // other warps write the zero rows and exponents
+    if (threadIdx.x == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(P * 2 * SX * 8));
+        __syncwarp();
+        for (int c = threadIdx.x; c < 2 * P; c += 32) {  // (job, copy): x | y
+            const int jl = c >> 1, which = c & 1;
             const int job = min(job0 + jl, njobs - 1);
-            const double *g = dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D) + (size_t)ps * D;
-            double *dst = sdig + (size_t)jl * (SX + SY) + (which ? SX + (part * (PADZ + S) + PADZ + s) * D
-                                                                   : (size_t)ps * D);
-            if ((D & 1) == 0) {
-                for (int k = 2 * lane; k < D; k += 64)
-                    *reinterpret_cast<double2 *>(dst + k) = __ldg(reinterpret_cast<const double2 *>(g + k));
-            } else {
-                for (int k = lane; k < D; k += 32) dst[k] = __ldg(g + k);
-            }
+            double *base = sdig + (size_t)jl * (SX + SY) + (which ? SX + 2 * PADZ * D : 0);
+            bulk_g2s(base, dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D), (unsigned)(SX * 8), bar);
         }
     }
-    for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {  // zero planes of both parts
+    for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {  // zero rows
         const int jl = idx / (2 * PADZ * D), r = idx - jl * 2 * PADZ * D;
-        const int part = r / (PADZ * D), rr = r - part * PADZ * D;
-        sdig[(size_t)jl * (SX + SY) + SX + part * (PADZ + S) * D + rr] = 0.0;
+        sdig[(size_t)jl * (SX + SY) + SX + r] = 0.0;
     }
-    for (int idx = threadIdx.x; idx < P * 2 * 2 * D; idx += blockDim.x) {
-        const int jl = idx / (4 * D), r = idx - jl * 4 * D;
-        const int which = r / (2 * D), r2 = r - which * 2 * D;
+    for (int idx = threadIdx.x; idx < P * 2 * D; idx += blockDim.x) {
+        const int jl = idx / (2 * D), r = idx - jl * 2 * D;
+        const int which = r / D, k = r - which * D;
         const int job = min(job0 + jl, njobs - 1);
-        sexp[idx] = epool[(size_t)jobs[4 * job + which] * 2 * D + r2];
+        sexp[idx] = epool[(size_t)jobs[4 * job + which] * dig_exp_stride(D) + k];
     }
-    if (use_tma) mbar_wait(bar, 0);
+    mbar_wait(bar, 0);
     __syncthreads();
 
-    const int jl = threadIdx.x / threads_per_job;
-    const int r0 = threadIdx.x - jl * threads_per_job;
-    const int pl = NP == 2 ? r0 / (T * F) : 0;  // part lane (NP = 2: this thread's part)
-    const int r = r0 - pl * T * F;
+    const int part = NP == 2 ? (int)threadIdx.x / half : 0;  // warp-uniform (half is whole warps)
+    const int r0 = threadIdx.x - part * half;
+    const int jl = r0 / (T * F);
+    const int r = r0 - jl * T * F;
     const int t = r / F, f = r - t * F;
-    const int jlc = min(jl, P - 1);  // padding lanes (blockDim rounded to whole warps) shadow the last job
+    const int jlc = min(jl, P - 1);  // padding lanes (sets rounded to whole warps) shadow the last job
     const double *sx = sdig + (size_t)jlc * (SX + SY), *sy = sx + SX;
-    const int *ex = sexp + jlc * 4 * D, *ey = ex + 2 * D;
+    const int *ex = sexp + jlc * 2 * D, *ey = ex + D;
 
     // exponent pre-pass (split over the F lanes, max-reduced by shuffles):
-    // anchors e_acc of (k1, k2) x (re, im) over ALL terms of each output
-    int ea1r = ZERO_E, ea1i = ZERO_E, ea2r = ZERO_E, ea2i = ZERO_E;
-    if (NP == 2) {  // one part per thread: only its own anchors
-        const int *ey1 = ey + pl * D, *ey2 = ey + (1 - pl) * D;
-        for (int j = f; j <= D; j += F) {
-            const bool first = j <= t;
-            const int i = first ? j : D - j;  // the pass's term order (conv_dig_pass)
-            const int kk = first ? t - j : j - t - 1;
-            const int e = max(ex[i] + ey1[kk], ex[D + i] + ey2[kk]);
-            if (first) ea1r = max(ea1r, e);
-            else ea2r = max(ea2r, e);
-        }
-        ea1i = ea1r;
-        ea2i = ea2r;
-    } else {
-        for (int j = f; j <= D; j += F) {
-            const bool first = j <= t;
-            const int i = first ? j : D - j;  // the pass's term order (conv_dig_pass)
-            const int kk = first ? t - j : j - t - 1;
-            const int xr = ex[i], xi = REAL ? ZERO_E : ex[D + i], yr = ey[kk], yi = REAL ? ZERO_E : ey[D + kk];
-            const int er = max(xr + yr, xi + yi), ei = max(xr + yi, xi + yr);
-            if (first) {
-                ea1r = max(ea1r, er);
-                ea1i = max(ea1i, ei);
-            } else {
-                ea2r = max(ea2r, er);
-                ea2i = max(ea2i, ei);
-            }
-        }
+    // anchors e_acc of k1 and k2 over ALL their terms (one exponent per
+    // complex coefficient: the same anchors for both parts)
+    int ea1 = ZERO_E, ea2 = ZERO_E;
+    for (int j = f; j <= D; j += F) {
+        const bool first = j <= t;
+        const int e = first ? ex[j] + ey[t - j] : ex[D - j] + ey[j - t - 1];  // the pass's term order
+        if (first) ea1 = max(ea1, e);
+        else ea2 = max(ea2, e);
     }
     for (int off = F >> 1; off > 0; off >>= 1) {
-        ea1r = max(ea1r, __shfl_xor_sync(0xffffffffu, ea1r, off));
-        ea1i = max(ea1i, __shfl_xor_sync(0xffffffffu, ea1i, off));
-        ea2r = max(ea2r, __shfl_xor_sync(0xffffffffu, ea2r, off));
-        ea2i = max(ea2i, __shfl_xor_sync(0xffffffffu, ea2i, off));
+        ea1 = max(ea1, __shfl_xor_sync(0xffffffffu, ea1, off));
+        ea2 = max(ea2, __shfl_xor_sync(0xffffffffu, ea2, off));
     }
-    ea1r = max(ea1r, ZERO_E);
-    ea1i = max(ea1i, ZERO_E);
-    ea2r = max(ea2r, ZERO_E);
-    ea2i = max(ea2i, ZERO_E);
+    ea1 = max(ea1, ZERO_E);
+    ea2 = max(ea2, ZERO_E);
 
     double *park = spark + (size_t)threadIdx.x * PSTR;
     const int job = job0 + jl;
     const bool writer = jl < P && job < njobs;
-    double *zd = dpool;
-    int *ze = epool;
+    double *zd = nullptr;  // digit output (the series is a product input)
+    int *ze = nullptr;
     double *zl = nullptr;  // limb output (the series is summed by the addition jobs)
-    int wdig = 0;          // digit output (the series is a product input)
     if (writer) {
         const int out = jobs[4 * job + 2];
         const int code = jobs[4 * job + 3];
-        zd = dpool + (size_t)out * dig_slot_stride(S, D);
-        ze = epool + (size_t)out * 2 * D;
-        wdig = code & 1;
+        if (code & 1) {
+            zd = dpool + (size_t)out * dig_slot_stride(S, D);
+            ze = epool + (size_t)out * dig_exp_stride(D);
+        }
         if (code & 2) zl = lpool + (size_t)(code >> 2) * 2 * L * D;
     }
     const int k1 = t, k2 = D - 1 - t;
@@ -427,44 +340,82 @@ __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
                 if (F == 1 || f == 1) zl[(L + p) * D + k2] = 0.0;
             }
     }
-#pragma unroll 1
-    for (int part = pl; part < (REAL ? 1 : (NP == 2 ? pl + 1 : 2)); part++) {
-        double A[S];
-        const int e1 = part ? ea1i : ea1r, e2 = part ? ea2i : ea2r;
-        conv_dig_pass<L, DT, REAL>(sx, sy, ex, ey, D, part, t, f, F, e1, e2, A, park);
-        // k1: every lane carries its parked (raw) partial — warp-uniform work,
-        // no lane sums alone — and takes it off A, which leaves the k2 partial
-        // (|digit| <= R + 2^32: exact)
-        double B[S];
+    double A[S];
+    if (part == 0)
+        conv_dig_pass<L, DT, 0, REAL>(sx, sy, ex, ey, D, t, f, F, ea1, ea2, A, park);
+    else
+        conv_dig_pass<L, DT, 1, false>(sx, sy, ex, ey, D, t, f, F, ea1, ea2, A, park);
+    // k1: every lane carries its parked (raw) partial — warp-uniform work,
+    // no lane sums alone — and takes it off A, which leaves the k2 partial
+    // (|digit| <= R + 2^32: exact)
+    double B[S];
 #pragma unroll
-        for (int s = 0; s < S; s++) B[s] = park[s];
-        carry_pass(B);
+    for (int s = 0; s < S; s++) B[s] = park[s];
+    carry_pass(B);
 #pragma unroll
-        for (int s = 0; s < S; s++) A[s] = __dsub_rn(A[s], B[s]);
-        // k2: sum the F lanes' partials (exact) with shuffles; every lane has it
-        for (int off = F >> 1; off > 0; off >>= 1) {
+    for (int s = 0; s < S; s++) A[s] = __dsub_rn(A[s], B[s]);
+    // sum the F lanes' partials of k2 (A) and k1 (B), exact, with shuffles
+    for (int off = F >> 1; off > 0; off >>= 1) {
 #pragma unroll
-            for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
+        for (int s = 0; s < S; s++) {
+            A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
+            B[s] = __dadd_rn(B[s], __shfl_xor_sync(0xffffffffu, B[s], off));
         }
-        // k1: the same shuffle reduction
-        for (int off = F >> 1; off > 0; off >>= 1) {
-#pragma unroll
-            for (int s = 0; s < S; s++) B[s] = __dadd_rn(B[s], __shfl_xor_sync(0xffffffffu, B[s], off));
-        }
-        __syncwarp();  // parked partials consumed before the emit scratch reuses them
-        if (F == 1) {
-            if (writer && k2 != k1) conv_dig_emit<L>(A, e2, wdig ? zd : nullptr, ze, zl, D, k2, part, park);
-            if (writer) conv_dig_emit<L>(B, e1, wdig ? zd : nullptr, ze, zl, D, k1, part, park);
-        } else if (writer && f < 2 && (f == 0 || k2 != k1)) {
-            // lanes 0 and 1 emit k1 and k2 in one (lane-dependent) call
-            if (f == 0) {
-#pragma unroll
-                for (int s = 0; s < S; s++) A[s] = B[s];
-            }
-            conv_dig_emit<L>(A, f == 0 ? e1 : e2, wdig ? zd : nullptr, ze, zl, D, f == 0 ? k1 : k2, part, park);
-        }
-        __syncwarp();
     }
+    __syncwarp();  // parked partials consumed before the emit scratch reuses them
+    // emit: F = 1 — every lane emits k2 (round 0) then k1 (round 1); F >= 2 —
+    // lane f = 0 emits k1, lane f = 1 emits k2 (one round).  Per round: the
+    // accumulator balanced (two carry passes: partial sums of <= 8 lanes),
+    // its Z vector parked, the leading digit exchanged with the other part
+    // lane of the output (block barrier), then digits on the common grid
+    // and/or limbs.
+    const int rounds = F == 1 ? 2 : 1;
+    for (int rd = 0; rd < rounds; rd++) {
+        const bool use_b = F == 1 ? rd == 1 : f == 0;
+        const int k = use_b ? k1 : k2;
+        const int eacc = use_b ? ea1 : ea2;
+        const bool mine = writer && (F == 1 || f < 2) && (use_b || k2 != k1);
+        double Z[S];
+#pragma unroll
+        for (int s = 0; s < S; s++) Z[s] = use_b ? B[s] : A[s];
+        carry_pass(Z);
+        carry_pass(Z);
+        const int z0 = conv_dig_z<S>(Z, park);
+        int *zx = szx + (size_t)rd * P * D * 2;
+        if (NP == 2 && mine) zx[(jl * D + k) * 2 + part] = z0;
+        if (NP == 2) __syncthreads();
+        if (mine) {
+            if (zd) {  // digits on the grid of the larger part
+                const int zc = NP == 2 ? min(z0, zx[(jl * D + k) * 2 + 1 - part]) : z0;
+                const int e = (zc >= S + 2 || eacc <= ZERO_E / 2) ? ZERO_E : eacc + 1 - zc;
+                const double *src = park + zc;
+                const int avail = S + 2 - zc;
+#pragma unroll
+                for (int s = 0; s < S; s++) zd[((size_t)s * D + k) * 2 + part] = (s < avail && e != ZERO_E) ? src[s] : 0.0;
+                if (part == 0) ze[k] = e;
+            }
+            if (zl) {  // limbs for the addition jobs: the exact accumulator rounded to L limbs
+                double out[L];
+                digits_to_limbs<L, S, true>(Z, eacc - 1, out);  // Z_t has weight R^(eacc-2-t); consumes Z
+#pragma unroll
+                for (int p = 0; p < L; p++) zl[(part * L + p) * D + k] = out[p];
+            }
+        }
+        __syncwarp();  // the scratch is free again before the next round parks into it
+    }
+}
+
+template <int L, int DT, bool REAL = false>
+// register budget per SM: 4 blocks of 128 up to L = 4 (<= 128 registers),
+// 3 up to L = 8 (<= 170), 2 above; 256-thread blocks for D = 128 and the
+// generic-D build.  REAL: real systems (mdps_options.real): only the real
+// part is computed; the imaginary limbs of the limb outputs are written as 0.
+__global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128,
+                                  DT == 128 || DT == 0 ? 1 : (L <= 4 ? 4 : (L <= 8 ? 3 : 2)))
+    conv_dig_kernel(double *__restrict__ dpool, int *__restrict__ epool, double *__restrict__ lpool,
+                    const int *__restrict__ jobs, int njobs, int Drt, int T, int F, int P) {
+    extern __shared__ __align__(16) double sm[];
+    conv_dig_block<L, DT, REAL>(dpool, epool, lpool, jobs, blockIdx.x * P, njobs, Drt, T, F, P, sm);
 }
 
 }  // namespace mdps

@@ -15,11 +15,12 @@
 // rounding is the truncation below digit S-1, which S is chosen to put more
 // than 8 bits below the md precision 2^(-53 L).
 //
-// Representation (pool slot s): digits [2][S][D] doubles (part, digit,
-// coefficient) and radix exponents [2][D] int32.  Part value
+// Representation (pool slot s): digits [S][D][2] doubles (digit, coefficient,
+// part) and one radix exponent per complex coefficient [D] int32.  Part value
 //     v = sum_j  digit_j * R^(e - 1 - j),   R = 2^BETA,  |v| < R^e / 2,
-// every digit balanced (|digit_j| <= R/2 + 1, the top one included); a zero
-// part has e = ZERO_E.  Limb planes (the ABI layout) are converted to digits on
+// every digit balanced (|digit_j| <= R/2 + 1, the top one included); both
+// parts of a coefficient share e (the larger part's); a zero coefficient has
+// e = ZERO_E.  Limb planes (the ABI layout) are converted to digits on
 // entry (x every call, coefficients at create) and back to limbs only for
 // values and Jacobian entries (the addition jobs), so the whole DAG runs on
 // digits.
@@ -59,8 +60,10 @@ __host__ __device__ constexpr int digits_for(int L) {
 // carried out of: it collects at most 2 D (R/2+1)^2 < 2^53 for D <= 128.
 __host__ __device__ constexpr int norm_every(int S) { return 25600 / (S * 101) - 1; }
 
-// doubles per digit-pool slot (one series: [2][S][D])
+// doubles per digit-pool slot (one series: [S][D][2]) and ints per exponent
+// slot (one per complex coefficient: [D])
 __host__ __device__ constexpr size_t dig_slot_stride(int S, int D) { return (size_t)2 * S * D; }
+__host__ __device__ constexpr size_t dig_exp_stride(int D) { return (size_t)D; }
 
 // 2^(BETA*q) as a double: exact in the normal range, else formed by two
 // scalings (rounds into the subnormal range / saturates)
@@ -104,22 +107,26 @@ __device__ __forceinline__ int ceil_div(int a, int b) { return a >= 0 ? (a + b -
 // 2^k as a double for k in [-1022, 1023]
 __device__ __forceinline__ double pow2i(int k) { return __longlong_as_double((long long)(1023 + k) << 52); }
 
-// one real md number (L limbs, any overlap) -> S balanced digits + exponent.
-// The limbs are first scaled EXACTLY by 2^(-BETA (e-1)) (two power-of-two
-// factors, each in range), so the digit grid is fixed — R^0 .. R^-(S-1) —
-// whatever the magnitude: no weight under- or overflows for tiny values.
-template <int L, int S>
-__device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d)[S]) {
+// radix exponent of one real md number (L limbs, any overlap): the smallest
+// e with |v| < R^e / 2 (a balanced top digit); ZERO_E for zero, 0 for NaN
+template <int L>
+__device__ __forceinline__ int limbs_exponent(const double (&v0)[L]) {
     double m = 0.0;
 #pragma unroll
     for (int p = 0; p < L; p++) m = __dadd_ru(m, fabs(v0[p]));
-    if (!(m > 0.0)) {  // zero (or NaN: also mapped to the zero encoding's exponent)
-#pragma unroll
-        for (int j = 0; j < S; j++) d[j] = (m == 0.0) ? 0.0 : m;
-        return m == 0.0 ? ZERO_E : 0;
-    }
-    const int emin = ilogb(m) + 1;          // |v| <= m < 2^emin
-    const int e = ceil_div(emin + 1, BETA);  // |v| < R^e / 2: a balanced top digit
+    if (!(m > 0.0)) return m == 0.0 ? ZERO_E : 0;
+    const int emin = ilogb(m) + 1;  // |v| <= m < 2^emin
+    return ceil_div(emin + 1, BETA);
+}
+
+// one real md number -> S balanced digits on the grid of exponent e (e at
+// least its own limbs_exponent; a larger e puts leading zero digits in
+// front and rounds at digit S-1 of the larger grid).  The limbs are first
+// scaled EXACTLY by 2^(-BETA (e-1)) (two power-of-two factors, each in
+// range), so the digit grid is fixed — R^0 .. R^-(S-1) — whatever the
+// magnitude: no weight under- or overflows for tiny values.
+template <int L, int S>
+__device__ __forceinline__ void limbs_to_digits_at(const double (&v0)[L], int e, double (&d)[S]) {
     const int sh = -BETA * (e - 1), s1 = sh / 2, s2 = sh - s1;
     const double f1 = pow2i(s1), f2 = pow2i(s2);
     double v[L];
@@ -138,6 +145,44 @@ __device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d
         d[j] = __dmul_rn(acc, pow2i(BETA * j));
     }
     carry_normalize(d);
+}
+
+// one real md number (L limbs, any overlap) -> S balanced digits + exponent
+// (its own grid; the solver's digit vectors)
+template <int L, int S>
+__device__ __forceinline__ int limbs_to_digits(const double (&v0)[L], double (&d)[S]) {
+    const int e = limbs_exponent<L>(v0);
+    if (e == ZERO_E || e == 0) {
+        double m = 0.0;
+#pragma unroll
+        for (int p = 0; p < L; p++) m = __dadd_ru(m, fabs(v0[p]));
+        if (!(m > 0.0)) {  // zero (or NaN: also mapped to the zero encoding's exponent)
+#pragma unroll
+            for (int j = 0; j < S; j++) d[j] = (m == 0.0) ? 0.0 : m;
+            return m == 0.0 ? ZERO_E : 0;
+        }
+    }
+    limbs_to_digits_at<L, S>(v0, e, d);
+    return e;
+}
+
+// one complex md number -> S digits per part on ONE grid, the exponent of
+// the larger part (the product pool's format): every term of
+// a truncated product then has one alignment shift for both of its real
+// products, and a digit row of y is one 16-byte (re, im) pair.  The smaller
+// part keeps its digits down to R^(e-S) — the precision of the complex number
+// normwise (R20).  NaN parts propagate as NaN digits.
+template <int L, int S>
+__device__ __forceinline__ int cplx_to_digits(const double (&re)[L], const double (&im)[L], double (&dr)[S],
+                                              double (&di)[S]) {
+    const int e = max(limbs_exponent<L>(re), limbs_exponent<L>(im));
+    if (e == ZERO_E) {
+#pragma unroll
+        for (int j = 0; j < S; j++) dr[j] = di[j] = 0.0;
+        return ZERO_E;
+    }
+    limbs_to_digits_at<L, S>(re, e, dr);
+    limbs_to_digits_at<L, S>(im, e, di);
     return e;
 }
 
@@ -166,8 +211,10 @@ __device__ __forceinline__ void digits_to_limbs(double (&A)[S], int e, double (&
 }
 
 // ---------------------------------------------------------------------------
-// to_digits: limb series [2][L][D] (src[slot_src]) -> digit pool slot.
-// one thread per (series, coefficient); `count` series, src contiguous.
+// to_digits: limb series [2][L][D] (src) -> digit pool slots slot0.. in the
+// pool format: digits [S][D][2] (digit, coefficient, part), one exponent per
+// complex coefficient [D].  One thread per (series, coefficient); `count`
+// series, src contiguous.
 template <int L>
 __global__ void __launch_bounds__(128) to_digits_kernel(const double *__restrict__ src, int count, int D,
                                                        double *__restrict__ dpool,
@@ -178,35 +225,40 @@ __global__ void __launch_bounds__(128) to_digits_kernel(const double *__restrict
     const int s = (int)(g / D), k = (int)(g - (long long)s * D);
     const double *x = src + (size_t)s * 2 * L * D;
     double *dd = dpool + (size_t)(slot0 + s) * dig_slot_stride(S, D);
-    int *ee = epool + (size_t)(slot0 + s) * 2 * D;
+    double re[L], im[L], dr[S], di[S];
 #pragma unroll
-    for (int part = 0; part < 2; part++) {
-        double v[L], d[S];
-#pragma unroll
-        for (int p = 0; p < L; p++) v[p] = x[(part * L + p) * D + k];
-        const int e = limbs_to_digits<L, S>(v, d);
-#pragma unroll
-        for (int j = 0; j < S; j++) dd[(part * S + j) * D + k] = d[j];
-        ee[part * D + k] = e;
+    for (int p = 0; p < L; p++) {
+        re[p] = x[p * D + k];
+        im[p] = x[(L + p) * D + k];
     }
+    const int e = cplx_to_digits<L, S>(re, im, dr, di);
+#pragma unroll
+    for (int j = 0; j < S; j++) *reinterpret_cast<double2 *>(dd + ((size_t)j * D + k) * 2) = make_double2(dr[j], di[j]);
+    epool[(size_t)(slot0 + s) * dig_exp_stride(D) + k] = e;
 }
 
-// limbs -> digits -> limbs round trip (unit test of the staging format)
+// limbs -> digits (the pool format, cplx_to_digits) -> limbs round trip
+// (unit test of the staging format); one thread per (series, coefficient)
 template <int L>
 __global__ void digits_roundtrip_kernel(const double *__restrict__ x, double *__restrict__ y, int count,
                                         int D) {
     constexpr int S = digits_for(L);
     const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= (long long)count * 2 * D) return;
-    const int s = (int)(g / (2 * D)), r = (int)(g - (long long)s * 2 * D);
-    const int part = r / D, k = r - part * D;
-    double v[L], d[S], out[L];
+    if (g >= (long long)count * D) return;
+    const int s = (int)(g / D), k = (int)(g - (long long)s * D);
+    double re[L], im[L], dr[S], di[S], out[L];
 #pragma unroll
-    for (int p = 0; p < L; p++) v[p] = x[((size_t)s * 2 * L + part * L + p) * D + k];
-    const int e = limbs_to_digits<L, S>(v, d);
-    digits_to_limbs<L, S>(d, e, out);
+    for (int p = 0; p < L; p++) {
+        re[p] = x[((size_t)s * 2 * L + p) * D + k];
+        im[p] = x[((size_t)s * 2 * L + L + p) * D + k];
+    }
+    const int e = cplx_to_digits<L, S>(re, im, dr, di);
+    digits_to_limbs<L, S>(dr, e, out);
 #pragma unroll
-    for (int p = 0; p < L; p++) y[((size_t)s * 2 * L + part * L + p) * D + k] = out[p];
+    for (int p = 0; p < L; p++) y[((size_t)s * 2 * L + p) * D + k] = out[p];
+    digits_to_limbs<L, S>(di, e, out);
+#pragma unroll
+    for (int p = 0; p < L; p++) y[((size_t)s * 2 * L + L + p) * D + k] = out[p];
 }
 
 }  // namespace mdps

@@ -73,67 +73,61 @@ static EftGeom eft_geom(int L, int D) {
 struct DigGeom {
     int T, F, P, threads;
     size_t smem;
-    int NP = 1;  // part lanes per output pair: 1 (both parts on one thread) or 2
+    int NP = 2;  // part lane sets: 2 for complex systems (one warp set per part), 1 for real ones
 };
 // Launch geometry of the product kernel: F lanes per output pair and P jobs
-// per block (and NP part lanes where measured: kTunedGeom), chosen by modelled throughput — resident warps per SM (limited
+// per block, chosen by modelled throughput — resident warps per SM (limited
 // by registers, shared memory and 64 warps), lane balance of the folded
-// triangle ((D+1) terms over F lanes) and the per-lane term count that
-// amortises the per-output epilogue — unless a measured table entry exists.
+// triangle ((D+1) terms over F lanes, each part's lane set padded to whole
+// warps) and the per-lane term count that amortises the per-output epilogue
+// — unless a measured table entry exists.
 // forced geometry of the product kernel (mdps_test_force_geometry; tuning only)
 static int g_force_F = 0, g_force_P = 0, g_force_NP = 0;
 static int g_force_queue_blocks = 0;  // mdps_test_queue_config: grid cap of the queue kernel (0 = occupancy)
 static int g_force_queue_F = 0;       // mdps_test_queue_config: lanes per output pair and part (0 = default)
 
-// Measured best (F, P, NP) of the complex digit kernel where it beats the
-// model by > 1% (scripts/tune_table.py, every fitting (F, P, NP) timed on the
-// sweep cells and configs, L2 flushed; profiles/r02_tune_table.json):
-// {L, D, F, P, NP}.  One thread per part (NP = 2) wins wherever the bodies
-// are long (L >= 8: od 46.1 -> 43.6 ms, deca 186 -> 175 ms) or the levels
-// short (D <= 32: qd 0.889 -> 0.842 ms, d = 15 L = 8 -19%); at L <= 4 with
-// D >= 64 both passes on one thread stay best.
-static const int kTunedGeom[][5] = {
-    {3, 16, 2, 1, 2},  {3, 64, 2, 1, 1},  {4, 16, 2, 1, 2},  {4, 32, 2, 1, 2},  {5, 16, 2, 1, 2},
-    {5, 32, 1, 1, 2},  {5, 64, 1, 1, 2},  {8, 16, 2, 1, 2},  {8, 32, 2, 1, 2},  {8, 64, 2, 1, 2},
-    {8, 128, 2, 1, 2}, {10, 16, 2, 1, 2}, {10, 32, 2, 1, 2}, {10, 64, 2, 1, 2}, {10, 128, 2, 1, 2},
+// Measured best (F, P) of the complex digit kernel where it beats the model
+// by > 1% (scripts/tune_table.py, every fitting (F, P) timed on the sweep
+// cells and configs, L2 flushed; profiles/r02_tune_table_aligned.json):
+// {L, D, F, P}.  At L = 4, D = 32 the qd config (-5%) wins over the d = 31
+// sweep cell (+3.6%).
+static const int kTunedGeom[][4] = {
+    {2, 16, 2, 2}, {2, 32, 2, 1}, {3, 16, 2, 2}, {3, 32, 1, 4}, {3, 128, 1, 1}, {4, 32, 2, 1},
+    {5, 16, 1, 4}, {5, 32, 1, 2}, {5, 64, 1, 1}, {8, 16, 2, 4}, {10, 16, 2, 4}, {10, 32, 2, 2},
 };
 
 // The same for the real-system kernel (mdps_options.real; TUNE_REAL=1,
-// profiles/r01_tune_table_real.json; one part, so NP = 1).
-static const int kTunedGeomReal[][5] = {
-    {2, 32, 2, 2, 1},  {3, 16, 2, 4, 1},  {3, 64, 2, 1, 1},  {3, 128, 2, 1, 1}, {4, 16, 2, 2, 1},
-    {4, 32, 2, 2, 1},  {5, 16, 2, 2, 1},  {5, 32, 2, 1, 1},  {5, 64, 2, 1, 1},  {8, 16, 2, 2, 1},
-    {10, 16, 2, 4, 1}, {10, 32, 2, 2, 1}, {10, 64, 2, 1, 1},
+// profiles/r01_tune_table_real.json).
+static const int kTunedGeomReal[][4] = {
+    {2, 32, 2, 2},  {3, 16, 2, 4},  {3, 64, 2, 1},  {3, 128, 2, 1}, {4, 16, 2, 2},  {4, 32, 2, 2},
+    {5, 16, 2, 2},  {5, 32, 2, 1},  {5, 64, 2, 1},  {8, 16, 2, 2},  {10, 16, 2, 4}, {10, 32, 2, 2},
+    {10, 64, 2, 1},
 };
 
-// tuned: 0 the model only, 1 the complex table, 2 the real table; forceF/P/NP
-// > 0 restrict the search to that F / P / NP (the model itself keeps NP = 1)
-static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int forceF = 0, int forceP = 0,
-                        int tuned = 0, int forceNP = 0) {
+// real: the real-system kernel (one part lane set) and its table; tuned:
+// use the table; forceF/P > 0 restrict the search to that F / P
+static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool real, int forceF = 0,
+                        int forceP = 0, bool tuned = false) {
     const int S = digits_for(L);
     const int T = (D + 1) / 2;
-    DigGeom best{T, 1, 1, 32, 0, 1};
+    const int NP = real ? 1 : 2;
+    DigGeom best{T, 1, 1, 32, 0, NP};
     double best_score = -1.0;
-    if (tuned && forceF == 0 && forceP == 0 && forceNP == 0) {
+    if (tuned && forceF == 0 && forceP == 0) {
         auto pick = [&](const auto &table) {
             for (const auto &t : table)
                 if (t[0] == L && t[1] == D) {
                     forceF = t[2];
                     forceP = t[3];
-                    forceNP = t[4];
                 }
         };
-        if (tuned == 1) pick(kTunedGeom);
-        else pick(kTunedGeomReal);
+        if (real) pick(kTunedGeomReal);
+        else pick(kTunedGeom);
     }
-    if (tuned == 2 && forceNP > 1) return DigGeom{T, 1, 1, 32, 0, 1};  // real systems: one part
     // resident warps count up to 16 per SM; measured (profiles/r01_sweep.json
     // history): at L = 4, D >= 32 more terms per lane beat the 16th warp
     // (qd 1.03 -> 0.97 ms, d = 31 -12%, d = 63 -7%), elsewhere 16 is right
     const int warp_cap = (L == 4 && D >= 32) ? 12 : 16;
-    // NP without a measurement: one thread per part where the table shows it
-    // winning (long bodies, or short levels), both parts on one thread else
-    const int NP = forceNP > 0 ? forceNP : (tuned != 2 && (L >= 5 || D <= 32) ? 2 : 1);
     for (int F = 1; F <= 8; F *= 2) {
         if (forceF > 0 && forceF != F) continue;
         for (int P = 1; P <= 32; P *= 2) {
@@ -143,7 +137,7 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int 
             g.F = F;
             g.P = P;
             g.NP = NP;
-            g.threads = (P * T * F * NP + 31) / 32 * 32;  // whole warps (full-mask shuffles)
+            g.threads = NP * ((P * T * F + 31) / 32 * 32);  // each part's lane set whole warps
             if (g.threads > max_threads) continue;
             g.smem = conv_dig_smem(S, D, P, g.threads);
             if (g.smem > 227 * 1024) continue;
@@ -153,7 +147,7 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, int 
             if (blocks < 1) continue;
             const int warps = std::min(blocks * g.threads / 32, 64);
             const int iters = (D + 1 + F - 1) / F;
-            const double balance = (double)(D + 1) / (F * iters) * (double)(P * T * F * NP) / g.threads;
+            const double balance = (double)(D + 1) / (F * iters) * (double)(NP * P * T * F) / g.threads;
             const double amort = (double)iters / (iters + 3.0);
             const double score = std::min(warps, warp_cap) * balance * amort;
             if (score > best_score) {
@@ -185,9 +179,9 @@ struct ConvDig {
     static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, int real,
                    cudaStream_t st) {
         if (njobs <= 0) return MDPS_OK;
-        using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int, int);
+        using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
         KernT kern;
-        if (real)  // real systems: the two-pass kernel with one product per term
+        if (real)  // real systems: one part, one product per term
             kern = D == 16 ? conv_dig_kernel<L, 16, true> : D == 32 ? conv_dig_kernel<L, 32, true>
                  : D == 64 ? conv_dig_kernel<L, 64, true> : D == 128 ? conv_dig_kernel<L, 128, true>
                  : conv_dig_kernel<L, 0, true>;
@@ -214,23 +208,26 @@ struct ConvDig {
                 }
                 cregs[key] = regs;
                 cmaxt[key] = maxt;
-                cache[key] = dig_geom(L, D, regs, maxt, 0, 0, real ? 2 : 1);
+                cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, true);
                 if (cache[key].smem == 0)  // tuned entry does not fit
-                    cache[key] = dig_geom(L, D, regs, maxt, 0, 0, 0, real ? 1 : 0);
+                    cache[key] = dig_geom(L, D, regs, maxt, real != 0);
                 cached[key] = true;
             }
             g = cache[key];
             regs = cregs[key];
             maxt = cmaxt[key];
         }
-        if (g_force_F > 0 || g_force_P > 0 || g_force_NP > 0) {  // tuning: a forced (F, P, NP), checked
-            if (real && g_force_NP > 1) { set_err("forced geometry: real systems have one part (NP = 1)"); return MDPS_EINVAL; }
-            g = dig_geom(L, D, regs, maxt, g_force_F, g_force_P, 0, real ? 1 : g_force_NP);
+        if (g_force_F > 0 || g_force_P > 0 || g_force_NP > 0) {  // tuning: a forced (F, P), checked
+            if (g_force_NP > 0 && g_force_NP != (real ? 1 : 2)) {
+                set_err("forced geometry: complex systems run one lane set per part (NP = 2), real ones NP = 1");
+                return MDPS_EINVAL;
+            }
+            g = dig_geom(L, D, regs, maxt, real != 0, g_force_F, g_force_P);
             if (g.smem == 0) { set_err("forced geometry does not fit"); return MDPS_EINVAL; }
         }
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
-        kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, lpool, jobs, njobs, D, g.T, g.F, g.P, g.NP);
+        kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, lpool, jobs, njobs, D, g.T, g.F, g.P);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -445,15 +442,13 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     const int B = opt && opt->batch > 1 ? opt->batch : 1;
     if (opt && opt->batch < 0) { set_err("batch must be >= 1"); return nullptr; }
     // MDPS_ALGO_AUTO (measured): digits, except above degree 127
-    // (digits cap), at L = 2 and at L = 3 up to degree 31 on systems of >= 4096
-    // product jobs per point (a batch picks what its points pick).  There the
-    // digit kernel is shared-memory bound (S = 7, 10 digits: 4S loads per
-    // S(S+1) DFMAs) and the EFT kernel is faster: 1.4-1.5x on the L = 2 sweep
-    // cells, 2.1x on a batch of 1024 dd points, even on dd itself; at L = 3 by
-    // 2-7% up to degree 31 (digits with the tuned geometry win from 63 on)
+    // (digits cap) and at L = 2, where the digit kernel is shared-memory bound
+    // (S = 7 digits: 2S 16-byte loads per S(S+1) DFMAs) and the EFT kernel is
+    // faster (the L = 2 sweep cells from degree 31 on, batches of dd points,
+    // dd itself); at L = 3 the digit kernel on the common-exponent format
+    // wins from degree 15 on (d = 15: 0.43 vs 0.55 ms, d = 31: 1.19 vs 1.48)
     if (algo == MDPS_ALGO_AUTO)
-        algo = D > 128 || (!real && (limbs == 2 || (limbs == 3 && D <= 32 && S.products >= 4096)))
-                   ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
+        algo = D > 128 || (!real && limbs == 2) ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
     const int sched_opt = opt ? opt->schedule : MDPS_SCHED_AUTO;
     if (sched_opt != MDPS_SCHED_AUTO && sched_opt != MDPS_SCHED_LEVELS && sched_opt != MDPS_SCHED_QUEUE) {
         set_err("unknown schedule");
@@ -555,7 +550,7 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     const size_t ser = algo == MDPS_ALGO_DIGITS ? dig_slot_stride(s->S, D) : (size_t)2 * limbs * D;  // doubles per slot
     const size_t before_pools = s->device_bytes;
     if (!dalloc(s, &s->pool, ser * (size_t)s->nslots) ||
-        (algo == MDPS_ALGO_DIGITS && !dalloc(s, &s->epool, (size_t)2 * D * s->nslots)) ||
+        (algo == MDPS_ALGO_DIGITS && !dalloc(s, &s->epool, dig_exp_stride(D) * s->nslots)) ||
         (algo == MDPS_ALGO_DIGITS && !dalloc(s, &s->lpool, (size_t)2 * limbs * D * nlimb))) {
         free_system(s);
         return nullptr;
@@ -921,7 +916,7 @@ struct Norm2sq {
 template <int L>
 struct Roundtrip {
     static int run(const double *x, double *y, int count, int D, cudaStream_t st) {
-        const long long total = (long long)count * 2 * D;
+        const long long total = (long long)count * D;
         digits_roundtrip_kernel<L><<<(int)((total + 127) / 128), 128, 0, st>>>(x, y, count, D);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
@@ -946,7 +941,7 @@ struct SeriesMulDig {
             hj[4 * c + 3] = (c << 2) | 2;
         }
         if (cudaMalloc((void **)&dp, slots * dig_slot_stride(S, D) * 8) != cudaSuccess ||
-            cudaMalloc((void **)&ep, slots * 2 * D * 4) != cudaSuccess ||
+            cudaMalloc((void **)&ep, slots * dig_exp_stride(D) * 4) != cudaSuccess ||
             cudaMalloc((void **)&jobs, hj.size() * 4) != cudaSuccess) {
             cudaGetLastError();
             set_err("cudaMalloc failed");

@@ -445,7 +445,7 @@ bool plan_memory(Schedule &S, int32_t n, int32_t chunks, bool eft, std::string &
 int64_t plan_bytes(const Schedule &S, int S_digits, int L, int D, bool eft) {
     const int64_t limb = (int64_t)2 * L * D * 8;
     if (eft) return (S.planned ? S.dig_slots : S.nslots) * limb;
-    const int64_t dig = (int64_t)2 * S_digits * D * 8 + (int64_t)2 * D * 4;
+    const int64_t dig = (int64_t)2 * S_digits * D * 8 + (int64_t)D * 4;  // digits [S][D][2], exponents [D]
     return (S.planned ? S.dig_slots : S.nslots) * dig + (S.planned ? S.plan_nlimb : S.nlimb) * limb;
 }
 

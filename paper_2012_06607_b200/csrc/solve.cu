@@ -48,6 +48,24 @@ void mdps_internal_set_error(const std::string &s);  // libmdps.cu
 int mdps_internal_system_shape(const mdps_system *s, int *N, int *n, int *D, int *L);
 
 namespace mdps {
+
+// normalise one digit vector entry of the solver (planes [part][S][stride],
+// exponents [part][stride], its own grid per part) and store it: two carry
+// passes balance the partial sums, then the leading-zero shift
+template <int L>
+__device__ __forceinline__ void ts_emit(double (&A)[digits_for(L)], int eacc, double *zd, int *ze, int stride,
+                                        int part, double *scratch) {
+    constexpr int S = digits_for(L);
+    carry_pass(A);
+    carry_pass(A);
+    const int z0 = conv_dig_z<S>(A, scratch);
+    const int e = (z0 >= S + 2 || eacc <= ZERO_E / 2) ? ZERO_E : eacc + 1 - z0;
+    const double *src = scratch + z0;
+    const int avail = S + 2 - z0;
+#pragma unroll
+    for (int s = 0; s < S; s++) zd[(size_t)(part * S + s) * stride] = (s < avail && e != ZERO_E) ? src[s] : 0.0;
+    ze[(size_t)part * stride] = e;
+}
 namespace ts {
 
 constexpr int GJ_THREADS = 1024;
@@ -649,7 +667,7 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
             for (int s = 0; s < S; s++) A[s] = __dadd_rn(A[s], __shfl_xor_sync(0xffffffffu, A[s], off));
         }
         if (valid && lg == 0) {
-            conv_dig_emit<L>(A, eacc, out.d, out.e, nullptr, out.stride, 0, part, scratch);
+            ts_emit<L>(A, eacc, out.d, out.e, out.stride, part, scratch);
             eout = max(eout, out.e[part * out.stride]);
             if (zl) {  // A is carry-normalised by the emit
                 double o[L];
