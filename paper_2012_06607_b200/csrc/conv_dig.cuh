@@ -46,7 +46,8 @@ constexpr int PADZ = 4;
 __host__ __device__ inline size_t conv_dig_smem(int S, int D, int P, int threads) {
     const size_t per_job = (size_t)2 * S * D + (size_t)2 * (PADZ + S) * D;  // doubles
     return (size_t)P * per_job * sizeof(double) + (size_t)threads * (S + 2) * sizeof(double) +
-           (size_t)P * 2 * D * sizeof(int) + (size_t)2 * P * D * 2 * sizeof(int) + 16;  // + mbarrier
+           (size_t)P * 2 * D * sizeof(int) + (size_t)2 * P * D * 2 * sizeof(int) +
+           (size_t)P * (2 * D + 4) * sizeof(int) + 16;  // + anchor exchange, mbarrier
 }
 
 // ---- TMA bulk copies (cp.async.bulk) with an mbarrier, single CTA ----------
@@ -259,7 +260,8 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
     constexpr int PSTR = S + 2;                               // parking / emit scratch slot
     int *sexp = (int *)(spark + (size_t)blockDim.x * PSTR);   // [P][2 series][D]
     int *szx = sexp + (size_t)P * 2 * D;                      // [2 rounds][P][D][2 parts]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(szx + (size_t)2 * P * D * 2);
+    int *sanc = szx + (size_t)2 * P * D * 2;                  // [P][T][2 outputs][2 parts]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sanc + (size_t)P * (2 * D + 4));
 
     // stage: x -> [S][D][2] (the pool layout), y -> [PADZ + S][D][2] behind
     // PADZ zero rows: two 16-byte aligned contiguous runs per job (every
@@ -303,16 +305,31 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
     // exponent pre-pass (split over the F lanes, max-reduced by shuffles):
     // anchors e_acc of k1 and k2 over ALL their terms (one exponent per
     // complex coefficient: the same anchors for both parts)
+    // complex systems up to L = 8: the two part lanes of a pair take every
+    // other term each and exchange their maxima through shared memory (one
+    // barrier; measured: od -1.4%, qd -2.6%; at L = 10, two blocks per SM,
+    // the barrier costs more than the halved pre-pass saves)
+    constexpr int SPLIT = (NP == 2 && L <= 8) ? 2 : 1;
     int ea1 = ZERO_E, ea2 = ZERO_E;
-    for (int j = f; j <= D; j += F) {
+#pragma unroll 2
+    for (int j = f + (SPLIT == 2 ? part : 0) * F; j <= D; j += SPLIT * F) {
         const bool first = j <= t;
-        const int e = first ? ex[j] + ey[t - j] : ex[D - j] + ey[j - t - 1];  // the pass's term order
-        if (first) ea1 = max(ea1, e);
-        else ea2 = max(ea2, e);
+        const int e = ex[first ? j : D - j] + ey[first ? t - j : j - t - 1];  // the pass's term order
+        ea1 = max(ea1, first ? e : ZERO_E);
+        ea2 = max(ea2, first ? ZERO_E : e);
     }
     for (int off = F >> 1; off > 0; off >>= 1) {
         ea1 = max(ea1, __shfl_xor_sync(0xffffffffu, ea1, off));
         ea2 = max(ea2, __shfl_xor_sync(0xffffffffu, ea2, off));
+    }
+    if (SPLIT == 2) {
+        if (f == 0 && jl < P) {
+            sanc[((jl * T + t) * 2 + 0) * 2 + part] = ea1;
+            sanc[((jl * T + t) * 2 + 1) * 2 + part] = ea2;
+        }
+        __syncthreads();
+        ea1 = max(ea1, sanc[((jlc * T + t) * 2 + 0) * 2 + 1 - part]);
+        ea2 = max(ea2, sanc[((jlc * T + t) * 2 + 1) * 2 + 1 - part]);
     }
     ea1 = max(ea1, ZERO_E);
     ea2 = max(ea2, ZERO_E);
