@@ -478,7 +478,13 @@ def main():
     tprof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_algo{st['algo']}.json")
     if os.path.exists(tprof):
         try:
-            roofline["traffic"] = json.load(open(tprof))["dram_bytes_per_launch"]
+            tp = json.load(open(tprof))
+            roofline["traffic"] = tp["dram_bytes_per_launch"]
+            # DRAM bytes of one whole evaluation (every launch of the step, ncu)
+            # next to its compulsory bytes (inputs, coefficients, outputs once)
+            if "dram_bytes_per_step" in tp:
+                roofline["traffic_per_step"] = tp["dram_bytes_per_step"]
+                roofline["compulsory_bytes_per_step"] = st["compulsory_bytes"]
         except Exception:
             pass
 

@@ -137,3 +137,22 @@ def test_binding_rejects_wrong_buffers():
             sol.solve(jac, vals[:2].contiguous())
         with pytest.raises(mdps.MdpsError, match="jacobian"):
             sol.solve(jac[:2].contiguous(), vals)
+
+
+@pytest.mark.parametrize("L", (3, 8))
+def test_parts_of_very_different_magnitude(L):
+    """DESIGN R20: the digit pool holds both parts of a complex coefficient on
+    the grid of the larger one.  Inputs whose imaginary parts are 2^-200 of
+    their real parts and coefficients whose real parts are 2^-90 of their
+    imaginary parts (exact power-of-two scalings) stay within the md
+    tolerance normwise (the metric R8); purely real inputs give exactly zero
+    imaginary outputs."""
+    si = mdinputs.random_system(770 + L, n=4, monos=5, m_range=(1, 3), exps=(1, 2), degree=9, limbs=L)
+    si.x[:, 1] *= 2.0 ** -200
+    si.coeffs[:, 0] *= 2.0 ** -90
+    full_check(si, L)
+    sr = mdinputs.random_system(780 + L, n=4, monos=5, m_range=(0, 3), exps=(1, 2), degree=9, limbs=L)
+    sr.x[:, 1] = 0.0
+    sr.coeffs[:, 1] = 0.0
+    vals, jac = full_check(sr, L)
+    assert not vals[:, 1].any() and not jac[:, :, 1].any()
