@@ -439,7 +439,8 @@ def main():
     if dist:
         dist.barrier()
     clocks = sampler.stop()
-    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), dist, "cuda")
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = max_over_ranks(sum(step_ms), dist, "cuda")
 
     # a separate instrumented pass (the library records CUDA events around
     # every launch group on the caller's stream) for the per-kernel split and
@@ -474,7 +475,25 @@ def main():
                 "ops_per_launch": conv_ops_per_launch, "avg_launch_ms": conv_launch_ms,
                 "share_of_step": tim["conv_ms"] / max(1e-9, tim["conv_ms"] + tim["accum_ms"] + tim["convert_ms"]),
                 "timing": "separate instrumented pass of the same steps (CUDA events around each launch group)",
-                "peak_source": f"{n_sm} SMs x 64 FP64 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"}
+                "peak_source": f"{n_sm} SMs x 64 FP64 lanes x {sm_max:.0f} MHz (MEASURED_PEAKS sm_max_mhz)",
+                # the same rate with an FMA counted as 2 FLOPs (every algorithmic
+                # instruction of the digit kernel is a DFMA), against 2 x peak
+                "fma_as_2_tflops": 2 * achieved / 1e12 if st["algo"] == 2 else None,
+                "fma_as_2_peak_tflops": 2 * peak_nominal / 1e12,
+                # compulsory bytes (x, coefficients, outputs once) per step over the step time
+                "compulsory_gbs": st["compulsory_bytes"] / (ms / args.steps * 1e-3) / 1e9}
+    # executed FP64 instructions per product (ncu hardware counters, one
+    # launch, profiles/r02_fp64_counts.json) next to the algorithmic count W
+    cprof = os.path.join(ROOT, "profiles", "r02_fp64_counts.json")
+    if os.path.exists(cprof) and st["algo"] == 2:
+        try:
+            for c in json.load(open(cprof))["launches"]:
+                if c["config"] == args.config:
+                    roofline["executed_fp64_per_product_ncu"] = (c["dfma_executed"] + c["dadd_executed"] +
+                                                                 c["dmul_executed"]) / c["jobs"]
+                    roofline["algorithmic_fp64_per_product"] = c["W_algorithmic_dfma"] / c["jobs"]
+        except Exception:
+            pass
     tprof = os.path.join(ROOT, "profiles", f"traffic_{args.config}_algo{st['algo']}.json")
     if os.path.exists(tprof):
         try:
@@ -535,7 +554,8 @@ def main():
         line = {
             "metric": METRIC,
             "value": value, "unit": "products/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "ms_median": statistics.median(step_ms), "ms_min": min(step_ms), "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": bench_config(si_full, args.config, world, sharded),
             "schedule": {"algo": {1: "eft", 2: "digits"}[st["algo"]], "digits": st["digits"],

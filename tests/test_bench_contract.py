@@ -50,6 +50,7 @@ def test_gpu_arm_line():
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in r, k
     assert 0 < r["frac"] < 1 and abs(r["achieved"] / r["peak"] - r["frac"]) < 1e-9
+    assert 0 < d["ms_min"] <= d["ms_median"] and r["compulsory_gbs"] > 0 and r["fma_as_2_peak_tflops"] > r["peak"]
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     c = d["cpu_baseline"]
