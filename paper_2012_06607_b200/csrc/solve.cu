@@ -601,11 +601,15 @@ struct Seg {
     const int *xe;
 };
 
+// pbeg, pend: the output parts this group computes — both (0, 2), or one
+// when the task is split over two groups, one per part (the latency-bound
+// substitution loop: the dependent task takes one pass instead of two).
 template <int L, int SE = digits_for(L)>
 __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const int *__restrict__ aexp,
                                        const double *xs, const int *xe, int n, int lg, int G, bool valid,
                                        DigRef init, bool one, DigOut out, double *zl, int lstride,
-                                       double *scratch, Seg seg2 = Seg{nullptr, nullptr, nullptr, nullptr}) {
+                                       double *scratch, Seg seg2 = Seg{nullptr, nullptr, nullptr, nullptr},
+                                       int pbeg = 0, int pend = 2) {
     constexpr int S = digits_for(L);
     int ea0 = ZERO_E, ea1 = ZERO_E;
     if (valid) {
@@ -634,7 +638,7 @@ __device__ __forceinline__ int ts_task(const double *__restrict__ arow, const in
     }
     int eout = ZERO_E;
 #pragma unroll 1
-    for (int part = 0; part < 2; part++) {
+    for (int part = pbeg; part < pend; part++) {
         const int eacc = max(part ? ea1 : ea0, ZERO_E);
         int eI = ZERO_E;
         if (valid && lg == 0 && init.d) {  // fetch the init digits early (they land during the pass)
@@ -985,7 +989,9 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
         const int tidd = ((int)blockIdx.x - b0) * blockDim.x + threadIdx.x;
         const int T = pair ? 2 * n : n;
         const int G = pick_group(T, pair ? 2 * N : N, nthd);
-        const int ng = nthd / G, g = tidd / G, lg = tidd % G;
+        // one group of G lanes per output part (2G lanes per task)
+        const int G2 = 2 * G;
+        const int ng = nthd / G2, g = tidd / G2, lg = tidd % G, pt = (tidd % G2) / G;
         double *X0 = xbuf(j, 0), *X1 = xbuf(j, 1);
         int *E0 = xebuf(j, 0), *E1 = xebuf(j, 1);
         for (int base = 0; base < T; base += ng) {
@@ -997,11 +1003,12 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
             const int *wre = Wre + (size_t)pp * 2 * N;
             if (!second)
                 ts_task<L>(wr, wre, xs, xe, N, lg, G, valid, none, false, DigOut{X0 + pp, E0 + pp, n},
-                           dx + (size_t)pp * 2 * L * D + j, D, scratch);
+                           dx + (size_t)pp * 2 * L * D + j, D, scratch, Seg{nullptr, nullptr, nullptr, nullptr},
+                           pt, pt + 1);
             else
                 ts_task<L>(wr, wre, xs1, xe1, N, lg, G, valid, none, false, DigOut{X1 + pp, E1 + pp, n},
                            dx + (size_t)pp * 2 * L * D + j + 1, D, scratch,
-                           Seg{Mr + (size_t)pp * VM, Mre + (size_t)pp * 2 * N, xs, xe});
+                           Seg{Mr + (size_t)pp * VM, Mre + (size_t)pp * 2 * N, xs, xe}, pt, pt + 1);
         }
     };
     dx_phase(0, 0);
@@ -1011,7 +1018,14 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
         // r_k -= A_{k-j} dx_j + A_{k-j-1} dx_{j+1}, k = j+2..d
         const int T = (D - 2 - j) * N;
         const int G = pick_group(T, 2 * n, nth);
-        const int ng = nth / G, g = tid / G, lg = tid % G;
+        // one group of G lanes per output part once the tasks fit about three
+        // sweeps that way (the latency-bound later pairs: the dependent task
+        // takes one pass instead of two); both parts per group while the
+        // updates are throughput-bound (measured, od: splitting every pair
+        // slows the early ones 100 -> 120 us, speeds the late ones 80 -> 58)
+        const bool split = (long long)T * 2 * G <= 3LL * nth;
+        const int G2 = split ? 2 * G : G;
+        const int ng = nth / G2, g = tid / G2, lg = tid % G, pt = split ? (tid % G2) / G : 0;
         const int nnext = j + 3 < D ? 2 * N : N;  // tasks of r_{j+2}, r_{j+3}
         // the dx blocks of the next pair: the last ones, disjoint from the
         // blocks holding the r_{j+2}, r_{j+3} tasks
@@ -1019,10 +1033,10 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
         const int Tdx = pair2 ? 2 * n : n, lendx = pair2 ? 2 * N : N;
         int nbdx = 0;
         {
-            const int Gd = pick_group(Tdx, lendx, nth);  // upper bound of the subset's group width
+            const int Gd = 2 * pick_group(Tdx, lendx, nth);  // upper bound of the subset's group width (2 parts)
             nbdx = (int)(((long long)Tdx * Gd + blockDim.x - 1) / blockDim.x);
         }
-        const int rblocks = (int)(((long long)nnext * G + blockDim.x - 1) / blockDim.x);
+        const int rblocks = (int)(((long long)nnext * G2 + blockDim.x - 1) / blockDim.x);
         const bool overlap = ng >= nnext && rblocks + nbdx <= (int)gridDim.x;
         const int b0 = (int)gridDim.x - nbdx;
         ts_stage<L>(xbuf(j, 0), xebuf(j, 0), n, 1, xs, xe);
@@ -1036,13 +1050,14 @@ __global__ void __launch_bounds__(main_threads(L), L == 10 ? 1 : 3) ts_main_kern
             double *rk = Rp + (size_t)k * VM + p;
             int *rke = Re + (size_t)k * 2 * N + p;
             ts_task<L>(Ad + row0 * VN, Ae + row0 * 2 * n, xs, xe, n, lg, G, valid, DigRef{rk, rke, N}, false,
-                       DigOut{rk, rke, N}, nullptr, 0, scratch, Seg{Ad + row1 * VN, Ae + row1 * 2 * n, xs1, xe1});
-            if (overlap && valid && lg == 0 && task < nnext) {  // r_{j+2} / r_{j+3} entry final
+                       DigOut{rk, rke, N}, nullptr, 0, scratch, Seg{Ad + row1 * VN, Ae + row1 * 2 * n, xs1, xe1},
+                       split ? pt : 0, split ? pt + 1 : 2);
+            if (overlap && valid && lg == 0 && task < nnext) {  // r_{j+2} / r_{j+3} entry part final
                 __threadfence();
                 atomicAdd(&ctl->rdy, 1u);
             }
         }
-        rdy_target += overlap ? (unsigned)nnext : 0u;
+        rdy_target += overlap ? (split ? 2u : 1u) * (unsigned)nnext : 0u;  // one signal per group
         if (overlap && (int)blockIdx.x >= b0) {
             __syncthreads();  // this block's update tasks no longer read xs / xs1
             if (threadIdx.x == 0) {
