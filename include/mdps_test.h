@@ -41,13 +41,14 @@ int mdps_test_digits_roundtrip(const double *x, double *y, int32_t count, int32_
 int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t stream);
 
 /* Launch-geometry override of the digit product kernel (tuning only): F
- * lanes per output pair, P jobs per block and NP part lanes (1: the real and
- * imaginary passes run one after the other on each thread; 2: one thread per
- * part, twice the threads per job) for every later launch in this process;
- * 0 = the model's / the tuned table's choice (the default).  F in
- * {0,1,2,4,8}, P a power of two <= 32, NP in {0,1,2}; MDPS_EINVAL otherwise,
- * and at launch when the geometry does not fit the kernel's thread /
- * shared-memory limits (or NP = 2 on a real system).  Not thread-safe. */
+ * lanes per output pair, P jobs per block and NP lane sets per job of a
+ * complex system (1: both parts of an output on one thread, the fused-parts
+ * kernel, where it exists — L <= 5, else ignored; 2: one lane set per part,
+ * twice the threads per job) for every later launch in this process; 0 =
+ * the model's / the tuned table's choice (the default).  F in {0,1,2,4,8}, P
+ * a power of two <= 32, NP in {0,1,2}; MDPS_EINVAL otherwise, and at launch
+ * when the geometry does not fit the kernel's thread / shared-memory limits.
+ * Real systems always run one lane set.  Not thread-safe. */
 int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP);
 
 /* Per-kernel timing of mdps_eval_diff (measurement only): when enabled, each

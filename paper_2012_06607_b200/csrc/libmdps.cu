@@ -13,6 +13,7 @@
 #include "../../include/libmdps.h"
 #include "../../include/mdps_test.h"
 #include "conv_dig.cuh"
+#include "conv_dig_fused.cuh"
 #include "kernels_dig.cuh"
 #include "kernels_eft.cuh"
 #include "queue_eft.cuh"
@@ -104,13 +105,20 @@ static const int kTunedGeomReal[][4] = {
     {10, 64, 2, 1},
 };
 
+// The same for the fused-parts kernel (conv_dig_fused.cuh, complex systems).
+// (profiles/r02_tune_fused.json; D = 128 runs the model's choice, F = 2, P = 1)
+static const int kTunedGeomFused[][4] = {
+    {2, 16, 2, 8}, {2, 32, 2, 4}, {2, 64, 2, 2}, {3, 16, 2, 2}, {3, 32, 2, 1}, {3, 64, 2, 1},
+    {4, 16, 2, 4}, {4, 32, 2, 2}, {4, 64, 2, 1}, {5, 16, 2, 2}, {5, 32, 2, 1}, {5, 64, 2, 1},
+};
+
 // real: the real-system kernel (one part lane set) and its table; tuned:
 // use the table; forceF/P > 0 restrict the search to that F / P
 static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool real, int forceF = 0,
-                        int forceP = 0, bool tuned = false) {
+                        int forceP = 0, bool tuned = false, bool fused = false) {
     const int S = digits_for(L);
     const int T = (D + 1) / 2;
-    const int NP = real ? 1 : 2;
+    const int NP = (real || fused) ? 1 : 2;  // lane sets per job (fused: both parts on one thread)
     DigGeom best{T, 1, 1, 32, 0, NP};
     double best_score = -1.0;
     if (tuned && forceF == 0 && forceP == 0) {
@@ -121,7 +129,8 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool
                     forceP = t[3];
                 }
         };
-        if (real) pick(kTunedGeomReal);
+        if (fused) pick(kTunedGeomFused);
+        else if (real) pick(kTunedGeomReal);
         else pick(kTunedGeom);
     }
     // resident warps count up to 16 per SM; measured (profiles/r01_sweep.json
@@ -139,7 +148,7 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool
             g.NP = NP;
             g.threads = NP * ((P * T * F + 31) / 32 * 32);  // each part's lane set whole warps
             if (g.threads > max_threads) continue;
-            g.smem = conv_dig_smem(S, D, P, g.threads);
+            g.smem = fused ? conv_fused_smem(S, D, P, g.threads) : conv_dig_smem(S, D, P, g.threads);
             if (g.smem > 227 * 1024) continue;
             const int blocks_smem = (int)(228 * 1024 / (g.smem + 1024));
             const int blocks_regs = 65536 / (std::max(regs_per_thread, 32) * g.threads);
@@ -174,6 +183,30 @@ struct ConvEft {
     }
 };
 
+// fused-parts kernel (conv_dig_fused.cuh): complex systems with few digits.
+// mode: 0 = never (part lanes), 1 = where measured faster (default), 2 = always
+// where the kernel exists (L <= 5); mdps_test_force_geometry's NP = 1 / 2
+static int g_fused_mode = 1;
+static bool fused_default(int L, int D) {
+    (void)D;
+    return L <= 5;
+}
+
+template <int L, bool HAS_FUSED = (L <= 5)>
+struct FusedKern {
+    using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
+    static KernT get(int) { return nullptr; }
+};
+template <int L>
+struct FusedKern<L, true> {
+    using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
+    static KernT get(int D) {
+        return D == 16 ? conv_fused_kernel<L, 16> : D == 32 ? conv_fused_kernel<L, 32>
+             : D == 64 ? conv_fused_kernel<L, 64> : D == 128 ? conv_fused_kernel<L, 128>
+             : conv_fused_kernel<L, 0>;
+    }
+};
+
 template <int L>
 struct ConvDig {
     static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, int real,
@@ -181,19 +214,22 @@ struct ConvDig {
         if (njobs <= 0) return MDPS_OK;
         using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
         KernT kern;
-        if (real)  // real systems: one part, one product per term
+        const bool fused = !real && L <= 5 && (g_fused_mode == 2 || (g_fused_mode == 1 && fused_default(L, D)));
+        if (fused)  // complex systems, few digits: both parts of an output on one thread
+            kern = FusedKern<L>::get(D);
+        else if (real)  // real systems: one part, one product per term
             kern = D == 16 ? conv_dig_kernel<L, 16, true> : D == 32 ? conv_dig_kernel<L, 32, true>
                  : D == 64 ? conv_dig_kernel<L, 64, true> : D == 128 ? conv_dig_kernel<L, 128, true>
                  : conv_dig_kernel<L, 0, true>;
         else
             kern = D == 16 ? conv_dig_kernel<L, 16> : D == 32 ? conv_dig_kernel<L, 32> : D == 64 ? conv_dig_kernel<L, 64>
                  : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
-        // geometry per (D, real), computed once per process under a lock
+        // geometry per (D, kernel), computed once per process under a lock
         static std::mutex mu;
-        static DigGeom cache[2 * 257];
-        static int cregs[2 * 257], cmaxt[2 * 257];
-        static bool cached[2 * 257];
-        const int key = D + (real ? 257 : 0);
+        static DigGeom cache[3 * 257];
+        static int cregs[3 * 257], cmaxt[3 * 257];
+        static bool cached[3 * 257];
+        const int key = D + (fused ? 2 * 257 : real ? 257 : 0);
         DigGeom g;
         int regs, maxt;
         {
@@ -208,21 +244,17 @@ struct ConvDig {
                 }
                 cregs[key] = regs;
                 cmaxt[key] = maxt;
-                cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, true);
+                cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, true, fused);
                 if (cache[key].smem == 0)  // tuned entry does not fit
-                    cache[key] = dig_geom(L, D, regs, maxt, real != 0);
+                    cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, false, fused);
                 cached[key] = true;
             }
             g = cache[key];
             regs = cregs[key];
             maxt = cmaxt[key];
         }
-        if (g_force_F > 0 || g_force_P > 0 || g_force_NP > 0) {  // tuning: a forced (F, P), checked
-            if (g_force_NP > 0 && g_force_NP != (real ? 1 : 2)) {
-                set_err("forced geometry: complex systems run one lane set per part (NP = 2), real ones NP = 1");
-                return MDPS_EINVAL;
-            }
-            g = dig_geom(L, D, regs, maxt, real != 0, g_force_F, g_force_P);
+        if (g_force_F > 0 || g_force_P > 0) {  // tuning: a forced (F, P), checked
+            g = dig_geom(L, D, regs, maxt, real != 0, g_force_F, g_force_P, false, fused);
             if (g.smem == 0) { set_err("forced geometry does not fit"); return MDPS_EINVAL; }
         }
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
@@ -1064,6 +1096,7 @@ extern "C" int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP) {
     g_force_F = F;
     g_force_P = P;
     g_force_NP = NP;
+    g_fused_mode = NP == 1 ? 2 : (NP == 2 ? 0 : 1);
     return MDPS_OK;
 }
 

@@ -62,6 +62,7 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/sweep.json")
     ap.add_argument("--eft", action="store_true", help="also time MDPS_ALGO_EFT")
+    ap.add_argument("--l2-both", action="store_true", help="the L = 2 cells also under the algorithm AUTO does not pick")
     a = ap.parse_args()
     res = []
     for name in ("dd", "qd", "od", "deca"):
@@ -73,4 +74,10 @@ if __name__ == "__main__":
         for L in mdinputs.SWEEP_LIMBS:
             res.append(measure(mdinputs.sweep_cell(d, L)))
             print(json.dumps(res[-1]), flush=True)
+            if a.l2_both and L == 2:
+                other = mdps.MDPS_ALGO_DIGITS if res[-1]["algo"] == mdps.MDPS_ALGO_EFT else mdps.MDPS_ALGO_EFT
+                r = measure(mdinputs.sweep_cell(d, L), algo=other)
+                r["cell"] += "_other_algo"
+                res.append(r)
+                print(json.dumps(r), flush=True)
     json.dump(res, open(a.out, "w"), indent=1)

@@ -1,10 +1,11 @@
 """The digit product kernel under every launch geometry that fits
-(mdps_test_force_geometry: F lanes per output pair x P jobs per block; one
-lane set per part),
-including F > D + 1 (lanes without terms), odd D (the generic-D build, scalar
-staging) and several jobs per block: every geometry matches the oracle within
-the tolerance, and the tuned defaults are among them; a complex system
-rejects NP = 1."""
+(mdps_test_force_geometry: F lanes per output pair x P jobs per block; NP = 2
+one lane set per part, NP = 1 both parts on one thread — the fused-parts
+kernel of L <= 5), including F > D + 1 (lanes without terms), odd D (the
+generic-D build) and several jobs per block: every geometry matches the
+oracle within the tolerance, and the tuned defaults are among them; the
+fused-parts kernel and the part-lane kernel give the same bits (both
+accumulate exactly and round once)."""
 import numpy as np
 import pytest
 
@@ -14,7 +15,7 @@ from tests.gpu_util import TOL
 
 pytestmark = pytest.mark.gpu
 
-GEOMS = [(f, p, 2) for f in (1, 2, 4, 8) for p in (1, 2, 4)]  # complex: one lane set per part
+GEOMS = [(f, p, q) for q in (2, 1) for f in (1, 2, 4, 8) for p in (1, 2, 4)]
 
 
 @pytest.mark.parametrize("L,degree", [(2, 6), (4, 15), (8, 31), (10, 15), (3, 63)])
@@ -44,15 +45,24 @@ def test_every_fitting_geometry_matches_the_oracle(L, degree):
     assert ran >= 3
 
 
-def test_complex_systems_reject_one_lane_set():
+@pytest.mark.parametrize("L,degree", [(2, 9), (3, 15), (4, 31), (4, 12), (5, 63), (5, 127)])
+def test_fused_parts_kernel_equals_the_part_lane_kernel_bitwise(L, degree):
     import torch
     import paper_2012_06607_b200 as mdps
-    si = mdinputs.random_system(950, n=3, monos=3, m_range=(1, 3), exps=(1,), degree=7, limbs=4)
+    si = mdinputs.random_system(950 + L + degree, n=4, monos=5, m_range=(1, 4), exps=(1, 2), degree=degree,
+                                limbs=L)
     with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS) as s:
         x = torch.from_numpy(si.x).cuda()
+        outs = {}
         try:
-            mdps.force_geometry(2, 1, 1)
-            with pytest.raises(mdps.MdpsError, match="NP = 2"):
-                s.eval_diff(x)
+            for q in (2, 1):
+                for f in (1, 2):
+                    mdps.force_geometry(f, 0, q)
+                    v, j = s.eval_diff(x)
+                    torch.cuda.synchronize()
+                    outs[(q, f)] = (v.cpu().numpy(), j.cpu().numpy())
         finally:
             mdps.force_geometry(0, 0, 0)
+    ref = outs[(2, 1)]
+    for key, (v, j) in outs.items():
+        assert np.array_equal(v, ref[0]) and np.array_equal(j, ref[1]), key
