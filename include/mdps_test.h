@@ -51,6 +51,14 @@ int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t stream);
  * Real systems always run one lane set.  Not thread-safe. */
 int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP);
 
+/* Programmatic dependent launch of the digit product levels (measurement
+ * only): 1 (default) = each level's kernel is launched with the
+ * programmatic-stream-serialization attribute, so its blocks are scheduled
+ * while the previous level drains and wait for it (griddepcontrol.wait)
+ * before reading the pools; 0 = plain stream order.  Results are identical.
+ * Applies to later launches in this process.  Not thread-safe. */
+int mdps_test_set_pdl(int32_t enable);
+
 /* Per-kernel timing of mdps_eval_diff (measurement only): when enabled, each
  * launch group is bracketed by CUDA events on the caller's stream (the CUDA
  * graph path is bypassed while enabled).  mdps_system_timing synchronises

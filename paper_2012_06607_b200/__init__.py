@@ -35,7 +35,7 @@ EXPORTED_SYMBOLS = (
     "mdps_system_create", "mdps_system_create_ex", "mdps_eval_diff", "mdps_eval_diff_host",
     "mdps_system_destroy", "mdps_last_error", "mdps_system_stats", "mdps_system_level_jobs",
     "mdps_test_series_mul", "mdps_test_md_op", "mdps_test_norm2sq", "mdps_test_digits_roundtrip",
-    "mdps_fp64_peak", "mdps_test_force_geometry", "mdps_system_set_timing", "mdps_system_timing",
+    "mdps_fp64_peak", "mdps_test_force_geometry", "mdps_test_set_pdl", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
     "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls", "mdps_test_queue_trace",
     "mdps_test_queue_config", "mdps_solver_flags", "mdps_test_plan",
@@ -117,6 +117,7 @@ def lib() -> ctypes.CDLL:
     L.mdps_test_digits_roundtrip.argtypes = [vp, vp, i32, i32, i32, vp]
     L.mdps_fp64_peak.argtypes = [i64, P(ctypes.c_double), vp]
     L.mdps_test_force_geometry.argtypes = [i32, i32, i32]
+    L.mdps_test_set_pdl.argtypes = [i32]
     L.mdps_system_set_timing.argtypes = [vp, i32]
     L.mdps_system_timing.argtypes = [vp, P(Timing), i32]
     L.mdps_solver_create.restype = vp
@@ -496,6 +497,11 @@ def queue_config(max_blocks: int = 0, lanes: int = 0) -> None:
 def force_geometry(F: int = 0, P: int = 0, NP: int = 0) -> None:
     """Tuning only: force the digit product kernel's (F, P, NP); 0, 0, 0 = the default."""
     _check(lib().mdps_test_force_geometry(F, P, NP), "mdps_test_force_geometry")
+
+
+def set_pdl(enable: bool = True) -> None:
+    """Measurement only: programmatic dependent launch of the digit product levels (default on)."""
+    _check(lib().mdps_test_set_pdl(1 if enable else 0), "mdps_test_set_pdl")
 
 
 def fp64_peak(iters: int = 20000, stream=None) -> float:

@@ -83,6 +83,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
         : "memory");
 }
 
+// programmatic dependent launch (griddepcontrol): no-ops in a launch without
+// the programmatic-serialization attribute
+__device__ __forceinline__ void grid_dep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // one product pass over this thread's fold iterations for part PART (0: re,
 // 1: im).  REAL: real series (imaginary digits zero and never read): one
 // product per term.
@@ -268,7 +273,16 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
     // slot and row is a multiple of 16 bytes), so one thread issues two TMA
     // bulk copies (cp.async.bulk) per job against an mbarrier while the
     // other warps write the zero rows and exponents
+    // programmatic dependent launch: the next level's blocks may be scheduled
+    // as this level's blocks drain; nothing a previous launch wrote (digit and
+    // exponent pools) is read before grid_dep_wait() — the job list is static
+    grid_dep_launch_dependents();
     if (threadIdx.x == 0) mbar_init(bar, 1);
+    for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {  // zero rows
+        const int jl = idx / (2 * PADZ * D), r = idx - jl * 2 * PADZ * D;
+        sdig[(size_t)jl * (SX + SY) + SX + r] = 0.0;
+    }
+    grid_dep_wait();
     __syncthreads();
     if (threadIdx.x < 32) {
         if (threadIdx.x == 0) mbar_expect_tx(bar, (unsigned)(P * 2 * SX * 8));
@@ -279,10 +293,6 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
             double *base = sdig + (size_t)jl * (SX + SY) + (which ? SX + 2 * PADZ * D : 0);
             bulk_g2s(base, dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D), (unsigned)(SX * 8), bar);
         }
-    }
-    for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {  // zero rows
-        const int jl = idx / (2 * PADZ * D), r = idx - jl * 2 * PADZ * D;
-        sdig[(size_t)jl * (SX + SY) + SX + r] = 0.0;
     }
     for (int idx = threadIdx.x; idx < P * 2 * D; idx += blockDim.x) {
         const int jl = idx / (2 * D), r = idx - jl * 2 * D;

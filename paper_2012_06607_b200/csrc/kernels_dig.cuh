@@ -79,18 +79,22 @@ __device__ __forceinline__ double radix_pow(int q) {
 __device__ __forceinline__ double rint_magic(double x) { return __dsub_rn(__dadd_rn(x, MAGIC), MAGIC); }
 
 // One parallel carry pass (exact): every digit t >= 1 hands rint(A_t / R) to
-// digit t-1 at once — S independent 5-instruction chains instead of one
-// serial chain.  From |A_t| < 2^53 one pass leaves |A_t| <= R/2 + 2^31, a
-// second <= R/2 + 2^9, a third <= R/2 + 1.
+// digit t-1 at once — S independent 4-instruction chains instead of one
+// serial chain.  q = (A_t + 1.5 2^52 R) - 1.5 2^52 R is A_t rounded to the
+// nearest multiple of R (ties to even; exact for |A_t| < 2^51 R), so the
+// carry costs two additions, one subtraction and one FMA per digit.  From
+// |A_t| < 2^53 one pass leaves |A_t| <= R/2 + 2^31, a second <= R/2 + 2^9, a
+// third <= R/2 + 1.
 template <int N>
 __device__ __forceinline__ void carry_pass(double (&A)[N]) {
+    constexpr double MAGIC_R = MAGIC * RADIX;
     double q[N];
 #pragma unroll
-    for (int t = N - 1; t >= 1; t--) q[t] = rint_magic(__dmul_rn(A[t], INV_RADIX));
+    for (int t = N - 1; t >= 1; t--) q[t] = __dsub_rn(__dadd_rn(A[t], MAGIC_R), MAGIC_R);
 #pragma unroll
     for (int t = N - 1; t >= 1; t--) {
-        A[t] = __fma_rn(-q[t], RADIX, A[t]);
-        A[t - 1] = __dadd_rn(A[t - 1], q[t]);
+        A[t] = __dsub_rn(A[t], q[t]);
+        A[t - 1] = __fma_rn(q[t], INV_RADIX, A[t - 1]);
     }
 }
 

@@ -95,26 +95,51 @@ __global__ void __launch_bounds__(128) conv_eft_kernel(double *__restrict__ pool
     }
 }
 
-// tasks [task0, task0 + ntasks) of [0, n) values_out, [n, n + n*n) jacobian_out (row-major)
+// B += the bins of another partial sum (level o at level o; guard plainly)
 template <int L>
-__global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict__ pool,
-                                                       const int *__restrict__ task_ptr,
-                                                       const int *__restrict__ ent_slot,
-                                                       const int *__restrict__ ent_w, int task0, int ntasks,
-                                                       int n, int D, double *__restrict__ values,
-                                                       double *__restrict__ jac) {
+__device__ __forceinline__ void bins_merge(double (&B)[L + 1], const double (&C)[L + 1]) {
+#pragma unroll
+    for (int o = 0; o < L; o++) {
+        double v = C[o];
+#pragma unroll
+        for (int t = o; t < L; t++) two_sum(B[t], v, B[t], v);
+        B[L] = __dadd_rn(B[L], v);
+    }
+    B[L] = __dadd_rn(B[L], C[L]);
+}
+
+// lanes per (addition job, coefficient): a value sums one series per monomial
+// of its polynomial (64..128 entries in the configs), a Jacobian entry one per
+// monomial that contains its variable (8..24) — one thread per output would
+// run the value jobs' chains (entries x one dependent md addition) long after
+// the Jacobian jobs are done.  Fixed per job type and (L, D), so the summation
+// order of an output never depends on the system it is part of (shards and
+// batches stay bitwise equal to the whole).  Jacobian jobs of long, wide
+// series (L D >= 512) fill the GPU on one lane each and are throughput-bound:
+// a second lane only adds its merge (measured: deca 0.88 -> 1.01 ms with two).
+constexpr int ACCUM_LANES_VALUE = 8;
+__host__ __device__ constexpr int accum_lanes_jac(int L, int D) { return L * D >= 512 ? 1 : 2; }
+
+// one addition job's coefficient k on G adjacent lanes: lane g sums entries
+// e0 + g, e0 + g + G, ... in order, then the lanes' bins are merged pairwise
+// in a fixed tree (lane g takes lane g + off's bins, off = 1, 2, 4, ...), and
+// lane 0 renormalises and stores.  Deterministic: no atomics, fixed order.
+// Structural zeros (no entries) are written as exact zeros.
+// `active` false: a padding thread (it still takes part in the shuffles).
+template <int L, int G>
+__device__ __forceinline__ void accum_lanes(const double *__restrict__ pool, const int *__restrict__ task_ptr,
+                                            const int *__restrict__ ent_slot, const int *__restrict__ ent_w,
+                                            int task, int k, int g, bool active, int n, int D,
+                                            double *__restrict__ values, double *__restrict__ jac) {
     const int LD2 = 2 * L * D;
-    const long long g = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= (long long)ntasks * D) return;
-    const int task = task0 + (int)(g / D), k = (int)(g % D);
     double Br[L + 1], Bi[L + 1];
     md_zero(Br);
     md_zero(Bi);
-    // software pipeline over the entries: entry e+1's limbs (and e+2's slot
-    // index) are loaded while entry e is summed — the loop is bound by the
-    // chained loads (slot index, then limbs), not by the bins arithmetic
-    const int e0 = task_ptr[task], e1 = task_ptr[task + 1];
-    auto load = [&](int e, double (&ar)[L], double (&ai)[L], int slot) {
+    // software pipeline over the lane's entries: entry e+G's limbs (and
+    // e+2G's slot index) are loaded while entry e is summed — the loop is
+    // bound by the chained loads (slot index, then limbs), not by the bins
+    const int e0 = active ? task_ptr[task] + g : 0, e1 = active ? task_ptr[task + 1] : 0;
+    auto load = [&](double (&ar)[L], double (&ai)[L], int slot) {
         const double *s = pool + (size_t)slot * LD2;
 #pragma unroll
         for (int p = 0; p < L; p++) {
@@ -125,17 +150,17 @@ __global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict
     double ar[L], ai[L];
     int w = 0, slot_next = 0;
     if (e0 < e1) {
-        load(e0, ar, ai, ent_slot[e0]);
+        load(ar, ai, ent_slot[e0]);
         w = ent_w[e0];
-        if (e0 + 1 < e1) slot_next = ent_slot[e0 + 1];
+        if (e0 + G < e1) slot_next = ent_slot[e0 + G];
     }
-    for (int e = e0; e < e1; e++) {
+    for (int e = e0; e < e1; e += G) {
         double nr[L], ni[L];
         int nw = 0, slot_nn = 0;
-        if (e + 1 < e1) {
-            load(e + 1, nr, ni, slot_next);
-            nw = ent_w[e + 1];
-            if (e + 2 < e1) slot_nn = ent_slot[e + 2];
+        if (e + G < e1) {
+            load(nr, ni, slot_next);
+            nw = ent_w[e + G];
+            if (e + 2 * G < e1) slot_nn = ent_slot[e + 2 * G];
         }
         if (w == 1) {
             bins_add<L>(Br, ar);
@@ -152,6 +177,18 @@ __global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict
         w = nw;
         slot_next = slot_nn;
     }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+        double Cr[L + 1], Ci[L + 1];
+#pragma unroll
+        for (int p = 0; p <= L; p++) {
+            Cr[p] = __shfl_down_sync(0xffffffffu, Br[p], off);
+            Ci[p] = __shfl_down_sync(0xffffffffu, Bi[p], off);
+        }
+        bins_merge<L>(Br, Cr);  // only lanes with g % (2 off) == 0 carry the result on
+        bins_merge<L>(Bi, Ci);
+    }
+    if (!active || g != 0) return;
     double zr[L], zi[L];
     md_renorm(Br, zr);
     md_renorm(Bi, zi);
@@ -160,6 +197,33 @@ __global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict
     for (int p = 0; p < L; p++) {
         o[p * D + k] = zr[p];
         o[(L + p) * D + k] = zi[p];
+    }
+}
+
+// Addition jobs of one chunk in one launch: the value jobs [v0, v0 + nv) on
+// ACCUM_LANES_VALUE lanes per coefficient (blocks [0, vblocks)), the Jacobian
+// jobs [j0, j0 + nj) on GJ = accum_lanes_jac(L, D) (the other blocks); tasks [0, n) are
+// values_out, [n, n + n*nvars) jacobian_out (row-major).  Threads of a job
+// type: [job][coefficient k][lane g].
+template <int L, int GJ>
+__global__ void __launch_bounds__(128) accum_eft_kernel(const double *__restrict__ pool,
+                                                       const int *__restrict__ task_ptr,
+                                                       const int *__restrict__ ent_slot,
+                                                       const int *__restrict__ ent_w, int v0, int nv, int vblocks,
+                                                       int j0, int nj, int n, int D, double *__restrict__ values,
+                                                       double *__restrict__ jac) {
+    if ((int)blockIdx.x < vblocks) {
+        constexpr int G = ACCUM_LANES_VALUE;
+        const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        const long long job = t / ((long long)D * G);
+        const int r = (int)(t - job * D * G);
+        accum_lanes<L, G>(pool, task_ptr, ent_slot, ent_w, v0 + (int)job, r / G, r % G, job < nv, n, D, values, jac);
+    } else {
+        constexpr int G = GJ;
+        const long long t = (long long)(blockIdx.x - vblocks) * blockDim.x + threadIdx.x;
+        const long long job = t / ((long long)D * G);
+        const int r = (int)(t - job * D * G);
+        accum_lanes<L, G>(pool, task_ptr, ent_slot, ent_w, j0 + (int)job, r / G, r % G, job < nj, n, D, values, jac);
     }
 }
 

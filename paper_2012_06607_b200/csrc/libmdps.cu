@@ -187,6 +187,7 @@ struct ConvEft {
 // mode: 0 = never (part lanes), 1 = where measured faster (default), 2 = always
 // where the kernel exists (L <= 5); mdps_test_force_geometry's NP = 1 / 2
 static int g_fused_mode = 1;
+static int g_pdl = 1;  // programmatic dependent launch of the digit product levels (mdps_test_set_pdl)
 static bool fused_default(int L, int D) {
     (void)D;
     return L <= 5;
@@ -259,7 +260,21 @@ struct ConvDig {
         }
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
-        kern<<<blocks, g.threads, g.smem, st>>>(dpool, epool, lpool, jobs, njobs, D, g.T, g.F, g.P);
+        // programmatic dependent launch: this level's blocks may be scheduled
+        // while the previous kernel of the stream drains (they wait for its
+        // completion before touching the pools: grid_dep_wait in the kernel)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)blocks);
+        cfg.blockDim = dim3((unsigned)g.threads);
+        cfg.dynamicSmemBytes = g.smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = g_pdl ? 1 : 0;
+        int T = g.T, F = g.F, P = g.P;
+        CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, dpool, epool, lpool, jobs, njobs, D, T, F, P), MDPS_ECUDA);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -315,13 +330,16 @@ struct QueueGeomFn {
 
 template <int L>
 struct AccumEft {
-    // addition jobs [task0, task0 + ntasks)
-    static int run(const double *pool, const int *tp, const int *es, const int *ew, int task0, int ntasks, int n,
-                   int D, double *values, double *jac, cudaStream_t st) {
-        if (ntasks <= 0) return MDPS_OK;
-        const long long total = (long long)ntasks * D;
-        const int blocks = (int)((total + 127) / 128);
-        accum_eft_kernel<L><<<blocks, 128, 0, st>>>(pool, tp, es, ew, task0, ntasks, n, D, values, jac);
+    // addition jobs: values [v0, v0 + nv) and Jacobian entries [j0, j0 + nj), one launch
+    static int run(const double *pool, const int *tp, const int *es, const int *ew, int v0, int nv, int j0, int nj,
+                   int n, int D, double *values, double *jac, cudaStream_t st) {
+        if (nv <= 0 && nj <= 0) return MDPS_OK;
+        const int gj = accum_lanes_jac(L, D);
+        const long long vb = ((long long)std::max(nv, 0) * D * ACCUM_LANES_VALUE + 127) / 128;
+        const long long jb = ((long long)std::max(nj, 0) * D * gj + 127) / 128;
+        auto kern = gj == 1 ? accum_eft_kernel<L, 1> : accum_eft_kernel<L, 2>;
+        kern<<<(unsigned)(vb + jb), 128, 0, st>>>(pool, tp, es, ew, v0, std::max(nv, 0), (int)vb, j0, std::max(nj, 0),
+                                                  n, D, values, jac);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
     }
@@ -697,10 +715,19 @@ static int enqueue(mdps_system *s, const double *in, double *vals, double *jac, 
             if (rc) return rc;
         }
         TimedGroup tg(s, st, 1);
-        for (int r = 0; r < 2; r++) {
+        {
+            // the chunk's value jobs and Jacobian jobs (one chunk: task range 0
+            // holds both kinds, values first)
+            const int NB = s->N * s->batch;
+            int v0 = ch.task0[0], nv = ch.ntask[0], j0 = ch.task0[1], nj = ch.ntask[1];
+            if (s->chunks.size() == 1) {
+                nv = std::min(ch.ntask[0], NB);
+                j0 = NB;
+                nj = ch.ntask[0] - nv;
+            }
             rc = dispatch_L<AccumEft>(L, (const double *)(eft ? s->pool : s->lpool), (const int *)s->task_ptr,
-                                      (const int *)s->ent_slot, (const int *)s->ent_w, ch.task0[r], ch.ntask[r],
-                                      s->N * s->batch, D, vals, jac, st);
+                                      (const int *)s->ent_slot, (const int *)s->ent_w, v0, nv, j0, nj, NB, D, vals,
+                                      jac, st);
             if (rc) return rc;
         }
     }
@@ -844,7 +871,7 @@ extern "C" int mdps_system_stats(const mdps_system *s, mdps_stats *out) {
     int32_t launches = 1;  // QUEUE: one persistent launch
     if (s->schedule != MDPS_SCHED_QUEUE) {
         launches = 1;  // input conversion / copy
-        for (const auto &ch : s->chunks) launches += (int32_t)ch.lv_cnt.size() + (ch.ntask[0] > 0) + (ch.ntask[1] > 0);
+        for (const auto &ch : s->chunks) launches += (int32_t)ch.lv_cnt.size() + (ch.ntask[0] > 0 || ch.ntask[1] > 0);
     }
     out->launches = launches;
     out->schedule = s->schedule;
@@ -1100,6 +1127,11 @@ extern "C" int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP) {
     return MDPS_OK;
 }
 
+extern "C" int mdps_test_set_pdl(int32_t enable) {
+    g_pdl = enable ? 1 : 0;
+    return MDPS_OK;
+}
+
 extern "C" int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t stream) {
     if (!inst_per_s || iters < 1) {
         set_err("invalid argument");
@@ -1194,7 +1226,7 @@ extern "C" int mdps_test_plan(const mdps_supports *sup, const int32_t *exponents
     out[1] = plan_bytes(S, Sd, limbs, D, eft != 0);
     out[2] = (int64_t)S.chunks.size();
     int64_t launches = 1;
-    for (auto &ch : S.chunks) launches += (int64_t)ch.levels4.size() + (ch.ntask[0] > 0) + (ch.ntask[1] > 0);
+    for (auto &ch : S.chunks) launches += (int64_t)ch.levels4.size() + (ch.ntask[0] > 0 || ch.ntask[1] > 0);
     out[3] = launches;
     if (corrupt > 0) {
         const int64_t nfix = (int64_t)S.batch * n + S.M;

@@ -92,19 +92,6 @@ __device__ __forceinline__ void queue_wait_all(const unsigned *flags, const int 
     }
 }
 
-// B += the bins of another partial sum (level o at level o; guard plainly)
-template <int L>
-__device__ __forceinline__ void bins_merge(double (&B)[L + 1], const double (&C)[L + 1]) {
-#pragma unroll
-    for (int o = 0; o < L; o++) {
-        double v = C[o];
-#pragma unroll
-        for (int t = o; t < L; t++) two_sum(B[t], v, B[t], v);
-        B[L] = __dadd_rn(B[L], v);
-    }
-    B[L] = __dadd_rn(B[L], C[L]);
-}
-
 // threads per job for the queue kernel: 2 parts x T pairs x F lanes, F the
 // largest power of two <= fmax with 2 T F <= 256 (default 4: measured on dd,
 // scripts/queue_tune.py — 8 and 16 lanes cost more in merges than they save)

@@ -66,3 +66,35 @@ def test_fused_parts_kernel_equals_the_part_lane_kernel_bitwise(L, degree):
     ref = outs[(2, 1)]
     for key, (v, j) in outs.items():
         assert np.array_equal(v, ref[0]) and np.array_equal(j, ref[1]), key
+
+
+@pytest.mark.parametrize("L,degree,graph", [(4, 31, False), (4, 31, True), (8, 15, False), (3, 63, True), (10, 31, False)])
+def test_programmatic_dependent_launch_changes_nothing(L, degree, graph):
+    """The product levels launched with programmatic stream serialization (the
+    default: a level's blocks are scheduled while the previous level drains and
+    wait for it before reading the pools) give the same bits as plain stream
+    order, evaluation after evaluation (a level reading a slot before its
+    producer finished, or overwriting one still being read, would show up)."""
+    import torch
+    import paper_2012_06607_b200 as mdps
+    si = mdinputs.random_system(970 + L + degree, n=12, monos=10, m_range=(2, 6), exps=(1, 2), degree=degree,
+                                limbs=L)
+    x = torch.from_numpy(si.x).cuda()
+    try:
+        mdps.set_pdl(False)
+        with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS) as s:
+            v, j = s.eval_diff(x)
+            torch.cuda.synchronize()
+            ref = (v.cpu().numpy(), j.cpu().numpy())
+        mdps.set_pdl(True)
+        with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS, use_graph=graph) as s:
+            v = torch.empty_like(v)
+            j = torch.empty_like(j)
+            for _ in range(25):
+                v.zero_()
+                j.zero_()
+                s.eval_diff(x, v, j)
+                torch.cuda.synchronize()
+                assert np.array_equal(v.cpu().numpy(), ref[0]) and np.array_equal(j.cpu().numpy(), ref[1])
+    finally:
+        mdps.set_pdl(True)
