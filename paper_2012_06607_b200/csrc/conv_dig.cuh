@@ -300,8 +300,7 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
         const int job = min(job0 + jl, njobs - 1);
         sexp[idx] = epool[(size_t)jobs[4 * job + which] * dig_exp_stride(D) + k];
     }
-    mbar_wait(bar, 0);
-    __syncthreads();
+    __syncthreads();  // exponents staged; the operand digits are still in flight
 
     const int part = NP == 2 ? (int)threadIdx.x / half : 0;  // warp-uniform (half is whole warps)
     const int r0 = threadIdx.x - part * half;
@@ -343,6 +342,8 @@ __device__ __forceinline__ void conv_dig_block(double *__restrict__ dpool, int *
     }
     ea1 = max(ea1, ZERO_E);
     ea2 = max(ea2, ZERO_E);
+
+    mbar_wait(bar, 0);  // operand digits landed (the pre-pass above ran under the bulk copies)
 
     double *park = spark + (size_t)threadIdx.x * PSTR;
     const int job = job0 + jl;

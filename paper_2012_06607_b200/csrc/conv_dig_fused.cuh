@@ -204,8 +204,7 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
         const int job = min(job0 + jl, njobs - 1);
         sexp[idx] = epool[(size_t)jobs[4 * job + which] * dig_exp_stride(D) + k];
     }
-    mbar_wait(bar, 0);
-    __syncthreads();
+    __syncthreads();  // exponents staged; the operand digits are still in flight
 
     const int jl = threadIdx.x / (T * F);
     const int r = threadIdx.x - jl * T * F;
@@ -228,6 +227,8 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
         ea1 = max(ea1, __shfl_xor_sync(0xffffffffu, ea1, off));
         ea2 = max(ea2, __shfl_xor_sync(0xffffffffu, ea2, off));
     }
+
+    mbar_wait(bar, 0);  // operand digits landed (the pre-pass above ran under the bulk copies)
 
     double2 *park = spark + (size_t)threadIdx.x * PS;
     const int job = job0 + jl;

@@ -115,10 +115,10 @@ __device__ __forceinline__ void bins_merge(double (&B)[L + 1], const double (&C)
 // the Jacobian jobs are done.  Fixed per job type and (L, D), so the summation
 // order of an output never depends on the system it is part of (shards and
 // batches stay bitwise equal to the whole).  Jacobian jobs of long, wide
-// series (L D >= 512) fill the GPU on one lane each and are throughput-bound:
+// series (L D >= 320) fill the GPU on one lane each and are throughput-bound:
 // a second lane only adds its merge (measured: deca 0.88 -> 1.01 ms with two).
 constexpr int ACCUM_LANES_VALUE = 8;
-__host__ __device__ constexpr int accum_lanes_jac(int L, int D) { return L * D >= 512 ? 1 : 2; }
+__host__ __device__ constexpr int accum_lanes_jac(int L, int D) { return L * D >= 320 ? 1 : 2; }
 
 // one addition job's coefficient k on G adjacent lanes: lane g sums entries
 // e0 + g, e0 + g + G, ... in order, then the lanes' bins are merged pairwise
