@@ -43,10 +43,10 @@ int mdps_fp64_peak(int64_t iters, double *inst_per_s, mdps_stream_t stream);
 /* Launch-geometry override of the digit product kernel (tuning only): F
  * lanes per output pair, P jobs per block and NP lane sets per job of a
  * complex system (1: both parts of an output on one thread, the fused-parts
- * kernel, where it exists — L <= 5, else ignored; 2: one lane set per part,
- * twice the threads per job) for every later launch in this process; 0 =
+ * kernel, where it exists — L <= 5, else ignored; 3: the same with the fold
+ * parked in local memory; 2: one lane set per part, twice the threads per job) for every later launch in this process; 0 =
  * the model's / the tuned table's choice (the default).  F in {0,1,2,4,8}, P
- * a power of two <= 32, NP in {0,1,2}; MDPS_EINVAL otherwise, and at launch
+ * a power of two <= 32, NP in {0,1,2,3}; MDPS_EINVAL otherwise, and at launch
  * when the geometry does not fit the kernel's thread / shared-memory limits.
  * Real systems always run one lane set.  Not thread-safe. */
 int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP);

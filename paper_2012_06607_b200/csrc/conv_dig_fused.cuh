@@ -33,21 +33,25 @@ namespace mdps {
 
 __host__ __device__ constexpr int fused_park_slot(int S) { return (S + 2) | 1; }  // double2 entries
 
-__host__ __device__ inline size_t conv_fused_smem(int S, int D, int P, int threads) {
+// lpark: the fold parks in local memory and the emit scratch reuses the job's
+// operand buffers (no per-thread shared-memory slot)
+__host__ __device__ inline size_t conv_fused_smem(int S, int D, int P, int threads, bool lpark = false) {
     const size_t per_job = (size_t)2 * S * D + (size_t)2 * (PADZ + S) * D;  // doubles
-    return (size_t)P * per_job * sizeof(double) + (size_t)threads * fused_park_slot(S) * 2 * sizeof(double) +
+    return (size_t)P * per_job * sizeof(double) +
+           (lpark ? 0 : (size_t)threads * fused_park_slot(S) * 2 * sizeof(double)) +
            (size_t)P * 2 * D * sizeof(int) + 16;  // + exponents, mbarrier
 }
 
 // one pass over this thread's fold iterations, both parts.  On return: park =
 // the k1 partials (raw, |digit| < 2^53), (Ar, Ai) = the k1 + k2 partials
 // (carried).
-template <int L, int DT>
+// park(s, v): stores entry s of the parked k1 partial.
+template <int L, int DT, class ParkFn>
 __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, const double *__restrict__ sy,
                                                 const int *__restrict__ ex, const int *__restrict__ ey, int Drt,
                                                 int t, int f, int F, int eacc1, int eacc2,
                                                 double (&Ar)[digits_for(L)], double (&Ai)[digits_for(L)],
-                                                double2 *park) {
+                                                ParkFn park) {
     constexpr int S = digits_for(L);
     constexpr int NORM = norm_every(S);
     const int D = DT > 0 ? DT : Drt;
@@ -94,7 +98,7 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
             if (j > t && !switched) {  // k1 partial complete: park a copy (raw), keep accumulating
                 switched = true;
 #pragma unroll
-                for (int s = 0; s < S; s++) park[s] = make_double2(Ar[s], Ai[s]);
+                for (int s = 0; s < S; s++) park(s, make_double2(Ar[s], Ai[s]));
             }
             const int jn = j + F <= D ? j + F : j;
             const double *uxn = sx + 2 * term_index(jn);
@@ -132,7 +136,7 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
     }
     if (!switched) {  // no k2 iterations on this lane: everything belongs to k1
 #pragma unroll
-        for (int s = 0; s < S; s++) park[s] = make_double2(Ar[s], Ai[s]);
+        for (int s = 0; s < S; s++) park(s, make_double2(Ar[s], Ai[s]));
     }
 }
 
@@ -162,7 +166,14 @@ __device__ __forceinline__ int conv_fused_z(const double (&A)[S], double2 *scrat
     return z0;
 }
 
-template <int L, int DT>
+// LPARK: the parked k1 partial goes to LOCAL memory (a per-thread array
+// indexed through a run-time zero, so it is not promoted to registers; written
+// once at the fold and read once after the loop, through L1/L2) and the emit
+// scratch reuses the job's operand buffers once all of the job's lanes have
+// finished their pass — no per-thread shared-memory slot, so the operand
+// buffers alone set the resident blocks (qd: 7 instead of 5 blocks of two
+// jobs per SM).
+template <int L, int DT, bool LPARK>
 __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int *__restrict__ epool,
                                                  double *__restrict__ lpool, const int *__restrict__ jobs, int job0,
                                                  int njobs, int Drt, int T, int F, int P, double *sm) {
@@ -171,8 +182,8 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
     const int D = DT > 0 ? DT : Drt;
     const int SX = 2 * S * D, SY = 2 * (PADZ + S) * D;
     double *sdig = sm;                                                  // [P][SX + SY]
-    double2 *spark = reinterpret_cast<double2 *>(sm + (size_t)P * (SX + SY));  // [threads][PS]
-    int *sexp = (int *)(spark + (size_t)blockDim.x * PS);               // [P][2 series][D]
+    double2 *spark = reinterpret_cast<double2 *>(sm + (size_t)P * (SX + SY));  // [threads][PS] (not LPARK)
+    int *sexp = (int *)(spark + (LPARK ? 0 : (size_t)blockDim.x * PS));  // [P][2 series][D]
     uint64_t *bar = reinterpret_cast<uint64_t *>(sexp + (size_t)P * 2 * D);
 
     // stage (as conv_dig_block): two TMA bulk copies per job against an
@@ -230,7 +241,9 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
 
     mbar_wait(bar, 0);  // operand digits landed (the pre-pass above ran under the bulk copies)
 
-    double2 *park = spark + (size_t)threadIdx.x * PS;
+    double2 *park = LPARK ? nullptr : spark + (size_t)threadIdx.x * PS;  // parking + emit scratch slot
+    double2 lpark[LPARK ? S : 1];
+    const int zero = Drt >> 30;  // 0 at run time (D <= 128), unknown to the compiler
     const int job = job0 + jl;
     const bool writer = jl < P && job < njobs;
     double *zd = nullptr;  // digit output (the series is a product input)
@@ -247,13 +260,16 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
     }
     const int k1 = t, k2 = D - 1 - t;
     double Ar[S], Ai[S];
-    conv_fused_pass<L, DT>(sx, sy, ex, ey, D, t, f, F, ea1, ea2, Ar, Ai, park);
+    conv_fused_pass<L, DT>(sx, sy, ex, ey, D, t, f, F, ea1, ea2, Ar, Ai, [&](int s, double2 v) {
+        if (LPARK) lpark[s + zero] = v;
+        else park[s] = v;
+    });
     // k1: every lane carries its parked (raw) partial and takes it off A,
     // which leaves the k2 partial (|digit| <= R + 2^32: exact)
     double Br[S], Bi[S];
 #pragma unroll
     for (int s = 0; s < S; s++) {
-        const double2 v = park[s];
+        const double2 v = LPARK ? lpark[s + zero] : park[s];
         Br[s] = v.x;
         Bi[s] = v.y;
     }
@@ -283,7 +299,18 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
             Ai[s] = Bi[s];
         }
     }
-    __syncwarp();  // parked partials consumed before the emit scratch reuses them
+    bool emits = true;
+    if (LPARK) {
+        // the emit scratch of lane (t, f < 2) lies in its job's operand
+        // buffers: every lane of the job must be done with them (a job's lanes
+        // share a warp, or the block holds whole jobs only)
+        if (T * F <= 32 && 32 % (T * F) == 0) __syncwarp();
+        else __syncthreads();
+        emits = jl < P && (F == 1 || f < 2);
+        park = reinterpret_cast<double2 *>(sdig + (size_t)jlc * (SX + SY)) + (size_t)(F == 1 ? t : 2 * t + f) * PS;
+    } else {
+        __syncwarp();  // parked partials consumed before the emit scratch reuses them
+    }
     const int rounds = F == 1 ? 2 : 1;
     for (int rd = 0; rd < rounds; rd++) {
         const bool is_k1 = F == 1 ? rd == 1 : f == 0;
@@ -297,12 +324,15 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
         const int k = is_k1 ? k1 : k2;
         const int eacc = max(is_k1 ? ea1 : ea2, ZERO_E);
         const bool mine = writer && (F == 1 || f < 2) && (is_k1 || k2 != k1);
-        carry_pass(Ar);
-        carry_pass(Ar);
-        carry_pass(Ai);
-        carry_pass(Ai);
-        const int z0r = conv_fused_z<S, 0>(Ar, park);
-        const int z0i = conv_fused_z<S, 1>(Ai, park);
+        int z0r = S + 2, z0i = S + 2;
+        if (emits) {
+            carry_pass(Ar);
+            carry_pass(Ar);
+            carry_pass(Ai);
+            carry_pass(Ai);
+            z0r = conv_fused_z<S, 0>(Ar, park);
+            z0i = conv_fused_z<S, 1>(Ai, park);
+        }
         if (mine) {
             if (zd) {  // digits of both parts on the grid of the larger part
                 const int zc = min(z0r, z0i);
@@ -334,13 +364,13 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
 // register budget per SM: 128-thread blocks, 4 resident up to S = 10 (<= 128
 // registers), 3 above (<= 168); 256-thread blocks for D = 128 and the
 // generic-D build
-template <int L, int DT>
+template <int L, int DT, bool LPARK = false>
 __global__ void __launch_bounds__(DT == 128 || DT == 0 ? 256 : 128, DT == 128 || DT == 0 ? 1 : (L <= 3 ? 4 : 3))
     conv_fused_kernel(double *__restrict__ dpool, int *__restrict__ epool, double *__restrict__ lpool,
                       const int *__restrict__ jobs, int njobs, int Drt, int T, int F, int P) {
     static_assert(L <= 5, "the fused-parts kernel holds 4 S doubles per thread: L <= 5");
     extern __shared__ __align__(16) double sm[];
-    conv_fused_block<L, DT>(dpool, epool, lpool, jobs, blockIdx.x * P, njobs, Drt, T, F, P, sm);
+    conv_fused_block<L, DT, LPARK>(dpool, epool, lpool, jobs, blockIdx.x * P, njobs, Drt, T, F, P, sm);
 }
 
 }  // namespace mdps

@@ -112,10 +112,17 @@ static const int kTunedGeomFused[][4] = {
     {4, 16, 2, 4}, {4, 32, 2, 2}, {4, 64, 2, 1}, {5, 16, 2, 2}, {5, 32, 2, 1}, {5, 64, 2, 1},
 };
 
+// The same with the fold parked in local memory (conv_fused_kernel<.., true>).
+// (profiles/r02_tune_lpark.json)
+static const int kTunedGeomFusedLpark[][4] = {
+    {3, 16, 2, 2}, {3, 32, 2, 2}, {3, 64, 2, 2}, {3, 128, 2, 1}, {4, 16, 2, 2}, {4, 32, 2, 1}, {4, 64, 2, 1},
+    {4, 128, 2, 1}, {5, 16, 2, 2}, {5, 32, 2, 1}, {5, 64, 2, 1},
+};
+
 // real: the real-system kernel (one part lane set) and its table; tuned:
 // use the table; forceF/P > 0 restrict the search to that F / P
 static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool real, int forceF = 0,
-                        int forceP = 0, bool tuned = false, bool fused = false) {
+                        int forceP = 0, bool tuned = false, bool fused = false, bool lpark = false) {
     const int S = digits_for(L);
     const int T = (D + 1) / 2;
     const int NP = (real || fused) ? 1 : 2;  // lane sets per job (fused: both parts on one thread)
@@ -129,7 +136,8 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool
                     forceP = t[3];
                 }
         };
-        if (fused) pick(kTunedGeomFused);
+        if (fused && lpark) pick(kTunedGeomFusedLpark);
+        else if (fused) pick(kTunedGeomFused);
         else if (real) pick(kTunedGeomReal);
         else pick(kTunedGeom);
     }
@@ -148,7 +156,7 @@ static DigGeom dig_geom(int L, int D, int regs_per_thread, int max_threads, bool
             g.NP = NP;
             g.threads = NP * ((P * T * F + 31) / 32 * 32);  // each part's lane set whole warps
             if (g.threads > max_threads) continue;
-            g.smem = fused ? conv_fused_smem(S, D, P, g.threads) : conv_dig_smem(S, D, P, g.threads);
+            g.smem = fused ? conv_fused_smem(S, D, P, g.threads, lpark) : conv_dig_smem(S, D, P, g.threads);
             if (g.smem > 227 * 1024) continue;
             const int blocks_smem = (int)(228 * 1024 / (g.smem + 1024));
             const int blocks_regs = 65536 / (std::max(regs_per_thread, 32) * g.threads);
@@ -185,8 +193,13 @@ struct ConvEft {
 
 // fused-parts kernel (conv_dig_fused.cuh): complex systems with few digits.
 // mode: 0 = never (part lanes), 1 = where measured faster (default), 2 = always
-// where the kernel exists (L <= 5); mdps_test_force_geometry's NP = 1 / 2
+// where the kernel exists (L <= 5), 3 = always, with the fold parked in local
+// memory; mdps_test_force_geometry's NP = 2 / 0 / 1 / 3
 static int g_fused_mode = 1;
+// measured (profiles/r02_tune_lpark.json, best geometry each): L = 3 -3..6%,
+// L = 5 -6..8% but +6% at D = 128, L = 4 -0..1%; L = 2 not measured (AUTO runs
+// the EFT kernel there)
+static bool fused_lpark_default(int L, int D) { return L == 3 || L == 4 || (L == 5 && D < 128); }
 static int g_pdl = 1;  // programmatic dependent launch of the digit product levels (mdps_test_set_pdl)
 static bool fused_default(int L, int D) {
     (void)D;
@@ -196,12 +209,16 @@ static bool fused_default(int L, int D) {
 template <int L, bool HAS_FUSED = (L <= 5)>
 struct FusedKern {
     using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
-    static KernT get(int) { return nullptr; }
+    static KernT get(int, bool) { return nullptr; }
 };
 template <int L>
 struct FusedKern<L, true> {
     using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
-    static KernT get(int D) {
+    static KernT get(int D, bool lpark) {
+        if (lpark)
+            return D == 16 ? conv_fused_kernel<L, 16, true> : D == 32 ? conv_fused_kernel<L, 32, true>
+                 : D == 64 ? conv_fused_kernel<L, 64, true> : D == 128 ? conv_fused_kernel<L, 128, true>
+                 : conv_fused_kernel<L, 0, true>;
         return D == 16 ? conv_fused_kernel<L, 16> : D == 32 ? conv_fused_kernel<L, 32>
              : D == 64 ? conv_fused_kernel<L, 64> : D == 128 ? conv_fused_kernel<L, 128>
              : conv_fused_kernel<L, 0>;
@@ -215,9 +232,11 @@ struct ConvDig {
         if (njobs <= 0) return MDPS_OK;
         using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
         KernT kern;
-        const bool fused = !real && L <= 5 && (g_fused_mode == 2 || (g_fused_mode == 1 && fused_default(L, D)));
+        const bool fused = !real && L <= 5 && (g_fused_mode >= 2 || (g_fused_mode == 1 && fused_default(L, D)));
+        // (D >= 2: the emit scratch of D + 1 lanes must fit the job's operand buffers)
+        const bool lpark = fused && D >= 2 && (g_fused_mode == 3 || (g_fused_mode == 1 && fused_lpark_default(L, D)));
         if (fused)  // complex systems, few digits: both parts of an output on one thread
-            kern = FusedKern<L>::get(D);
+            kern = FusedKern<L>::get(D, lpark);
         else if (real)  // real systems: one part, one product per term
             kern = D == 16 ? conv_dig_kernel<L, 16, true> : D == 32 ? conv_dig_kernel<L, 32, true>
                  : D == 64 ? conv_dig_kernel<L, 64, true> : D == 128 ? conv_dig_kernel<L, 128, true>
@@ -227,10 +246,10 @@ struct ConvDig {
                  : D == 128 ? conv_dig_kernel<L, 128> : conv_dig_kernel<L, 0>;
         // geometry per (D, kernel), computed once per process under a lock
         static std::mutex mu;
-        static DigGeom cache[3 * 257];
-        static int cregs[3 * 257], cmaxt[3 * 257];
-        static bool cached[3 * 257];
-        const int key = D + (fused ? 2 * 257 : real ? 257 : 0);
+        static DigGeom cache[4 * 257];
+        static int cregs[4 * 257], cmaxt[4 * 257];
+        static bool cached[4 * 257];
+        const int key = D + (lpark ? 3 * 257 : fused ? 2 * 257 : real ? 257 : 0);
         DigGeom g;
         int regs, maxt;
         {
@@ -245,9 +264,9 @@ struct ConvDig {
                 }
                 cregs[key] = regs;
                 cmaxt[key] = maxt;
-                cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, true, fused);
+                cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, true, fused, lpark);
                 if (cache[key].smem == 0)  // tuned entry does not fit
-                    cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, false, fused);
+                    cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, false, fused, lpark);
                 cached[key] = true;
             }
             g = cache[key];
@@ -255,7 +274,7 @@ struct ConvDig {
             maxt = cmaxt[key];
         }
         if (g_force_F > 0 || g_force_P > 0) {  // tuning: a forced (F, P), checked
-            g = dig_geom(L, D, regs, maxt, real != 0, g_force_F, g_force_P, false, fused);
+            g = dig_geom(L, D, regs, maxt, real != 0, g_force_F, g_force_P, false, fused, lpark);
             if (g.smem == 0) { set_err("forced geometry does not fit"); return MDPS_EINVAL; }
         }
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
@@ -1116,14 +1135,14 @@ __global__ void fp64_peak_kernel(int64_t iters, double *sink) {
 }
 
 extern "C" int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP) {
-    if (F < 0 || F > 8 || (F & (F - 1)) || P < 0 || P > 32 || (P & (P - 1)) || NP < 0 || NP > 2) {
-        set_err("forced geometry: F in {0,1,2,4,8}, P in {0,1,...,32} (powers of two), NP in {0,1,2}");
+    if (F < 0 || F > 8 || (F & (F - 1)) || P < 0 || P > 32 || (P & (P - 1)) || NP < 0 || NP > 3) {
+        set_err("forced geometry: F in {0,1,2,4,8}, P in {0,1,...,32} (powers of two), NP in {0,1,2,3}");
         return MDPS_EINVAL;
     }
     g_force_F = F;
     g_force_P = P;
     g_force_NP = NP;
-    g_fused_mode = NP == 1 ? 2 : (NP == 2 ? 0 : 1);
+    g_fused_mode = NP == 1 ? 2 : NP == 3 ? 3 : (NP == 2 ? 0 : 1);
     return MDPS_OK;
 }
 

@@ -16,7 +16,7 @@ import paper_2012_06607_b200 as mdps  # noqa: E402
 CELLS = sys.argv[1].split(",") if len(sys.argv) > 1 else (
     ["qd", "od", "deca"] + [f"sweep_d{d}_L{L}" for d in (15, 31, 63, 127) for L in (2, 3, 4, 5, 8, 10)])
 # lane sets per job: real systems 1; complex 2 (part lanes) and 1 (the fused-parts kernel, L <= 5)
-NPS = (1,) if os.environ.get("TUNE_REAL") == "1" else (2, 1)
+NPS = (1,) if os.environ.get("TUNE_REAL") == "1" else tuple(int(v) for v in os.environ.get("TUNE_NPS", "2,1,3").split(","))
 GEOMS = [(0, 0, 0)] + [(f, p, q) for q in NPS for f in (1, 2, 4, 8) for p in (1, 2, 4, 8)]
 
 
