@@ -55,8 +55,10 @@ int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP);
  * only): 1 (default) = each level's kernel is launched with the
  * programmatic-stream-serialization attribute, so its blocks are scheduled
  * while the previous level drains and wait for it (griddepcontrol.wait)
- * before reading the pools; 0 = plain stream order.  Results are identical.
- * Applies to later launches in this process.  Not thread-safe. */
+ * before reading the pools; 0 = plain stream order.  Bit 1 set (2, 3): also
+ * run every level on the default launch geometry (no wider geometry for
+ * levels below one wave).  Results are identical.  Applies to later launches
+ * in this process.  Not thread-safe. */
 int mdps_test_set_pdl(int32_t enable);
 
 /* Per-kernel timing of mdps_eval_diff (measurement only): when enabled, each

@@ -200,6 +200,7 @@ static int g_fused_mode = 1;
 // L = 5 -6..8% but +6% at D = 128, L = 4 -0..1%; L = 2 not measured (AUTO runs
 // the EFT kernel there)
 static bool fused_lpark_default(int L, int D) { return L == 3 || L == 4 || (L == 5 && D < 128); }
+static int g_small_levels = 1;  // wider geometry for levels below one wave (mdps_test_set_pdl bit 1 clears it)
 static int g_pdl = 1;  // programmatic dependent launch of the digit product levels (mdps_test_set_pdl)
 static bool fused_default(int L, int D) {
     (void)D;
@@ -249,6 +250,14 @@ struct ConvDig {
         static DigGeom cache[4 * 257];
         static int cregs[4 * 257], cmaxt[4 * 257];
         static bool cached[4 * 257];
+        // small levels (a level that cannot fill the GPU: the last levels of a
+        // system whose monomials differ in length): the same kernel with 2x
+        // and 4x the lanes per output pair, one job per block, and the jobs
+        // one wave of each geometry holds — a level runs on the widest
+        // geometry that still takes all its jobs in one wave (the results do
+        // not depend on the geometry: exact accumulation)
+        static DigGeom wide[4 * 257][2];
+        static long long cap[4 * 257][3];  // jobs per wave: default, 2x, 4x
         const int key = D + (lpark ? 3 * 257 : fused ? 2 * 257 : real ? 257 : 0);
         DigGeom g;
         int regs, maxt;
@@ -267,11 +276,39 @@ struct ConvDig {
                 cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, true, fused, lpark);
                 if (cache[key].smem == 0)  // tuned entry does not fit
                     cache[key] = dig_geom(L, D, regs, maxt, real != 0, 0, 0, false, fused, lpark);
+                int dev = 0, sms = 1;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                auto wave = [&](const DigGeom &q) -> long long {
+                    if (q.smem == 0) return 0;
+                    if (q.smem > 48 * 1024)
+                        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)q.smem);
+                    int per = 0;
+                    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, q.threads, q.smem) != cudaSuccess) {
+                        cudaGetLastError();
+                        return 0;
+                    }
+                    return (long long)per * sms * q.P;
+                };
+                cap[key][0] = wave(cache[key]);
+                for (int w = 0; w < 2; w++) {
+                    const int Fw = cache[key].F << (w + 1);
+                    wide[key][w] = Fw <= 8 ? dig_geom(L, D, regs, maxt, real != 0, Fw, 1, false, fused, lpark)
+                                           : DigGeom{0, 0, 0, 0, 0, 0};
+                    cap[key][w + 1] = wave(wide[key][w]);
+                }
                 cached[key] = true;
             }
             g = cache[key];
             regs = cregs[key];
             maxt = cmaxt[key];
+            if (g_small_levels && njobs < cap[key][0]) {
+                for (int w = 1; w >= 0; w--)
+                    if (njobs <= cap[key][w + 1]) {
+                        g = wide[key][w];
+                        break;
+                    }
+            }
         }
         if (g_force_F > 0 || g_force_P > 0) {  // tuning: a forced (F, P), checked
             g = dig_geom(L, D, regs, maxt, real != 0, g_force_F, g_force_P, false, fused, lpark);
@@ -1147,7 +1184,8 @@ extern "C" int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP) {
 }
 
 extern "C" int mdps_test_set_pdl(int32_t enable) {
-    g_pdl = enable ? 1 : 0;
+    g_pdl = (enable & 1) ? 1 : 0;
+    g_small_levels = (enable & 2) ? 0 : 1;
     return MDPS_OK;
 }
 

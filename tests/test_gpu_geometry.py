@@ -76,8 +76,9 @@ def test_fused_parts_kernel_equals_the_part_lane_kernel_bitwise(L, degree):
 def test_programmatic_dependent_launch_changes_nothing(L, degree, graph):
     """The product levels launched with programmatic stream serialization (the
     default: a level's blocks are scheduled while the previous level drains and
-    wait for it before reading the pools) give the same bits as plain stream
-    order, evaluation after evaluation (a level reading a slot before its
+    wait for it before reading the pools), small levels on the wider launch
+    geometry, give the same bits as plain stream order on the default geometry,
+    evaluation after evaluation (a level reading a slot before its
     producer finished, or overwriting one still being read, would show up)."""
     import torch
     import paper_2012_06607_b200 as mdps
@@ -85,7 +86,7 @@ def test_programmatic_dependent_launch_changes_nothing(L, degree, graph):
                                 limbs=L)
     x = torch.from_numpy(si.x).cuda()
     try:
-        mdps.set_pdl(False)
+        mdps.set_pdl(False, small_levels=False)
         with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS) as s:
             v, j = s.eval_diff(x)
             torch.cuda.synchronize()
