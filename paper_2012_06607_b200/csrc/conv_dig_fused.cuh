@@ -46,7 +46,7 @@ __host__ __device__ inline size_t conv_fused_smem(int S, int D, int P, int threa
 // the k1 partials (raw, |digit| < 2^53), (Ar, Ai) = the k1 + k2 partials
 // (carried).
 // park(s, v): stores entry s of the parked k1 partial.
-template <int L, int DT, class ParkFn>
+template <int L, int DT, bool PRE, class ParkFn>
 __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, const double *__restrict__ sy,
                                                 const int *__restrict__ ex, const int *__restrict__ ey, int Drt,
                                                 int t, int f, int F, int eacc1, int eacc2,
@@ -74,10 +74,25 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
         Ur[u] = v.x;
         Ui[u] = v.y;
     };
+    // Row 0 of the NEXT term's y operand is loaded inside the current body too
+    // (at row PF, once the next term's offset and shift are known): at S <= 14 a
+    // body is short and the first DFMA of every term otherwise waits out that
+    // load (ncu at qd: 10% of the kernel's stall samples on that one
+    // instruction).  The row is read through the fast-path base with the shift
+    // clamped to PADZ, which is also the right value on the select path: a
+    // lane with d > PADZ reads a zero row there, as its row 0 must be.
+    // PRE = false (the shared-memory-slot build, kept for L = 5 at degree 127,
+    // where the prefetch measured +3.9%): row 0 is loaded at the term's start.
+    constexpr int PF = S > 6 ? S - 5 : 2;
+    auto fast_base = [&](int kk_, int d_) { return sy + (PADZ - min(d_, PADZ)) * D2 + 2 * kk_; };
     int kk, d;
+    const double *Wf;  // y's digit row 0 moved down by min(d, PADZ) rows
+    double2 w0;        // its (re, im) pair
     {
         const int j0 = min(f, D);  // a lane with f > D has no terms (clamped reads only)
         term_meta(j0, kk, d);
+        Wf = fast_base(kk, d);
+        w0 = *reinterpret_cast<const double2 *>(Wf);
         const double *ux = sx + 2 * term_index(j0);
 #pragma unroll
         for (int u = 0; u < S; u++) load_x(ux, u);
@@ -103,13 +118,20 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
             const int jn = j + F <= D ? j + F : j;
             const double *uxn = sx + 2 * term_index(jn);
             int kkn, dn;
+            const double *Wfn;
+            double2 w0n = make_double2(0.0, 0.0);
             auto ahead = [&](int l) {  // called after digit row l of the body
-                if (l == 1) term_meta(jn, kkn, dn);
+                if (l == 1) {
+                    term_meta(jn, kkn, dn);
+                    Wfn = fast_base(kkn, dn);
+                }
+                if (PRE && l == PF) w0n = *reinterpret_cast<const double2 *>(Wfn);
                 load_x(uxn, S - 1 - l);
             };
             if (__all_sync(__activemask(), d <= PADZ)) {
-                const double *W = sy + (PADZ - d) * D2 + 2 * kk;
-                double2 w = *reinterpret_cast<const double2 *>(W);
+                const double *W = Wf;
+                if (!PRE) w0 = *reinterpret_cast<const double2 *>(Wf);
+                double2 w = w0;
 #pragma unroll
                 for (int l = 0; l < S; l++) {
                     double2 wn = make_double2(0.0, 0.0);
@@ -120,16 +142,19 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
                 }
             } else {
                 const double *W = sy + 2 * kk;
+                if (!PRE) w0 = *reinterpret_cast<const double2 *>(Wf);
 #pragma unroll
                 for (int l = 0; l < S; l++) {
-                    double2 w = make_double2(0.0, 0.0);
-                    if (l >= d) w = *reinterpret_cast<const double2 *>(W + (PADZ + l - d) * D2);
+                    double2 w = l == 0 ? w0 : make_double2(0.0, 0.0);
+                    if (l > 0 && l >= d) w = *reinterpret_cast<const double2 *>(W + (PADZ + l - d) * D2);
                     row(l, w.x, w.y);
                     ahead(l);
                 }
             }
             kk = kkn;
             d = dn;
+            Wf = Wfn;
+            w0 = w0n;
         }
         carry_pass(Ar);
         carry_pass(Ai);
@@ -260,7 +285,7 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
     }
     const int k1 = t, k2 = D - 1 - t;
     double Ar[S], Ai[S];
-    conv_fused_pass<L, DT>(sx, sy, ex, ey, D, t, f, F, ea1, ea2, Ar, Ai, [&](int s, double2 v) {
+    conv_fused_pass<L, DT, LPARK>(sx, sy, ex, ey, D, t, f, F, ea1, ea2, Ar, Ai, [&](int s, double2 v) {
         if (LPARK) lpark[s + zero] = v;
         else park[s] = v;
     });
