@@ -88,11 +88,21 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
     int kk, d;
     const double *Wf;  // y's digit row 0 moved down by min(d, PADZ) rows
     double2 w0;        // its (re, im) pair
+    // every lane of the warp within the PADZ window: voted one term ahead,
+    // inside the body (the lanes of the next iteration are among the voters;
+    // a lane that drops out votes with its last term's shift, and any lane
+    // outside the window only sends the warp down the select path, which is
+    // always right)
+    // (VA: where measured faster — L = 3: -0.7..2.3%; L = 5: +0.5..2.8%, L = 4:
+    // +-0.5%, so there the vote stays at the term's start)
+    constexpr bool VA = L == 3;
+    bool fast;
     {
         const int j0 = min(f, D);  // a lane with f > D has no terms (clamped reads only)
         term_meta(j0, kk, d);
         Wf = fast_base(kk, d);
         w0 = *reinterpret_cast<const double2 *>(Wf);
+        fast = __all_sync(__activemask(), d <= PADZ);
         const double *ux = sx + 2 * term_index(j0);
 #pragma unroll
         for (int u = 0; u < S; u++) load_x(ux, u);
@@ -120,15 +130,18 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
             int kkn, dn;
             const double *Wfn;
             double2 w0n = make_double2(0.0, 0.0);
+            bool fastn = false;
             auto ahead = [&](int l) {  // called after digit row l of the body
                 if (l == 1) {
                     term_meta(jn, kkn, dn);
                     Wfn = fast_base(kkn, dn);
                 }
+                if (VA && l == 2) fastn = __all_sync(__activemask(), dn <= PADZ);
                 if (PRE && l == PF) w0n = *reinterpret_cast<const double2 *>(Wfn);
                 load_x(uxn, S - 1 - l);
             };
-            if (__all_sync(__activemask(), d <= PADZ)) {
+            if (!VA) fast = __all_sync(__activemask(), d <= PADZ);
+            if (fast) {
                 const double *W = Wf;
                 if (!PRE) w0 = *reinterpret_cast<const double2 *>(Wf);
                 double2 w = w0;
@@ -155,6 +168,7 @@ __device__ __forceinline__ void conv_fused_pass(const double *__restrict__ sx, c
             d = dn;
             Wf = Wfn;
             w0 = w0n;
+            fast = fastn;
         }
         carry_pass(Ar);
         carry_pass(Ai);
