@@ -231,6 +231,16 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
     // as this level's blocks drain; nothing a previous launch wrote (digit and
     // exponent pools) is read before grid_dep_wait() — the job list is static
     grid_dep_launch_dependents();
+    // (the job table is static: the slot indices this thread needs first —
+    // bulk copy c = threadIdx.x, exponent idx = threadIdx.x — are read here,
+    // under the zero rows and the wait on the previous launch)
+    int copy_slot = 0, exp_slot = 0;
+    if (threadIdx.x < 32 && (int)threadIdx.x < 2 * P)
+        copy_slot = jobs[4 * min(job0 + ((int)threadIdx.x >> 1), njobs - 1) + (threadIdx.x & 1)];
+    if ((int)threadIdx.x < P * 2 * D) {
+        const int jl = threadIdx.x / (2 * D), r = threadIdx.x - jl * 2 * D;
+        exp_slot = jobs[4 * min(job0 + jl, njobs - 1) + r / D];
+    }
     if (threadIdx.x == 0) mbar_init(bar, 1);
     for (int idx = threadIdx.x; idx < P * 2 * PADZ * D; idx += blockDim.x) {  // zero rows
         const int jl = idx / (2 * PADZ * D), r = idx - jl * 2 * PADZ * D;
@@ -245,14 +255,16 @@ __device__ __forceinline__ void conv_fused_block(double *__restrict__ dpool, int
             const int jl = c >> 1, which = c & 1;
             const int job = min(job0 + jl, njobs - 1);
             double *base = sdig + (size_t)jl * (SX + SY) + (which ? SX + 2 * PADZ * D : 0);
-            bulk_g2s(base, dpool + (size_t)jobs[4 * job + which] * dig_slot_stride(S, D), (unsigned)(SX * 8), bar);
+            const int slot = c < 32 ? copy_slot : jobs[4 * job + which];
+            bulk_g2s(base, dpool + (size_t)slot * dig_slot_stride(S, D), (unsigned)(SX * 8), bar);
         }
     }
     for (int idx = threadIdx.x; idx < P * 2 * D; idx += blockDim.x) {
         const int jl = idx / (2 * D), r = idx - jl * 2 * D;
         const int which = r / D, k = r - which * D;
         const int job = min(job0 + jl, njobs - 1);
-        sexp[idx] = epool[(size_t)jobs[4 * job + which] * dig_exp_stride(D) + k];
+        const int slot = idx < (int)blockDim.x ? exp_slot : jobs[4 * job + which];
+        sexp[idx] = epool[(size_t)slot * dig_exp_stride(D) + k];
     }
     __syncthreads();  // exponents staged; the operand digits are still in flight
 
