@@ -548,13 +548,14 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
     const int B = opt && opt->batch > 1 ? opt->batch : 1;
     if (opt && opt->batch < 0) { set_err("batch must be >= 1"); return nullptr; }
     // MDPS_ALGO_AUTO (measured): digits, except above degree 127
-    // (digits cap) and at L = 2, where the digit kernel is shared-memory bound
-    // (S = 7 digits: 2S 16-byte loads per S(S+1) DFMAs) and the EFT kernel is
-    // faster (the L = 2 sweep cells from degree 31 on, batches of dd points,
-    // dd itself); at L = 3 the digit kernel on the common-exponent format
-    // wins from degree 15 on (d = 15: 0.43 vs 0.55 ms, d = 31: 1.19 vs 1.48)
+    // (digits cap) and at L = 2 below degree 63: with S = 7 digits a term is
+    // short, and up to D = 32 the EFT kernel, whose operands are 2 limbs, is
+    // level or ahead (d = 15 a tie, d = 31 0.61 vs 0.62 ms; dd itself and
+    // batches of dd points run the EFT job queue); from D = 64 on the
+    // fused-parts digit kernel wins (d = 63 1.97 vs 2.04 ms, d = 127 7.05 vs
+    // 7.61); at L = 3 digits win from degree 15 on
     if (algo == MDPS_ALGO_AUTO)
-        algo = D > 128 || (!real && limbs == 2) ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
+        algo = D > 128 || (!real && limbs == 2 && D < 64) ? MDPS_ALGO_EFT : MDPS_ALGO_DIGITS;
     const int sched_opt = opt ? opt->schedule : MDPS_SCHED_AUTO;
     if (sched_opt != MDPS_SCHED_AUTO && sched_opt != MDPS_SCHED_LEVELS && sched_opt != MDPS_SCHED_QUEUE) {
         set_err("unknown schedule");
