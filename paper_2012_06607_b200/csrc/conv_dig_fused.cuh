@@ -23,9 +23,13 @@
 // DESIGN.md §7.4).
 //
 // Threads of a block: [job][pair t][lane f], padded to whole warps.  Shared
-// memory per job as in conv_dig.cuh; per thread a parking slot of PS (re, im)
+// memory per job as in conv_dig.cuh.  Parking at the fold and the emit
+// scratch: LPARK = false — a per-thread shared-memory slot of PS (re, im)
 // pairs, PS = S + 2 rounded up to odd (16-byte accesses at an odd multiple of
-// 16 bytes between lanes are bank-conflict free).
+// 16 bytes between lanes are bank-conflict free); LPARK = true (the default
+// wherever measured faster, libmdps.cu fused_lpark_default) — the parked
+// partial in local memory and the emit scratch in the job's own operand
+// buffers, so that the operand buffers alone set the resident blocks.
 #pragma once
 #include "conv_dig.cuh"
 
