@@ -57,8 +57,9 @@ int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP);
  * while the previous level drains and wait for it (griddepcontrol.wait)
  * before reading the pools; 0 = plain stream order.  Bit 1 set (2, 3): also
  * run every level on the default launch geometry (no wider geometry for
- * levels below one wave).  Results are identical.  Applies to later launches
- * in this process.  Not thread-safe. */
+ * levels below one wave).  Bit 2 set (4..7): systems created afterwards keep
+ * every product in its earliest level (no level balancing).  Results are
+ * identical.  Applies to later launches in this process.  Not thread-safe. */
 int mdps_test_set_pdl(int32_t enable);
 
 /* Per-kernel timing of mdps_eval_diff (measurement only): when enabled, each

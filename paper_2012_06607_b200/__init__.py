@@ -499,10 +499,12 @@ def force_geometry(F: int = 0, P: int = 0, NP: int = 0) -> None:
     _check(lib().mdps_test_force_geometry(F, P, NP), "mdps_test_force_geometry")
 
 
-def set_pdl(enable: bool = True, small_levels: bool = True) -> None:
-    """Measurement only: programmatic dependent launch of the digit product levels and the
-    wider launch geometry of levels below one wave (both default on)."""
-    _check(lib().mdps_test_set_pdl((1 if enable else 0) | (0 if small_levels else 2)), "mdps_test_set_pdl")
+def set_pdl(enable: bool = True, small_levels: bool = True, balance: bool = True) -> None:
+    """Measurement only: programmatic dependent launch of the digit product levels, the wider
+    launch geometry of levels below one wave, and (for systems created afterwards) the level
+    balancing of the schedule (all default on)."""
+    _check(lib().mdps_test_set_pdl((1 if enable else 0) | (0 if small_levels else 2) | (0 if balance else 4)),
+           "mdps_test_set_pdl")
 
 
 def fp64_peak(iters: int = 20000, stream=None) -> float:

@@ -201,6 +201,7 @@ static int g_fused_mode = 1;
 // the EFT kernel there)
 static bool fused_lpark_default(int L, int D) { return L == 3 || L == 4 || (L == 5 && D < 128); }
 static int g_small_levels = 1;  // wider geometry for levels below one wave (mdps_test_set_pdl bit 1 clears it)
+static int g_balance_levels = 1;  // level balancing at create (mdps_test_set_pdl bit 2 clears it)
 static int g_pdl = 1;  // programmatic dependent launch of the digit product levels (mdps_test_set_pdl)
 static bool fused_default(int L, int D) {
     (void)D;
@@ -228,11 +229,9 @@ struct FusedKern<L, true> {
 
 template <int L>
 struct ConvDig {
-    static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, int real,
-                   cudaStream_t st) {
-        if (njobs <= 0) return MDPS_OK;
-        using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
-        KernT kern;
+    using KernT = void (*)(double *, int *, double *, const int *, int, int, int, int, int);
+    // kernel, launch geometry and jobs per wave of resident blocks for a level of njobs jobs
+    static int geom(int njobs, int D, int real, KernT &kern, DigGeom &g, long long &wave_jobs) {
         const bool fused = !real && L <= 5 && (g_fused_mode >= 2 || (g_fused_mode == 1 && fused_default(L, D)));
         // (D >= 2: the emit scratch of D + 1 lanes must fit the job's operand buffers)
         const bool lpark = fused && D >= 2 && (g_fused_mode == 3 || (g_fused_mode == 1 && fused_lpark_default(L, D)));
@@ -259,7 +258,6 @@ struct ConvDig {
         static DigGeom wide[4 * 257][2];
         static long long cap[4 * 257][3];  // jobs per wave: default, 2x, 4x
         const int key = D + (lpark ? 3 * 257 : fused ? 2 * 257 : real ? 257 : 0);
-        DigGeom g;
         int regs, maxt;
         {
             std::lock_guard<std::mutex> lk(mu);
@@ -302,6 +300,7 @@ struct ConvDig {
             g = cache[key];
             regs = cregs[key];
             maxt = cmaxt[key];
+            wave_jobs = cap[key][0];
             if (g_small_levels && njobs < cap[key][0]) {
                 for (int w = 1; w >= 0; w--)
                     if (njobs <= cap[key][w + 1]) {
@@ -314,6 +313,17 @@ struct ConvDig {
             g = dig_geom(L, D, regs, maxt, real != 0, g_force_F, g_force_P, false, fused, lpark);
             if (g.smem == 0) { set_err("forced geometry does not fit"); return MDPS_EINVAL; }
         }
+        return MDPS_OK;
+    }
+
+    static int run(double *dpool, int *epool, double *lpool, const int *jobs, int njobs, int D, int real,
+                   cudaStream_t st) {
+        if (njobs <= 0) return MDPS_OK;
+        KernT kern;
+        DigGeom g;
+        long long wave_jobs = 0;
+        const int rc = geom(njobs, D, real, kern, g, wave_jobs);
+        if (rc != MDPS_OK) return rc;
         if (g.smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
         const int blocks = (njobs + g.P - 1) / g.P;
         // programmatic dependent launch: this level's blocks may be scheduled
@@ -333,6 +343,19 @@ struct ConvDig {
         CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, dpool, epool, lpool, jobs, njobs, D, T, F, P), MDPS_ECUDA);
         CUDA_TRY(cudaGetLastError(), MDPS_ECUDA);
         return MDPS_OK;
+    }
+};
+
+// jobs one wave of resident blocks of the digit product kernel holds (default geometry)
+template <int L>
+struct ConvDigWave {
+    static int run(int D, int real, long long *out) {
+        typename ConvDig<L>::KernT kern;
+        DigGeom g;
+        long long wave = 0;
+        const int rc = ConvDig<L>::geom(1 << 30, D, real, kern, g, wave);
+        *out = wave;
+        return rc;
     }
 };
 
@@ -572,6 +595,12 @@ extern "C" mdps_system *mdps_system_create_ex(const mdps_supports *sup, const in
                               (sched_opt == MDPS_SCHED_AUTO && algo == MDPS_ALGO_EFT &&
                                S.products * (opt && opt->batch > 1 ? opt->batch : 1) <= MDPS_QUEUE_MAX_PRODUCTS)
                           ? MDPS_SCHED_QUEUE : MDPS_SCHED_LEVELS;
+    if (sched == MDPS_SCHED_LEVELS && algo == MDPS_ALGO_DIGITS && B == 1 && g_balance_levels) {
+        // level balancing (schedule.hpp): summed-only products move from the
+        // full early levels into later levels below one wave of the kernel
+        long long wave = 0;
+        if (dispatch_L<ConvDigWave>(limbs, D, real, &wave) == MDPS_OK && wave > 0) balance_levels(S, wave);
+    }
     if (B > 1 && !replicate_schedule(S, n, B, err)) {
         set_err(err);
         return nullptr;
@@ -1187,6 +1216,7 @@ extern "C" int mdps_test_force_geometry(int32_t F, int32_t P, int32_t NP) {
 extern "C" int mdps_test_set_pdl(int32_t enable) {
     g_pdl = (enable & 1) ? 1 : 0;
     g_small_levels = (enable & 2) ? 0 : 1;
+    g_balance_levels = (enable & 4) ? 0 : 1;
     return MDPS_OK;
 }
 

@@ -182,6 +182,49 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
     return true;
 }
 
+int64_t balance_levels(Schedule &S, int64_t min_jobs) {
+    const int nl = (int)S.levels4.size();
+    if (nl < 2 || min_jobs <= 0 || S.levels.size() != S.levels4.size()) return 0;
+    int64_t moved = 0;
+    for (int t = nl - 1; t >= 1; t--) {
+        int64_t need = min_jobs - (int64_t)(S.levels4[(size_t)t].size() / 4);
+        for (int s = 0; s < t && need > 0; s++) {
+            auto &src4 = S.levels4[(size_t)s];
+            auto &src3 = S.levels[(size_t)s];
+            const int64_t have = (int64_t)(src4.size() / 4);
+            int64_t give = std::min(need, have - min_jobs);
+            if (give <= 0) continue;
+            // the level's last `give` summed-only jobs (code bit 0 clear), order kept
+            std::vector<int32_t> keep4, keep3, mv4, mv3;
+            keep4.reserve(src4.size());
+            keep3.reserve(src3.size());
+            for (int64_t q = have - 1; q >= 0; q--) {
+                const bool leaf = (src4[(size_t)(4 * q + 3)] & 1) == 0;
+                auto &d4 = (leaf && give > 0) ? mv4 : keep4;
+                auto &d3 = (leaf && give > 0) ? mv3 : keep3;
+                if (leaf && give > 0) give--;
+                for (int c = 3; c >= 0; c--) d4.push_back(src4[(size_t)(4 * q + c)]);
+                for (int c = 2; c >= 0; c--) d3.push_back(src3[(size_t)(3 * q + c)]);
+            }
+            std::reverse(keep4.begin(), keep4.end());
+            std::reverse(keep3.begin(), keep3.end());
+            std::reverse(mv4.begin(), mv4.end());
+            std::reverse(mv3.begin(), mv3.end());
+            const int64_t got = (int64_t)(mv4.size() / 4);
+            if (got == 0) continue;
+            src4 = std::move(keep4);
+            src3 = std::move(keep3);
+            auto &dst4 = S.levels4[(size_t)t];
+            auto &dst3 = S.levels[(size_t)t];
+            dst4.insert(dst4.end(), mv4.begin(), mv4.end());
+            dst3.insert(dst3.end(), mv3.begin(), mv3.end());
+            need -= got;
+            moved += got;
+        }
+    }
+    return moved;
+}
+
 bool replicate_schedule(Schedule &S, int32_t n, int32_t B, std::string &err) {
     const int64_t M = S.M, J = S.nslots - n - M, nl = S.nlimb;
     const int64_t total = (int64_t)B * n + M + (int64_t)B * J;

@@ -67,6 +67,17 @@ bool build_schedule(int32_t n_polys, const int32_t *poly_ptr, const int32_t *mon
                     const int32_t *vars, const int32_t *exps, int32_t n, Schedule &S,
                     std::string &err);
 
+// Level balancing (leveled schedule): a product whose output is only summed by
+// the addition jobs (never a product input) may run in any later level.  The
+// levels of a system whose monomials differ in length shrink towards the end
+// — the last ones cannot fill the GPU — so such jobs are moved, in order,
+// from the earlier levels that hold more than min_jobs into every later
+// level that holds fewer, until it holds min_jobs (one wave of the product
+// kernel's resident blocks) or the donors run out.  Same jobs, same
+// arithmetic: the outputs do not change.  Call before replicate_schedule /
+// plan_memory.  Returns the number of jobs moved.
+int64_t balance_levels(Schedule &S, int64_t min_jobs);
+
 // The same system at B points in one schedule (mdps_options.batch): slots
 // [0, B n) = the points' x, [B n, B n + M) = the shared coefficients, then B
 // blocks of product slots; every level holds the B copies of its jobs, the

@@ -31,8 +31,9 @@ for c in CELLS:
     j = torch.empty((si.n, si.n, 2, si.limbs, si.D), dtype=torch.float64, device="cuda")
     row = {"cell": c}
     for graph in (False, True):
-        for pdl in (False, True, 2):  # 2: programmatic launch, but every level on the default geometry
-            mdps.set_pdl(bool(pdl), small_levels=pdl != 2)
+        # 2: programmatic launch, but every level on the default geometry; 3: no level balancing
+        for pdl in (False, True, 2, 3):
+            mdps.set_pdl(bool(pdl), small_levels=pdl != 2, balance=pdl != 3)
             with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS, use_graph=graph) as s:
                 for _ in range(3):
                     s.eval_diff(x, v, j)
@@ -47,6 +48,6 @@ for c in CELLS:
                     torch.cuda.synchronize()
                     ts.append(a.elapsed_time(b))
                 ts.sort()
-                row[f"graph={int(graph)},pdl={int(bool(pdl))}" + (",default_geometry" if pdl == 2 else "")] = ts[len(ts) // 2]
+                row[f"graph={int(graph)},pdl={int(bool(pdl))}" + (",default_geometry" if pdl == 2 else ",unbalanced_levels" if pdl == 3 else "")] = ts[len(ts) // 2]
     mdps.set_pdl(True)
     print(json.dumps(row), flush=True)

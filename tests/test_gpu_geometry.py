@@ -86,7 +86,7 @@ def test_programmatic_dependent_launch_changes_nothing(L, degree, graph):
                                 limbs=L)
     x = torch.from_numpy(si.x).cuda()
     try:
-        mdps.set_pdl(False, small_levels=False)
+        mdps.set_pdl(False, small_levels=False, balance=False)
         with mdps.System.from_inputs(si, algo=mdps.MDPS_ALGO_DIGITS) as s:
             v, j = s.eval_diff(x)
             torch.cuda.synchronize()
@@ -103,3 +103,30 @@ def test_programmatic_dependent_launch_changes_nothing(L, degree, graph):
                 assert np.array_equal(v.cpu().numpy(), ref[0]) and np.array_equal(j.cpu().numpy(), ref[1])
     finally:
         mdps.set_pdl(True)
+
+
+def test_level_balancing_changes_nothing():
+    """Summed-only products moved into later, emptier levels (balance_levels):
+    the qd config's last levels fill up to one wave, the outputs stay bit for
+    bit those of the earliest-level schedule."""
+    import torch
+    import paper_2012_06607_b200 as mdps
+    si = mdinputs.make_config("qd")
+    x = torch.from_numpy(si.x).cuda()
+    try:
+        mdps.set_pdl(True, balance=False)
+        with mdps.System.from_inputs(si) as s:
+            lv0 = s.level_jobs()
+            v, j = s.eval_diff(x)
+            torch.cuda.synchronize()
+            ref = (v.cpu().numpy(), j.cpu().numpy())
+        mdps.set_pdl(True)
+        with mdps.System.from_inputs(si) as s:
+            lv1 = s.level_jobs()
+            v, j = s.eval_diff(x)
+            torch.cuda.synchronize()
+            assert np.array_equal(v.cpu().numpy(), ref[0]) and np.array_equal(j.cpu().numpy(), ref[1])
+    finally:
+        mdps.set_pdl(True)
+    assert sum(lv0) == sum(lv1) and len(lv0) == len(lv1)
+    assert min(lv1) > min(lv0) and lv1 != lv0
