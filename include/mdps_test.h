@@ -102,6 +102,17 @@ int mdps_test_queue_trace(mdps_system *sys, int32_t enable, int64_t *out, int32_
  * (a power of two; 0 = the default rule).  Returns MDPS_OK or MDPS_EINVAL. */
 int mdps_test_queue_config(int32_t max_blocks, int32_t lanes);
 
+/* Host-only (no GPU): level balancing of a system's schedule (a product whose
+ * output is only summed may run in any later level; such jobs move from the
+ * earlier levels above `min_jobs` jobs into later levels below it), then the
+ * schedule check and the memory plan of mdps_test_plan.  before / after:
+ * product jobs per level (max_levels entries each, zero-filled); *moved: jobs
+ * moved; *same_jobs: 1 if the balanced levels hold exactly the original
+ * jobs, none moved to an earlier level.  Returns the number of levels, or
+ * MDPS_EINVAL (a failed check included). */
+int mdps_test_balance(const mdps_supports *supports, const int32_t *exponents, int32_t n, int64_t min_jobs,
+                      int64_t *before, int64_t *after, int32_t max_levels, int64_t *moved, int32_t *same_jobs);
+
 /* Host-only (no GPU): build the job schedule of a system, check it (every
  * slot in range, every input written by an earlier launch, no slot read and
  * written in one launch, no live slot overwritten — schedule.hpp

@@ -38,7 +38,7 @@ EXPORTED_SYMBOLS = (
     "mdps_fp64_peak", "mdps_test_force_geometry", "mdps_test_set_pdl", "mdps_system_set_timing", "mdps_system_timing",
     "mdps_solver_create", "mdps_solve", "mdps_solver_status", "mdps_solver_stats", "mdps_solver_destroy",
     "mdps_solver_trace", "mdps_newton_step", "mdps_newton", "mdps_solver_create_ls", "mdps_test_queue_trace",
-    "mdps_test_queue_config", "mdps_solver_flags", "mdps_test_plan",
+    "mdps_test_queue_config", "mdps_solver_flags", "mdps_test_plan", "mdps_test_balance",
 )
 
 
@@ -134,6 +134,7 @@ def lib() -> ctypes.CDLL:
     L.mdps_test_queue_trace.argtypes = [vp, i32, P(i64), i32]
     L.mdps_test_queue_config.argtypes = [i32, i32]
     L.mdps_test_plan.argtypes = [P(_Supports), P(i32), i32, i32, i32, i32, i32, i32, i32, P(i64)]
+    L.mdps_test_balance.argtypes = [P(_Supports), P(i32), i32, i64, P(i64), P(i64), i32, P(i64), P(i32)]
     L.mdps_solver_destroy.argtypes = [vp]
     L.mdps_solver_destroy.restype = None
     _lib = L
@@ -487,6 +488,19 @@ def test_plan(si, eft: bool, batch: int = 1, chunks: int = 1, corrupt: int = 0):
     rc = lib().mdps_test_plan(ctypes.byref(sup), _ptr_i32(ee), si.n, si.degree, si.limbs, 1 if eft else 0, batch,
                               chunks, corrupt, out)
     return rc, dict(unplanned_bytes=out[0], planned_bytes=out[1], chunks=out[2], launches=out[3]), mdps_last_error()
+
+
+def test_balance(si, min_jobs: int, max_levels: int = 256):
+    """Host-only level balancing + checks (mdps_test_balance): returns
+    (levels or rc < 0, before, after, moved, same_jobs, message)."""
+    pp, mp, vv, ee = _i32(si.poly_ptr), _i32(si.mono_ptr), _i32(si.vars), _i32(si.exps)
+    sup = _Supports(len(pp) - 1, _ptr_i32(pp), _ptr_i32(mp), _ptr_i32(vv))
+    before, after = (ctypes.c_int64 * max_levels)(), (ctypes.c_int64 * max_levels)()
+    moved, same = ctypes.c_int64(0), ctypes.c_int32(0)
+    rc = lib().mdps_test_balance(ctypes.byref(sup), _ptr_i32(ee), si.n, min_jobs, before, after, max_levels,
+                                 ctypes.byref(moved), ctypes.byref(same))
+    nl = max(rc, 0)
+    return rc, list(before[:nl]), list(after[:nl]), moved.value, same.value, mdps_last_error()
 
 
 def queue_config(max_blocks: int = 0, lanes: int = 0) -> None:

@@ -1285,6 +1285,62 @@ extern "C" int mdps_test_queue_trace(mdps_system *s, int32_t enable, int64_t *ou
     return (int)s->qtickets;
 }
 
+// Host-only: level balancing (schedule.hpp balance_levels) of a system's
+// schedule with `min_jobs` jobs per level as the target, then the checks and
+// the memory plan of mdps_test_plan.  before / after: product jobs per level
+// (up to max_levels each); *moved: jobs moved; *same_jobs: 1 if the balanced
+// levels hold exactly the jobs of the original ones, every moved job summed
+// only, none moved to an earlier level.  Returns the number of levels, or
+// MDPS_EINVAL (a failed check included).
+extern "C" int mdps_test_balance(const mdps_supports *sup, const int32_t *exponents, int32_t n, int64_t min_jobs,
+                                 int64_t *before, int64_t *after, int32_t max_levels, int64_t *moved,
+                                 int32_t *same_jobs) {
+    if (!sup || !before || !after || !moved || !same_jobs || n < 1 || max_levels < 1) {
+        set_err("invalid argument");
+        return MDPS_EINVAL;
+    }
+    Schedule S;
+    std::string err;
+    if (!build_schedule(sup->n_polys, sup->poly_ptr, sup->mono_ptr, sup->vars, exponents, n, S, err)) {
+        set_err(err);
+        return MDPS_EINVAL;
+    }
+    const auto old4 = S.levels4;
+    *moved = balance_levels(S, min_jobs);
+    const int nl = (int)S.levels4.size();
+    // job -> level maps (a job is named by its output slot)
+    std::vector<std::pair<int32_t, int32_t>> a, b;  // (out, level)
+    for (int lv = 0; lv < (int)old4.size(); lv++)
+        for (size_t q = 0; q < old4[(size_t)lv].size(); q += 4) a.push_back({old4[(size_t)lv][q + 2], lv});
+    for (int lv = 0; lv < nl; lv++)
+        for (size_t q = 0; q < S.levels4[(size_t)lv].size(); q += 4) b.push_back({S.levels4[(size_t)lv][q + 2], lv});
+    std::sort(a.begin(), a.end());
+    std::sort(b.begin(), b.end());
+    bool same = a.size() == b.size() && old4.size() == S.levels4.size() && S.levels.size() == S.levels4.size();
+    int64_t changed = 0;
+    for (size_t i = 0; same && i < a.size(); i++) {
+        same = a[i].first == b[i].first && b[i].second >= a[i].second;
+        changed += a[i].second != b[i].second;
+    }
+    for (int lv = 0; same && lv < nl; lv++) {
+        same = S.levels[(size_t)lv].size() / 3 == S.levels4[(size_t)lv].size() / 4;
+        for (size_t q = 0, r = 0; same && q < S.levels4[(size_t)lv].size(); q += 4, r += 3)
+            same = S.levels4[(size_t)lv][q] == S.levels[(size_t)lv][r] &&
+                   S.levels4[(size_t)lv][q + 1] == S.levels[(size_t)lv][r + 1] &&
+                   S.levels4[(size_t)lv][q + 2] == S.levels[(size_t)lv][r + 2];
+    }
+    *same_jobs = same && changed == *moved ? 1 : 0;
+    for (int lv = 0; lv < max_levels; lv++) {
+        before[lv] = lv < (int)old4.size() ? (int64_t)(old4[(size_t)lv].size() / 4) : 0;
+        after[lv] = lv < nl ? (int64_t)(S.levels4[(size_t)lv].size() / 4) : 0;
+    }
+    if (!check_schedule(S, n, false, err) || !plan_memory(S, n, 1, false, err)) {
+        set_err(err);
+        return MDPS_EINVAL;
+    }
+    return nl;
+}
+
 // host-only check of the job schedule and its memory plan (no GPU needed):
 // out[0] pool bytes without reuse, out[1] with the plan, out[2] chunks,
 // out[3] launches per evaluation.  corrupt > 0 damages the plan first (1: a

@@ -66,3 +66,25 @@ def test_workspace_bounds():
         out[name] = (one, four)
     assert out["od"][1]["planned_bytes"] < 1 << 30
     assert out["deca"][1]["planned_bytes"] < 3 << 30
+
+
+@pytest.mark.parametrize("name,min_jobs", [("qd", 1776), ("qd", 4000), ("dd", 100), ("od", 20000), ("qd", 10 ** 6)])
+def test_level_balancing_keeps_the_jobs_and_passes_the_checks(name, min_jobs):
+    """balance_levels (schedule.hpp): the balanced levels hold exactly the
+    original jobs, none moved to an earlier level, every moved job summed
+    only; later levels below the target fill up to it while earlier levels
+    above it have such jobs to give; the balanced schedule passes the schedule
+    check and the memory plan's check."""
+    import mdinputs
+    import paper_2012_06607_b200 as mdps
+    si = mdinputs.make_config(name)
+    rc, before, after, moved, same, msg = mdps.test_balance(si, min_jobs)
+    assert rc > 0, msg
+    assert same == 1
+    assert sum(before) == sum(after) and len(before) == len(after) == rc
+    assert moved == sum(max(0, a - b) for a, b in zip(after, before))
+    for b, a in zip(before, after):
+        assert a <= max(b, min_jobs)          # a level grows at most to the target
+        assert a >= min(b, min_jobs)          # and gives only what it holds above it
+    if name == "qd" and min_jobs == 1776:
+        assert before[-3:] == [1476, 856, 270] and after[-3:] == [1776, 1776, 1776] and moved == 2726
