@@ -130,3 +130,27 @@ def test_level_balancing_changes_nothing():
         mdps.set_pdl(True)
     assert sum(lv0) == sum(lv1) and len(lv0) == len(lv1)
     assert min(lv1) > min(lv0) and lv1 != lv0
+
+
+@pytest.mark.parametrize("name,mb", [("qd", 48), ("qd", 24)])
+def test_row_chunks_change_nothing(name, mb):
+    """Under a workspace bound (mdps_options.workspace_mb) the rows run in
+    chunks, each its (balanced) levels then its own addition jobs, with the
+    pool slots reused across chunks: the outputs equal the unchunked
+    evaluation's bit for bit."""
+    import torch
+    import paper_2012_06607_b200 as mdps
+    si = mdinputs.make_config(name)
+    x = torch.from_numpy(si.x).cuda()
+    with mdps.System.from_inputs(si) as s:
+        assert s.stats()["chunks"] == 1
+        v, j = s.eval_diff(x)
+        torch.cuda.synchronize()
+        ref = (v.cpu().numpy(), j.cpu().numpy())
+    with mdps.System.from_inputs(si, workspace_mb=mb) as s:
+        st = s.stats()
+        assert st["chunks"] >= 2 and st["workspace_bytes"] <= (mb << 20) * 1.05
+        for _ in range(2):
+            v, j = s.eval_diff(x)
+            torch.cuda.synchronize()
+            assert np.array_equal(v.cpu().numpy(), ref[0]) and np.array_equal(j.cpu().numpy(), ref[1])
